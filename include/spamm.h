@@ -1,0 +1,156 @@
+/*
+ * spamm.h — C ABI of the B200 (sm_100a) SpAMM / Newton-Schulz library
+ * (libspamm_b200.so).  No C++ or torch types cross this boundary.
+ *
+ * Method: Challacombe, Haut & Bock, "A N-Body Solver for Square Root
+ * Iteration", arXiv 1508.05856 (PAPER.md; citations P:<line>):
+ *   - quadtree matrix with Frobenius-norm decorations ............ P:115-129
+ *   - SpAMM product a (x)_tau b, Eq. newspamm; cull iff
+ *     ||a^i|| ||b^i|| < tau ||a|| ||b|| ............................ P:199-216
+ *   - dual-channel Newton-Schulz square-root iteration, Eq.
+ *     cannonical, in the north_star form of BASELINE.json:
+ *     X = Z (x) Y, H = 1/2(3I - X), Y <- Y (x) H, Z <- H (x) Z ..... P:380-389
+ *   - trace error t_k = (n - tr X)/n .............................. P:438-440
+ *
+ * Conventions (all entry points):
+ *   - Return SPAMM_OK (0) or an error code; never throws / exits.  A textual
+ *     reason is available from spamm_last_error(ctx) until the next call.
+ *   - Work is enqueued on the context's CUDA stream.  Calls that return host
+ *     values (spamm_norm, spamm_multiply stats, spamm_ns_sqrt history,
+ *     spamm_export_tasks, spamm_mat_info) synchronise that stream.
+ *   - "Pointer, host or device": the library inspects the pointer with
+ *     cudaPointerGetAttributes; host memory (pageable or pinned) is staged
+ *     through the stream, device memory is read in place.
+ *   - Matrices are square, n = b * 2^L with b in {16, 32, 64}; dense inputs
+ *     are row-major fp64 with leading dimension ld >= n.  A leaf block is
+ *     "present" iff its fp64 sum of squares is > 0 (reading L6);
+ *     absent blocks are exact zeros and never form leaf tasks.
+ *   - spamm_mat handles returned through out-parameters are owned by the
+ *     caller and released with spamm_mat_free (before spamm_ctx_destroy).
+ *   - All device memory comes from the context allocator (the Python layer
+ *     passes PyTorch's caching allocator), else cudaMallocAsync on the stream.
+ */
+#ifndef SPAMM_B200_H
+#define SPAMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct spamm_ctx_s *spamm_ctx;
+typedef struct spamm_mat_s *spamm_mat;
+
+typedef enum {
+    SPAMM_OK = 0,
+    SPAMM_EINVAL = 1,      /* bad argument (negative / non-finite tau, b, iters, NULL) */
+    SPAMM_ESHAPE = 2,      /* operands differ in n or b                                 */
+    SPAMM_ENOMEM = 3,      /* allocator returned NULL                                   */
+    SPAMM_ECUDA = 4,       /* CUDA runtime / launch error                               */
+    SPAMM_ENCCL = 5,       /* reserved (multi-GPU)                                      */
+    SPAMM_ENOTFINITE = 6,  /* non-finite root norm or trace error (history is kept)     */
+    SPAMM_ECAPACITY = 7    /* internal capacity could not be grown                      */
+} spamm_status;
+
+/* Device allocator callbacks (stream-ordered).  alloc returns NULL on failure. */
+typedef struct {
+    void *(*alloc)(size_t bytes, void *stream, void *user);
+    void (*free)(void *ptr, size_t bytes, void *stream, void *user);
+    void *user;
+} spamm_allocator;
+
+/* Per-product counters (filled on request; host memory). */
+typedef struct {
+    int64_t tasks;              /* surviving leaf triples |S| (P:217-218 vol)        */
+    int64_t segments;           /* output blocks (i,j) with >= 1 surviving task      */
+    int64_t candidates;         /* leaf-level candidate triples tested               */
+    int64_t level_survivors[24];/* survivors per quadtree level (index = level)      */
+    double flops;               /* 2 b^3 |S|                                         */
+} spamm_stats;
+
+/* Options of spamm_ns_sqrt (NULL => defaults).  History buffers are HOST memory. */
+typedef struct {
+    double tau_s;           /* sensitive threshold for Y (x) H; < 0 => tau */
+    double mu;              /* relative Tikhonov shift: Y0 = (s/c + mu I)/(1+mu); 0 => none
+                               (reading L13)                       */
+    double scale;           /* > 0 => use as c ~ ||s||_2; else power iteration          */
+    int32_t power_iters;    /* power steps for c (default 100, reading L12)             */
+    double *t_history;      /* [iters] trace errors t_k, nullable                        */
+    spamm_stats *per_product;/* [3*iters] stats of X, Y', Z' per k, nullable             */
+    double *c_out;          /* scale actually used, nullable                             */
+} spamm_ns_opts;
+
+/* ---------------------------------------------------------------- context */
+/* device: CUDA ordinal; cuda_stream: cudaStream_t (NULL = a library-owned stream);
+ * allocator: nullable (=> cudaMallocAsync). */
+spamm_status spamm_ctx_create(int device, void *cuda_stream, const spamm_allocator *allocator,
+                              spamm_ctx *out);
+void spamm_ctx_destroy(spamm_ctx ctx);
+const char *spamm_last_error(spamm_ctx ctx);
+/* number of library kernels launched on this context since creation */
+int64_t spamm_kernel_launches(spamm_ctx ctx);
+
+/* ------------------------------------------------------------ quadtree */
+/* Build the quadtree of a dense n x n row-major matrix (host or device pointer):
+ * leaf norms, Morton-ordered norm pyramid, packed block pool. */
+spamm_status spamm_build_tree(spamm_ctx ctx, const double *dense, int64_t n, int64_t ld,
+                              int32_t b, spamm_mat *out);
+/* Build from a block list: nblocks blocks (bi[t], bj[t]) each b*b row-major at
+ * blocks + t*b*b (host or device pointers; coordinates must be distinct). */
+spamm_status spamm_build_tree_blocks(spamm_ctx ctx, int64_t n, int32_t b, int64_t nblocks,
+                                     const int32_t *bi, const int32_t *bj, const double *blocks,
+                                     spamm_mat *out);
+void spamm_mat_free(spamm_mat m);
+/* n, b, number of stored blocks (syncs). */
+spamm_status spamm_mat_info(spamm_mat m, int64_t *n, int32_t *b, int64_t *nblocks);
+/* Frobenius norm ||m||_F = sqrt(root of the squared-norm pyramid) (syncs). */
+spamm_status spamm_norm(spamm_ctx ctx, spamm_mat m, double *fro);
+/* Dense copy (host or device pointer, ld >= n); absent blocks are written as 0. */
+spamm_status spamm_to_dense(spamm_ctx ctx, spamm_mat m, double *dense, int64_t ld);
+/* Squared Frobenius norms of one pyramid level (0 = root, L = leaves) as a
+ * 2^level x 2^level row-major array (host or device pointer). */
+spamm_status spamm_level_norms2(spamm_ctx ctx, spamm_mat m, int32_t level, double *out);
+/* Gather nreq blocks (bi[t], bj[t]) into out + t*b*b (zeros if absent); present[t]
+ * (nullable) = 1/0.  All pointers host or device. */
+spamm_status spamm_get_blocks(spamm_ctx ctx, spamm_mat m, int64_t nreq, const int32_t *bi,
+                              const int32_t *bj, double *out, int32_t *present);
+
+/* --------------------------------------------------------------- SpAMM */
+/* C = A (x)_tau B (Eq. newspamm): level-by-level two-sided norm query
+ * keeping (i,k,j) iff n2A[i,k]*n2B[k,j] >= tau^2 ||A||^2 ||B||^2 (squared form of
+ * P:205, reading L5), then C_ij = sum_k A_ik B_kj over surviving k (FP64 DMMA).
+ * Errors: ESHAPE (n or b differ), EINVAL (tau < 0 or not finite). */
+spamm_status spamm_multiply(spamm_ctx ctx, spamm_mat A, spamm_mat B, double tau, spamm_mat *C,
+                            spamm_stats *stats /* nullable, host */);
+/* Leaf triples (i,k,j) of the last product on ctx, grouped by output block (i,j)
+ * in Morton order, k ascending; ikj is HOST [3*cap]; *n = total count. */
+spamm_status spamm_export_tasks(spamm_ctx ctx, int32_t *ikj, int64_t cap, int64_t *n);
+
+/* -------------------------------------------------------- Newton-Schulz */
+/* One dual step (north_star form): X = Z (x)_tau Y; t = (n - tr X)/n;
+ * H = 1/2 (3I - X) (fused in the X epilogue, X is never stored);
+ * Y' = Y (x)_tau_s H; Z' = H (x)_tau Z.  H_out nullable (else freed). */
+spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
+                           spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
+                           double *t_k /* host, nullable */, spamm_stats stats[3] /* nullable */);
+/* Scale estimate c ~ ||s||_2: K power steps from 1/sqrt(n) * ones, Rayleigh quotient. */
+spamm_status spamm_power_scale(spamm_ctx ctx, spamm_mat s, int32_t K, double *c);
+/* Y0 = s/c (mu = 0) or (s/c + mu I)/(1+mu). */
+spamm_status spamm_ns_y0(spamm_ctx ctx, spamm_mat s, double c, double mu, spamm_mat *Y0);
+/* Identity quadtree (diagonal blocks = I). */
+spamm_status spamm_identity(spamm_ctx ctx, int64_t n, int32_t b, spamm_mat *I);
+/* Full run: setup (c, Y0 = s/c, Z0 = I), iters dual steps, unscale
+ * (Y * sqrt(c(1+mu)), Z / sqrt(c(1+mu))).  On ENOTFINITE, Y/Z hold the last finite
+ * iterates (unscaled) and t_history is filled up to the failing step. */
+spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, int32_t iters, spamm_mat *Y,
+                           spamm_mat *Z, const spamm_ns_opts *opts);
+/* m * alpha (divide = 0) or m / alpha (divide = 1), new matrix, same pattern. */
+spamm_status spamm_scale(spamm_ctx ctx, spamm_mat m, double alpha, int32_t divide,
+                         spamm_mat *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPAMM_B200_H */

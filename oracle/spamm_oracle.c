@@ -421,7 +421,7 @@ static onode *map_rec(const onode *p, int lev, int L, int b, int I, int J, int o
                       double c, double mu)
 {
     int diag = (I == J);
-    int fill = (op == 4 || op == 5);   /* ops that create absent diagonal blocks */
+    int fill = (op == 1 || op == 4 || op == 5);   /* ops that create absent diagonal blocks */
     if (!p && !(diag && fill)) return NULL;
     if (!p && lev < L && diag && fill) {
         onode *q = new_interior();

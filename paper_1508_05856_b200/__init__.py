@@ -1,0 +1,363 @@
+"""paper_1508_05856_b200 — B200 (sm_100a) SpAMM and dual Newton-Schulz.
+
+Thin ctypes binding over the C ABI of ``libspamm_b200.so`` (``include/spamm.h``).
+Function names are the C names; this module only marshals arguments (torch
+tensors / numpy arrays -> raw pointers, handles -> objects).  Every step of
+the method runs in the library's CUDA kernels.  PyTorch supplies device memory
+(its caching allocator, passed to the library as allocator callbacks) and the
+CUDA stream.  There is no CPU fallback: if the library cannot be loaded, or
+there is no sm_100 device, the calls raise.
+
+Method: Challacombe, Haut & Bock, arXiv 1508.05856 — SpAMM (Eq. newspamm,
+PAPER.md P:199-216) inside the dual-channel Newton-Schulz square-root
+iteration (Eq. cannonical).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _build
+
+__all__ = [
+    "SpammError", "Ctx", "Mat", "load",
+    "spamm_ctx_create", "spamm_ctx_destroy", "spamm_last_error", "spamm_kernel_launches",
+    "spamm_build_tree", "spamm_build_tree_blocks", "spamm_mat_free", "spamm_mat_info",
+    "spamm_norm", "spamm_to_dense", "spamm_level_norms2", "spamm_get_blocks",
+    "spamm_multiply", "spamm_export_tasks", "spamm_ns_step", "spamm_power_scale",
+    "spamm_ns_y0", "spamm_identity", "spamm_ns_sqrt", "spamm_scale",
+]
+
+STATUS = {0: "SPAMM_OK", 1: "SPAMM_EINVAL", 2: "SPAMM_ESHAPE", 3: "SPAMM_ENOMEM",
+          4: "SPAMM_ECUDA", 5: "SPAMM_ENCCL", 6: "SPAMM_ENOTFINITE", 7: "SPAMM_ECAPACITY"}
+
+
+class SpammError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class spamm_stats(C.Structure):
+    _fields_ = [("tasks", C.c_int64), ("segments", C.c_int64), ("candidates", C.c_int64),
+                ("level_survivors", C.c_int64 * 24), ("flops", C.c_double)]
+
+    def as_dict(self):
+        return dict(tasks=self.tasks, segments=self.segments, candidates=self.candidates,
+                    level_survivors=list(self.level_survivors), flops=self.flops)
+
+
+class spamm_ns_opts(C.Structure):
+    _fields_ = [("tau_s", C.c_double), ("mu", C.c_double), ("scale", C.c_double),
+                ("power_iters", C.c_int32), ("t_history", C.c_void_p),
+                ("per_product", C.c_void_p), ("c_out", C.c_void_p)]
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class spamm_allocator(C.Structure):
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("user", C.c_void_p)]
+
+
+_LIB = None
+
+
+def load():
+    """Load (building in-tree first if needed) libspamm_b200.so."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = _build.LIB
+    if not os.path.exists(path):
+        path = _build.build()
+    L = C.CDLL(path)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    sigs = {
+        "spamm_ctx_create": (i32, [C.c_int, vp, P(spamm_allocator), P(vp)]),
+        "spamm_ctx_destroy": (None, [vp]),
+        "spamm_last_error": (C.c_char_p, [vp]),
+        "spamm_kernel_launches": (i64, [vp]),
+        "spamm_build_tree": (i32, [vp, vp, i64, i64, i32, P(vp)]),
+        "spamm_build_tree_blocks": (i32, [vp, i64, i32, i64, vp, vp, vp, P(vp)]),
+        "spamm_mat_free": (None, [vp]),
+        "spamm_mat_info": (i32, [vp, P(i64), P(i32), P(i64)]),
+        "spamm_norm": (i32, [vp, vp, P(dbl)]),
+        "spamm_to_dense": (i32, [vp, vp, vp, i64]),
+        "spamm_level_norms2": (i32, [vp, vp, i32, vp]),
+        "spamm_get_blocks": (i32, [vp, vp, i64, vp, vp, vp, vp]),
+        "spamm_multiply": (i32, [vp, vp, vp, dbl, P(vp), P(spamm_stats)]),
+        "spamm_export_tasks": (i32, [vp, vp, i64, P(i64)]),
+        "spamm_ns_step": (i32, [vp, vp, vp, dbl, dbl, P(vp), P(vp), P(vp), P(dbl), vp]),
+        "spamm_power_scale": (i32, [vp, vp, i32, P(dbl)]),
+        "spamm_ns_y0": (i32, [vp, vp, dbl, dbl, P(vp)]),
+        "spamm_identity": (i32, [vp, i64, i32, P(vp)]),
+        "spamm_ns_sqrt": (i32, [vp, vp, dbl, i32, P(vp), P(vp), P(spamm_ns_opts)]),
+        "spamm_scale": (i32, [vp, vp, dbl, i32, P(vp)]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _LIB = L
+    return L
+
+
+def exported_symbols():
+    """Names declared in include/spamm.h that the binding resolves."""
+    load()
+    return [n for n in __all__ if n.startswith("spamm_")]
+
+
+# --------------------------------------------------------------- marshalling
+def _ptr(x):
+    """Raw pointer of a torch tensor (host or device) or numpy array."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags.c_contiguous
+        return C.c_void_p(x.ctypes.data)
+    assert x.is_contiguous()
+    return C.c_void_p(x.data_ptr())
+
+
+class Ctx:
+    """A library context bound to a CUDA device and (torch's current) stream."""
+
+    def __init__(self, device: int = 0, stream=None, torch_allocator: bool = True):
+        import torch
+        if not torch.cuda.is_available():
+            raise SpammError(4, "no CUDA device: the SpAMM library has no CPU path")
+        L = load()
+        self.torch = torch
+        self.device = device
+        torch.cuda.set_device(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        self._keep = []
+        alloc_p = None
+        if torch_allocator:
+            raw_alloc = torch._C._cuda_cudaCachingAllocator_raw_alloc
+            raw_delete = torch._C._cuda_cudaCachingAllocator_raw_delete
+
+            def _alloc(nbytes, strm, user):
+                try:
+                    return raw_alloc(int(nbytes), strm or 0)
+                except Exception:  # noqa: BLE001 — reported as SPAMM_ENOMEM by the library
+                    return None
+
+            def _free(ptr, nbytes, strm, user):
+                raw_delete(ptr)
+
+            a = spamm_allocator(ALLOC_FN(_alloc), FREE_FN(_free), None)
+            self._keep = [a, _alloc, _free]
+            alloc_p = C.byref(a)
+        h = C.c_void_p()
+        rc = L.spamm_ctx_create(device, C.c_void_p(stream.cuda_stream), alloc_p, C.byref(h))
+        if rc:
+            raise SpammError(rc, "spamm_ctx_create failed (device must be sm_100)")
+        self.h = h
+
+    def check(self, rc):
+        if rc:
+            raise SpammError(rc, load().spamm_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            load().spamm_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class Mat:
+    """Owning handle of a device-resident quadtree matrix."""
+
+    def __init__(self, ctx: Ctx, h):
+        self.ctx = ctx
+        self.h = h
+
+    def free(self):
+        if getattr(self, "h", None) and getattr(self.ctx, "h", None):
+            load().spamm_mat_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def info(self):
+        n, b, nblk = C.c_int64(), C.c_int32(), C.c_int64()
+        self.ctx.check(load().spamm_mat_info(self.h, C.byref(n), C.byref(b), C.byref(nblk)))
+        return n.value, b.value, nblk.value
+
+    @property
+    def n(self):
+        return self.info()[0]
+
+    @property
+    def b(self):
+        return self.info()[1]
+
+    @property
+    def nblocks(self):
+        return self.info()[2]
+
+
+# ------------------------------------------------------------------- calls
+def spamm_ctx_create(device: int = 0, stream=None, torch_allocator: bool = True) -> Ctx:
+    return Ctx(device, stream, torch_allocator)
+
+
+def spamm_ctx_destroy(ctx: Ctx):
+    ctx.close()
+
+
+def spamm_last_error(ctx: Ctx) -> str:
+    return load().spamm_last_error(ctx.h).decode()
+
+
+def spamm_kernel_launches(ctx: Ctx) -> int:
+    return load().spamm_kernel_launches(ctx.h)
+
+
+def spamm_build_tree(ctx: Ctx, dense, b: int) -> Mat:
+    """dense: n x n row-major fp64 torch tensor (cuda or cpu) or numpy array."""
+    n = dense.shape[0]
+    h = C.c_void_p()
+    ctx.check(load().spamm_build_tree(ctx.h, _ptr(dense), n, dense.shape[1], b, C.byref(h)))
+    return Mat(ctx, h)
+
+
+def spamm_build_tree_blocks(ctx: Ctx, n: int, b: int, bi, bj, blocks) -> Mat:
+    h = C.c_void_p()
+    ctx.check(load().spamm_build_tree_blocks(ctx.h, n, b, len(bi), _ptr(bi), _ptr(bj),
+                                             _ptr(blocks), C.byref(h)))
+    return Mat(ctx, h)
+
+
+def spamm_mat_free(m: Mat):
+    m.free()
+
+
+def spamm_mat_info(m: Mat):
+    return m.info()
+
+
+def spamm_norm(ctx: Ctx, m: Mat) -> float:
+    v = C.c_double()
+    ctx.check(load().spamm_norm(ctx.h, m.h, C.byref(v)))
+    return v.value
+
+
+def spamm_to_dense(ctx: Ctx, m: Mat, out=None, device: bool = True):
+    """Dense copy as a torch tensor (device=True) or numpy array."""
+    n = m.n
+    if out is None:
+        if device:
+            out = ctx.torch.empty((n, n), dtype=ctx.torch.float64, device=f"cuda:{ctx.device}")
+        else:
+            out = np.empty((n, n))
+    ctx.check(load().spamm_to_dense(ctx.h, m.h, _ptr(out), out.shape[1]))
+    return out
+
+
+def spamm_level_norms2(ctx: Ctx, m: Mat, level: int) -> np.ndarray:
+    side = 1 << level
+    out = np.empty((side, side))
+    ctx.check(load().spamm_level_norms2(ctx.h, m.h, level, _ptr(out)))
+    return out
+
+
+def spamm_get_blocks(ctx: Ctx, m: Mat, bi, bj):
+    bi = np.ascontiguousarray(bi, dtype=np.int32)
+    bj = np.ascontiguousarray(bj, dtype=np.int32)
+    b = m.b
+    out = np.empty((len(bi), b, b))
+    pres = np.empty(len(bi), dtype=np.int32)
+    ctx.check(load().spamm_get_blocks(ctx.h, m.h, len(bi), _ptr(bi), _ptr(bj), _ptr(out), _ptr(pres)))
+    return out, pres.astype(bool)
+
+
+def spamm_multiply(ctx: Ctx, A: Mat, B: Mat, tau: float, want_stats: bool = False):
+    h = C.c_void_p()
+    st = spamm_stats()
+    ctx.check(load().spamm_multiply(ctx.h, A.h, B.h, float(tau), C.byref(h), C.byref(st)))
+    m = Mat(ctx, h)
+    return (m, st.as_dict()) if want_stats else m
+
+
+def spamm_export_tasks(ctx: Ctx) -> np.ndarray:
+    """Leaf triples (i,k,j) of the last product: [ntasks, 3] int32."""
+    n = C.c_int64()
+    ctx.check(load().spamm_export_tasks(ctx.h, None, 0, C.byref(n)))
+    buf = np.empty(3 * max(n.value, 1), dtype=np.int32)
+    ctx.check(load().spamm_export_tasks(ctx.h, _ptr(buf), n.value, C.byref(n)))
+    return buf[: 3 * n.value].reshape(-1, 3)
+
+
+def spamm_ns_step(ctx: Ctx, Y: Mat, Z: Mat, tau: float, tau_s: float | None = None,
+                  want_h: bool = False):
+    """One dual NS step; returns (Y', Z', t_k, [stats X, Y', Z'] [, H])."""
+    tau_s = tau if tau_s is None else tau_s
+    yn, zn, hn = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    t = C.c_double()
+    sts = (spamm_stats * 3)()
+    ctx.check(load().spamm_ns_step(ctx.h, Y.h, Z.h, float(tau), float(tau_s), C.byref(yn),
+                                   C.byref(zn), C.byref(hn) if want_h else None, C.byref(t), sts))
+    out = (Mat(ctx, yn), Mat(ctx, zn), t.value, [s.as_dict() for s in sts])
+    return out + (Mat(ctx, hn),) if want_h else out
+
+
+def spamm_power_scale(ctx: Ctx, s: Mat, K: int = 100) -> float:
+    c = C.c_double()
+    ctx.check(load().spamm_power_scale(ctx.h, s.h, K, C.byref(c)))
+    return c.value
+
+
+def spamm_ns_y0(ctx: Ctx, s: Mat, c: float, mu: float = 0.0) -> Mat:
+    h = C.c_void_p()
+    ctx.check(load().spamm_ns_y0(ctx.h, s.h, float(c), float(mu), C.byref(h)))
+    return Mat(ctx, h)
+
+
+def spamm_identity(ctx: Ctx, n: int, b: int) -> Mat:
+    h = C.c_void_p()
+    ctx.check(load().spamm_identity(ctx.h, n, b, C.byref(h)))
+    return Mat(ctx, h)
+
+
+def spamm_scale(ctx: Ctx, m: Mat, alpha: float, divide: bool = False) -> Mat:
+    h = C.c_void_p()
+    ctx.check(load().spamm_scale(ctx.h, m.h, float(alpha), int(divide), C.byref(h)))
+    return Mat(ctx, h)
+
+
+def spamm_ns_sqrt(ctx: Ctx, s: Mat, tau: float, iters: int, tau_s: float | None = None,
+                  mu: float = 0.0, scale: float = 0.0, power_iters: int = 100,
+                  want_stats: bool = True):
+    """Full dual NS run: returns dict(Y, Z, t, stats, c)."""
+    t = np.zeros(iters)
+    sts = (spamm_stats * (3 * iters))() if want_stats else None
+    c = C.c_double()
+    o = spamm_ns_opts(-1.0 if tau_s is None else float(tau_s), float(mu), float(scale),
+                      int(power_iters), t.ctypes.data, C.cast(sts, C.c_void_p) if want_stats else None,
+                      C.cast(C.pointer(c), C.c_void_p))
+    yo, zo = C.c_void_p(), C.c_void_p()
+    ctx.check(load().spamm_ns_sqrt(ctx.h, s.h, float(tau), int(iters), C.byref(yo), C.byref(zo),
+                                   C.byref(o)))
+    stats = None
+    if want_stats:
+        stats = [[sts[3 * k + p].as_dict() for p in range(3)] for k in range(iters)]
+    return dict(Y=Mat(ctx, yo), Z=Mat(ctx, zo), t=t, stats=stats, c=c.value)

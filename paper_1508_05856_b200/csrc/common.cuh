@@ -1,0 +1,167 @@
+// common.cuh — internal types and helpers of libspamm_b200 (sm_100a only).
+//
+// HBM layout of one quadtree matrix:
+//   norm2 : fp64 squared-Frobenius pyramid, level l (0 = root .. L = leaves)
+//           at offset pyr_off(l), 4^l entries in Morton order, so the four
+//           children of node m are the 32-byte sector 4m..4m+3 of level l+1
+//           (P:125-129 stored squared, reading L5).
+//   slot  : int32 [nb*nb] Morton order -> pool slot, -1 = absent block.
+//   pool  : fp64 [cap][b*b], each leaf block row-major, 256-B aligned.
+//   coord : int32 [cap] Morton code of the block in each pool slot.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/spamm.h"
+
+#define SPAMM_MAX_L 15
+
+struct spamm_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    spamm_allocator alloc{};
+    bool has_alloc = false;
+    std::string err;
+    int64_t launches = 0;
+    int sm_count = 148;
+    // last product's leaf tasks (for spamm_export_tasks)
+    struct Cull *last = nullptr;
+    // cull workspaces owned by the context (grown on demand), one per product role
+    struct Cull *cw[3] = {nullptr, nullptr, nullptr};
+    double *dscratch = nullptr;   // small device scratch (norms, trace, t)
+    int64_t *iscratch = nullptr;  // small device scratch (counters)
+    double *hpinned = nullptr;    // pinned host scratch
+};
+
+struct spamm_mat_s {
+    spamm_ctx ctx = nullptr;
+    int64_t n = 0;
+    int b = 0, nb = 0, L = 0;
+    double *norm2 = nullptr;   // pyramid
+    int32_t *slot = nullptr;   // nb*nb Morton
+    double *pool = nullptr;    // cap * b*b
+    int32_t *coord = nullptr;  // cap
+    int64_t nblk = 0, cap = 0;
+};
+
+// ------------------------------------------------------------------ memory
+void *dev_alloc(spamm_ctx ctx, size_t bytes);
+void dev_free(spamm_ctx ctx, void *p, size_t bytes);
+
+template <typename T>
+static inline T *dalloc(spamm_ctx ctx, int64_t count)
+{
+    return (T *)dev_alloc(ctx, sizeof(T) * (size_t)(count > 0 ? count : 1));
+}
+
+// Pyramid level offsets, padded so every level starts on a 32-byte sector:
+// off(0) = 0 (root, padded to 4 entries), off(l) = (4^l + 8)/3 for l >= 1.
+__host__ __device__ static inline int64_t pyr_off(int l)
+{
+    return l == 0 ? 0 : ((int64_t(1) << (2 * l)) + 8) / 3;
+}
+__host__ __device__ static inline int64_t pyr_size(int L)
+{
+    return L == 0 ? 4 : pyr_off(L) + (int64_t(1) << (2 * L));
+}
+
+// ------------------------------------------------------------------ Morton
+__host__ __device__ static inline uint32_t spread_bits(uint32_t x)
+{
+    x &= 0xFFFF;
+    x = (x | (x << 8)) & 0x00FF00FF;
+    x = (x | (x << 4)) & 0x0F0F0F0F;
+    x = (x | (x << 2)) & 0x33333333;
+    x = (x | (x << 1)) & 0x55555555;
+    return x;
+}
+__host__ __device__ static inline uint32_t compact_bits(uint32_t x)
+{
+    x &= 0x55555555;
+    x = (x | (x >> 1)) & 0x33333333;
+    x = (x | (x >> 2)) & 0x0F0F0F0F;
+    x = (x | (x >> 4)) & 0x00FF00FF;
+    x = (x | (x >> 8)) & 0x0000FFFF;
+    return x;
+}
+// row index i in the odd bits, column j in the even bits: children of m are 4m + (di<<1|dj)
+__host__ __device__ static inline uint32_t morton(uint32_t i, uint32_t j)
+{
+    return (spread_bits(i) << 1) | spread_bits(j);
+}
+__host__ __device__ static inline uint32_t morton_i(uint32_t m) { return compact_bits(m >> 1); }
+__host__ __device__ static inline uint32_t morton_j(uint32_t m) { return compact_bits(m); }
+
+// ------------------------------------------------------------------ errors
+spamm_status set_err(spamm_ctx ctx, spamm_status st, const char *fmt, ...);
+spamm_status check_cuda(spamm_ctx ctx, cudaError_t e, const char *what);
+#define CK(call)                                                              \
+    do {                                                                      \
+        cudaError_t _e = (call);                                              \
+        if (_e != cudaSuccess) return check_cuda(ctx, _e, #call);             \
+    } while (0)
+#define CKL(ctx)                                                              \
+    do {                                                                      \
+        (ctx)->launches++;                                                    \
+        cudaError_t _e = cudaGetLastError();                                  \
+        if (_e != cudaSuccess) return check_cuda(ctx, _e, "kernel launch");   \
+    } while (0)
+#define ST(call)                                                              \
+    do {                                                                      \
+        spamm_status _s = (call);                                             \
+        if (_s != SPAMM_OK) return _s;                                        \
+    } while (0)
+
+static inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ------------------------------------------------------------ internal API
+// tree.cu
+spamm_status mat_new(spamm_ctx ctx, int64_t n, int b, int64_t cap, spamm_mat *out);
+spamm_status mat_reset_pattern(spamm_ctx ctx, spamm_mat m);     // slot=-1, leaf norms=0
+spamm_status pyramid_build(spamm_ctx ctx, spamm_mat m);           // levels L-1..0 from leaves
+spamm_status mat_map(spamm_ctx ctx, spamm_mat src, int op, double c, double mu, spamm_mat *out);
+spamm_status leaf_norms_from_pool(spamm_ctx ctx, spamm_mat m);  // recompute leaf norm2 from pool
+int is_device_ptr(const void *p);
+
+// cull.cu — the level-by-level two-sided norm query (Eq. newspamm)
+enum { CNT_OVERFLOW = 16, CNT_NSEG = 17, CNT_TICKET = 20 };  // counters[] layout; [0..15] = level counts
+struct Cull {
+    int64_t cap = 0;              // task capacity of every level
+    int64_t cap_segs = 0;         // segment capacity
+    int4 *rec[2] = {nullptr, nullptr};  // ping-pong level records {code(I,J), K, gstart, gend}
+    int4 *pre = nullptr;          // per-task exclusive scan of child counts per quadrant [cap+1]
+    uint8_t *mask = nullptr;      // per-task 8-bit child mask, bit (2q + dk)
+    int32_t *tA = nullptr, *tB = nullptr, *tK = nullptr;  // final tasks: A slot, B slot, k
+    int32_t *seg_code = nullptr, *seg_start = nullptr, *seg_len = nullptr;
+    int64_t tiles = 0;            // tiles per scan
+    int32_t *tile_flag = nullptr; // [(SPAMM_MAX_L + 2) * tiles]
+    int4 *tile_agg = nullptr, *tile_pre = nullptr;  // [tiles]
+    int32_t *counters = nullptr;  // [64] device
+    int32_t *hcnt = nullptr;      // [64] pinned host mirror
+    int final_buf = 0;            // rec[] index holding the leaf-level records
+    int L = 0, l0 = 0, b = 0;
+    int64_t ntasks = 0, nsegs = 0;  // host copies after cull_sync
+    int64_t hint = 0;             // capacity hint for the next use
+    spamm_stats stats{};
+};
+// Enqueue the query, synchronise once to read the counts, and grow + re-run
+// on capacity overflow.
+spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau);
+void cull_free(spamm_ctx ctx, Cull *cw);
+spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj_host, int64_t cap, int64_t *n);
+
+// gemm.cu — FP64 DMMA leaf GEMM with fused epilogues
+enum { EPI_STORE = 0, EPI_NS_H = 1 };
+spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_mat C, int epi,
+                      double *trace_part);
+spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg);
+// append value*I blocks for absent diagonal positions at slots base..; *added = count (syncs)
+spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value, int64_t *added);
+spamm_status trace_finish(spamm_ctx ctx, const double *trace_part, int nb, int64_t n,
+                          double *t_out);
+
+// power.cu
+spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host);

@@ -1,0 +1,435 @@
+// cull.cu — the SpAMM occlusion-cull as a level-by-level two-sided metric query.
+//
+// PAPER.md Eq. newspamm culls a sub-volume (i,k,j) of the product
+// tensor when ||a^i|| ||b^i|| < tau ||a|| ||b||; "two-sided metric query"
+// (P:329-330).  Because a child's norm never exceeds its parent's, the
+// recursion returns exactly the flat leaf set
+//     S = {(i,k,j) : n2A[i,k] * n2B[k,j] >= T},  T = tau^2 ||A||^2 ||B||^2
+// (squared form, reading L5; absent blocks, n2 = 0, never form tasks: L3/L6).
+// The GPU walks the levels breadth-first:
+//   k_cull_init     level l0 = min(L,4): all 8^l0 triples in one CTA (dense start)
+//   k_cull_scan     per parent task: 8-bit child mask (2 pyramid sectors read),
+//                   per-quadrant child counts, single-pass decoupled look-back
+//                   scan (int4) -> exclusive prefixes
+//   k_cull_scatter  order-preserving compaction: children of parent group (I,J)
+//                   are emitted per quadrant q = (di,dj) in (K, dk) order, so the
+//                   list stays sorted by (Morton(i,j), k) with no sort; at the
+//                   leaf level the groups are the output segments and tasks
+//                   carry their A / B pool slots.
+//   k_cull_segments compaction of segment heads -> {code, start, len}.
+// Counts live in device memory; kernels are persistent / grid-stride, so the
+// whole query is enqueued with no host round trip.
+#include "common.cuh"
+#include "scan.cuh"
+
+constexpr int CT = 512;  // scan tile = threads per CTA (one task per thread)
+
+struct CullArgs {
+    const double *a_n2, *b_n2;   // pyramids
+    const int32_t *a_slot, *b_slot;
+    double tau;
+    int64_t cap;
+};
+
+__device__ __forceinline__ double cull_T(const CullArgs &g)
+{
+    // T = tau^2 * ||A||^2 * ||B||^2, evaluated left to right (same on every kernel)
+    return ((g.tau * g.tau) * g.a_n2[0]) * g.b_n2[0];
+}
+
+__device__ __forceinline__ bool keep(double pa, double pb, double T)
+{
+    // strict '<' culls: survive iff pa*pb >= T; absent blocks never survive
+    return pa > 0.0 && pb > 0.0 && pa * pb >= T;
+}
+
+__device__ __forceinline__ int clamp_n(const int32_t *cnt, int l, int64_t cap)
+{
+    int v = cnt[l];
+    return v < cap ? v : (int)cap;
+}
+
+// ---------------------------------------------------------------- init
+// One CTA of 1024 threads; 8^l0 <= 4096 candidates, 4 per thread, ordered
+// (Morton(I,J), K).  Writes level-l0 records and counters[l0].
+__global__ void __launch_bounds__(1024) k_cull_init(CullArgs g, int l0, int4 *rec, int32_t *cnt)
+{
+    __shared__ int sw[32];
+    __shared__ int spre[4097];
+    const int S = 1 << l0;
+    const int C = S * S * S;
+    const double T = cull_T(g);
+    const double *an = g.a_n2 + pyr_off(l0), *bn = g.b_n2 + pyr_off(l0);
+    bool f[4];
+    int mycount = 0;
+    for (int e = 0; e < 4; e++) {
+        int idx = threadIdx.x * 4 + e;
+        f[e] = false;
+        if (idx < C) {
+            uint32_t code = idx / S;
+            int K = idx % S;
+            int I = morton_i(code), J = morton_j(code);
+            f[e] = keep(an[morton(I, K)], bn[morton(K, J)], T);
+        }
+        mycount += f[e];
+    }
+    // block exclusive scan of mycount
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int inc = mycount;
+    for (int d = 1; d < 32; d <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) sw[warp] = inc;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+    for (int w = 0; w < 32; w++) {
+        if (w < warp) wpre += sw[w];
+        tot += sw[w];
+    }
+    int ex = wpre + inc - mycount;
+    int run = ex;
+    for (int e = 0; e < 4; e++) {
+        int idx = threadIdx.x * 4 + e;
+        if (idx <= C) spre[idx] = run;
+        run += f[e];
+    }
+    if (threadIdx.x == 0) spre[C] = tot;
+    __syncthreads();
+    run = ex;
+    for (int e = 0; e < 4; e++) {
+        int idx = threadIdx.x * 4 + e;
+        if (f[e]) {
+            int code = idx / S;
+            int gs = spre[code * S], ge = spre[(code + 1) * S];
+            if (run < g.cap) rec[run] = make_int4(code, idx % S, gs, ge);
+            run++;
+        }
+    }
+    if (threadIdx.x == 0) {
+        cnt[l0] = tot;
+        if (tot > g.cap) cnt[CNT_OVERFLOW] = 1;
+    }
+}
+
+// ------------------------------------------------------- level mask + scan
+// Parent task t at level l -> 8 children at level l+1.  child (di,dk,dj):
+//   pa = n2A_{l+1}[4*Morton(I,K) + (di<<1|dk)],  pb = n2B_{l+1}[4*Morton(K,J) + (dk<<1|dj)]
+// mask bit (2q + dk), q = (di<<1|dj).
+__global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 *rec,
+                                                  uint8_t *mask, int4 *pre, ScanTiles<int4> st,
+                                                  int32_t *cnt)
+{
+    __shared__ int4 sw[CT / 32];
+    __shared__ int s_tile;
+    __shared__ int4 s_excl;
+    const int n = clamp_n(cnt, l, g.cap);
+    const double T = cull_T(g);
+    const double *an = g.a_n2 + pyr_off(l + 1), *bn = g.b_n2 + pyr_off(l + 1);
+    int tile;
+    while ((tile = next_tile(st.ticket, n, CT, &s_tile)) >= 0) {
+        int t = tile * CT + threadIdx.x;
+        int4 c = make_int4(0, 0, 0, 0);
+        uint32_t m = 0;
+        if (t < n) {
+            int4 r = rec[t];
+            uint32_t code = r.x;
+            int K = r.y, I = morton_i(code), J = morton_j(code);
+            const double2 *pa2 = reinterpret_cast<const double2 *>(an + 4 * (int64_t)morton(I, K));
+            const double2 *pb2 = reinterpret_cast<const double2 *>(bn + 4 * (int64_t)morton(K, J));
+            double2 a01 = __ldg(pa2), a23 = __ldg(pa2 + 1), b01 = __ldg(pb2), b23 = __ldg(pb2 + 1);
+            double pa[2][2] = {{a01.x, a01.y}, {a23.x, a23.y}};  // [di][dk]
+            double pb[2][2] = {{b01.x, b01.y}, {b23.x, b23.y}};  // [dk][dj]
+#pragma unroll
+            for (int di = 0; di < 2; di++)
+#pragma unroll
+                for (int dj = 0; dj < 2; dj++)
+#pragma unroll
+                    for (int dk = 0; dk < 2; dk++)
+                        if (keep(pa[di][dk], pb[dk][dj], T)) m |= 1u << (2 * ((di << 1) | dj) + dk);
+            c = make_int4(__popc(m & 3u), __popc((m >> 2) & 3u), __popc((m >> 4) & 3u),
+                          __popc((m >> 6) & 3u));
+            mask[t] = (uint8_t)m;
+        }
+        int4 tot;
+        int4 ex = block_excl_scan<int4, CT>(c, &tot, sw);
+        if (threadIdx.x == 0) s_excl = tile_lookback(st, tile, tot);
+        __syncthreads();
+        int4 p = vadd(s_excl, ex);
+        if (t < n) pre[t] = p;
+        if (t == n - 1) {
+            int4 e = vadd(p, c);
+            pre[n] = e;
+            int total = e.x + e.y + e.z + e.w;
+            cnt[l + 1] = total;
+            if (total > g.cap) cnt[CNT_OVERFLOW] = 1;
+        }
+        __syncthreads();
+    }
+    if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+        pre[0] = make_int4(0, 0, 0, 0);
+        cnt[l + 1] = 0;
+    }
+}
+
+__device__ __forceinline__ int comp(int4 v, int q) { return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w; }
+
+// ------------------------------------------------------------- scatter
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const int4 *rec,
+                                                      const uint8_t *mask, const int4 *pre,
+                                                      int4 *rec_out, int32_t *tA, int32_t *tB,
+                                                      int32_t *tK, const int32_t *cnt)
+{
+    const int n = clamp_n(cnt, l, g.cap);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        uint32_t m = mask[t];
+        if (!m) continue;
+        int4 r = rec[t];
+        int4 P = pre[t], Ps = pre[r.z], Pe = pre[r.w];
+        int base = Ps.x + Ps.y + Ps.z + Ps.w;  // children of all earlier groups
+        uint32_t code = r.x;
+        int K = r.y;
+        int I = morton_i(code), J = morton_j(code);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            int cq = comp(Pe, q) - comp(Ps, q);
+            uint32_t mq = (m >> (2 * q)) & 3u;
+            if (mq) {
+                int gs = base, ge = base + cq;
+                int pos = base + comp(P, q) - comp(Ps, q);
+#pragma unroll
+                for (int dk = 0; dk < 2; dk++) {
+                    if (mq & (1u << dk)) {
+                        if (pos < g.cap) {
+                            uint32_t ccode = 4 * code + q;
+                            int ck = 2 * K + dk;
+                            rec_out[pos] = make_int4((int)ccode, ck, gs, ge);
+                            if (FINAL) {
+                                int i = 2 * I + (q >> 1), j = 2 * J + (q & 1);
+                                tA[pos] = g.a_slot[morton(i, ck)];
+                                tB[pos] = g.b_slot[morton(ck, j)];
+                                tK[pos] = ck;
+                            }
+                        }
+                        pos++;
+                    }
+                }
+            }
+            base += cq;
+        }
+    }
+}
+
+// Final records -> segments when the init level is already the leaf level.
+__global__ void k_cull_leaf_direct(CullArgs g, int l, const int4 *rec, int32_t *tA, int32_t *tB,
+                                   int32_t *tK, const int32_t *cnt)
+{
+    const int n = clamp_n(cnt, l, g.cap);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        int4 r = rec[t];
+        int i = morton_i(r.x), j = morton_j(r.x), k = r.y;
+        tA[t] = g.a_slot[morton(i, k)];
+        tB[t] = g.b_slot[morton(k, j)];
+        tK[t] = k;
+    }
+}
+
+// --------------------------------------------------------- segment heads
+__global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, int64_t cap,
+                                                      int64_t cap_segs, ScanTiles<V1> st,
+                                                      int32_t *seg_code, int32_t *seg_start,
+                                                      int32_t *seg_len, int32_t *cnt)
+{
+    __shared__ V1 sw[CT / 32];
+    __shared__ int s_tile, s_excl;
+    const int n = clamp_n(cnt, L, cap);
+    int tile;
+    while ((tile = next_tile(st.ticket, n, CT, &s_tile)) >= 0) {
+        int t = tile * CT + threadIdx.x;
+        int4 r = make_int4(0, 0, -1, 0);
+        if (t < n) r = rec[t];
+        V1 h{(t < n && r.z == t) ? 1 : 0};
+        V1 tot;
+        V1 ex = block_excl_scan<V1, CT>(h, &tot, sw);
+        if (threadIdx.x == 0) s_excl = tile_lookback(st, tile, tot).x;
+        __syncthreads();
+        int s = s_excl + ex.x;
+        if (h.x && s < cap_segs) {
+            seg_code[s] = r.x;
+            seg_start[s] = t;
+            seg_len[s] = r.w - r.z;
+        }
+        if (t == n - 1) {
+            cnt[CNT_NSEG] = s + h.x;
+            if (s + h.x > cap_segs) cnt[CNT_OVERFLOW] = 1;
+        }
+        __syncthreads();
+    }
+    if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) cnt[CNT_NSEG] = 0;
+}
+
+// ------------------------------------------------------------- host side
+void cull_free(spamm_ctx ctx, Cull *cw)
+{
+    if (!cw) return;
+    int64_t cap = cw->cap, cs = cw->cap_segs, tiles = cw->tiles;
+    dev_free(ctx, cw->rec[0], sizeof(int4) * cap);
+    dev_free(ctx, cw->rec[1], sizeof(int4) * cap);
+    dev_free(ctx, cw->pre, sizeof(int4) * (cap + 1));
+    dev_free(ctx, cw->mask, cap);
+    dev_free(ctx, cw->tA, sizeof(int32_t) * cap);
+    dev_free(ctx, cw->tB, sizeof(int32_t) * cap);
+    dev_free(ctx, cw->tK, sizeof(int32_t) * cap);
+    dev_free(ctx, cw->seg_code, sizeof(int32_t) * cs);
+    dev_free(ctx, cw->seg_start, sizeof(int32_t) * cs);
+    dev_free(ctx, cw->seg_len, sizeof(int32_t) * cs);
+    dev_free(ctx, cw->tile_flag, sizeof(int32_t) * (SPAMM_MAX_L + 2) * tiles);
+    dev_free(ctx, cw->tile_agg, sizeof(int4) * tiles);
+    dev_free(ctx, cw->tile_pre, sizeof(int4) * tiles);
+    cw->rec[0] = cw->rec[1] = cw->pre = cw->tile_agg = cw->tile_pre = nullptr;
+    cw->mask = nullptr;
+    cw->tA = cw->tB = cw->tK = cw->seg_code = cw->seg_start = cw->seg_len = cw->tile_flag = nullptr;
+    cw->cap = cw->cap_segs = cw->tiles = 0;
+}
+
+static spamm_status cull_alloc(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap_segs)
+{
+    cull_free(ctx, cw);
+    cw->cap = cap;
+    cw->cap_segs = cap_segs;
+    cw->tiles = cdiv(cap + 1, CT);
+    cw->rec[0] = dalloc<int4>(ctx, cap);
+    cw->rec[1] = dalloc<int4>(ctx, cap);
+    cw->pre = dalloc<int4>(ctx, cap + 1);
+    cw->mask = dalloc<uint8_t>(ctx, cap);
+    cw->tA = dalloc<int32_t>(ctx, cap);
+    cw->tB = dalloc<int32_t>(ctx, cap);
+    cw->tK = dalloc<int32_t>(ctx, cap);
+    cw->seg_code = dalloc<int32_t>(ctx, cap_segs);
+    cw->seg_start = dalloc<int32_t>(ctx, cap_segs);
+    cw->seg_len = dalloc<int32_t>(ctx, cap_segs);
+    cw->tile_flag = dalloc<int32_t>(ctx, (SPAMM_MAX_L + 2) * cw->tiles);
+    cw->tile_agg = dalloc<int4>(ctx, cw->tiles);
+    cw->tile_pre = dalloc<int4>(ctx, cw->tiles);
+    if (!cw->counters) {
+        cw->counters = dalloc<int32_t>(ctx, 64);
+        if (cudaMallocHost(&cw->hcnt, sizeof(int32_t) * 64) != cudaSuccess) cw->hcnt = nullptr;
+    }
+    if (!cw->rec[0] || !cw->rec[1] || !cw->pre || !cw->mask || !cw->tA || !cw->tB || !cw->tK ||
+        !cw->seg_code || !cw->seg_start || !cw->seg_len || !cw->tile_flag || !cw->tile_agg ||
+        !cw->tile_pre || !cw->counters || !cw->hcnt)
+        return set_err(ctx, SPAMM_ENOMEM, "cull workspace (%lld tasks)", (long long)cap);
+    return SPAMM_OK;
+}
+
+// Enqueue the whole query (no host sync).
+static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau)
+{
+    const int L = A->L;
+    const int l0 = L < 4 ? L : 4;
+    cw->L = L;
+    cw->l0 = l0;
+    cw->b = A->b;
+    CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap};
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemsetAsync(cw->counters, 0, sizeof(int32_t) * 64, s));
+    CK(cudaMemsetAsync(cw->tile_flag, 0, sizeof(int32_t) * (SPAMM_MAX_L + 2) * cw->tiles, s));
+    int cur = 0;
+    k_cull_init<<<1, 1024, 0, s>>>(g, l0, cw->rec[cur], cw->counters);
+    CKL(ctx);
+    const int persist = 2 * ctx->sm_count;
+    int grid_scan = cw->tiles < persist ? (int)cw->tiles : persist;
+    int grid_sc = cdiv(cw->cap, 256);
+    if (grid_sc > 4 * ctx->sm_count) grid_sc = 4 * ctx->sm_count;
+    for (int l = l0; l < L; l++) {
+        ScanTiles<int4> st{cw->tile_flag + (int64_t)(l - l0) * cw->tiles, cw->tile_agg, cw->tile_pre,
+                           cw->counters + CNT_TICKET + l};
+        k_cull_scan<<<grid_scan, CT, 0, s>>>(g, l, cw->rec[cur], cw->mask, cw->pre, st, cw->counters);
+        CKL(ctx);
+        if (l + 1 == L)
+            k_cull_scatter<true><<<grid_sc, 256, 0, s>>>(g, l, cw->rec[cur], cw->mask, cw->pre,
+                                                         cw->rec[cur ^ 1], cw->tA, cw->tB, cw->tK,
+                                                         cw->counters);
+        else
+            k_cull_scatter<false><<<grid_sc, 256, 0, s>>>(g, l, cw->rec[cur], cw->mask, cw->pre,
+                                                          cw->rec[cur ^ 1], nullptr, nullptr, nullptr,
+                                                          cw->counters);
+        CKL(ctx);
+        cur ^= 1;
+    }
+    if (l0 == L) {
+        k_cull_leaf_direct<<<grid_sc, 256, 0, s>>>(g, L, cw->rec[cur], cw->tA, cw->tB, cw->tK,
+                                                   cw->counters);
+        CKL(ctx);
+    }
+    cw->final_buf = cur;
+    ScanTiles<V1> st{cw->tile_flag + (int64_t)(SPAMM_MAX_L + 1) * cw->tiles, (V1 *)cw->tile_agg,
+                     (V1 *)cw->tile_pre, cw->counters + CNT_TICKET + SPAMM_MAX_L + 1};
+    k_cull_segments<<<grid_scan, CT, 0, s>>>(cw->rec[cur], L, cw->cap, cw->cap_segs, st, cw->seg_code,
+                                             cw->seg_start, cw->seg_len, cw->counters);
+    CKL(ctx);
+    return SPAMM_OK;
+}
+
+spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau)
+{
+    int64_t nb = A->nb;
+    int64_t want = cw->hint > 0 ? cw->hint : (int64_t)1 << 16;
+    if (want > cw->cap || cw->cap_segs < nb * nb || !cw->tA) {
+        int64_t cap = want > cw->cap ? want : cw->cap;
+        ST(cull_alloc(ctx, cw, cap, nb * nb));
+    }
+    for (int attempt = 0; attempt < 8; attempt++) {
+        ST(cull_enqueue(ctx, cw, A, B, tau));
+        CK(cudaMemcpyAsync(cw->hcnt, cw->counters, sizeof(int32_t) * 64, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (!cw->hcnt[CNT_OVERFLOW]) {
+            cw->ntasks = cw->hcnt[cw->L];
+            cw->nsegs = cw->hcnt[CNT_NSEG];
+            spamm_stats &s = cw->stats;
+            s = spamm_stats{};
+            s.tasks = cw->ntasks;
+            s.segments = cw->nsegs;
+            for (int l = cw->l0; l <= cw->L && l < 24; l++) s.level_survivors[l] = cw->hcnt[l];
+            s.candidates = cw->L > cw->l0 ? 8 * (int64_t)cw->hcnt[cw->L - 1]
+                                          : ((int64_t)1 << (3 * cw->L));
+            s.flops = 2.0 * (double)cw->b * cw->b * cw->b * (double)cw->ntasks;
+            // next capacity hint: 25% headroom over the largest level seen
+            int64_t mx = 0;
+            for (int l = cw->l0; l <= cw->L; l++) mx = cw->hcnt[l] > mx ? cw->hcnt[l] : mx;
+            int64_t h = mx + mx / 4 + 1024;
+            if (h > cw->hint) cw->hint = h;
+            ctx->last = cw;
+            return SPAMM_OK;
+        }
+        // grow: the largest count seen (the first overflowing level) times 2
+        int64_t mx = cw->cap;
+        for (int l = cw->l0; l <= cw->L; l++) mx = cw->hcnt[l] > mx ? cw->hcnt[l] : mx;
+        int64_t cap = 2 * mx;
+        if (cap > ((int64_t)1 << 30)) return set_err(ctx, SPAMM_ECAPACITY, "cull capacity > 2^30 tasks");
+        ST(cull_alloc(ctx, cw, cap, nb * nb));
+        cw->hint = cap;
+    }
+    return set_err(ctx, SPAMM_ECAPACITY, "cull capacity did not converge");
+}
+
+spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj, int64_t cap, int64_t *n)
+{
+    *n = cw->ntasks;
+    int64_t m = cw->ntasks < cap ? cw->ntasks : cap;
+    if (m <= 0) return SPAMM_OK;
+    int4 *h = nullptr;
+    CK(cudaMallocHost(&h, sizeof(int4) * m));
+    CK(cudaMemcpyAsync(h, cw->rec[cw->final_buf], sizeof(int4) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int64_t t = 0; t < m; t++) {
+        uint32_t code = h[t].x;
+        ikj[3 * t + 0] = (int32_t)morton_i(code);
+        ikj[3 * t + 1] = h[t].y;
+        ikj[3 * t + 2] = (int32_t)morton_j(code);
+    }
+    cudaFreeHost(h);
+    return SPAMM_OK;
+}

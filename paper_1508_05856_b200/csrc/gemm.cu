@@ -1,0 +1,319 @@
+// gemm.cu — the batched leaf-block GEMM of SpAMM on FP64 tensor cores (sm_100a).
+//
+// For every output segment (i,j) produced by the cull (tasks sorted by k):
+//     C_ij = sum_{k in S_ij} A_ik . B_kj            (Eq. newspamm leaf)
+// accumulated in registers in ascending k (segmented in-register reduction, no
+// atomics), with fused epilogues:
+//   EPI_STORE : C_ij -> pool, ||C_ij||^2 -> leaf level of the norm pyramid
+//   EPI_NS_H  : H_ij = 1/2 (3 delta_ij I - X_ij) (alpha = 1) -> pool,
+//               ||H_ij||^2, and tr(X_ii) partials for t_k;
+//               X itself is never stored.
+// FP64 MMA on sm_100a is warp-level mma.sync m8n8k4 (SASS DMMA.8x8x4); tcgen05
+// has no f64 kind, so operands go shared memory -> registers.  Tiles are staged
+// by a multi-stage cp.async pipeline into a 128-byte XOR swizzle
+// (chunk' = chunk ^ (row & 7)) which makes both fragment patterns conflict-free:
+//   A: lane (g,t) reads A[g][4t..4t+3] (2 x LDS.128) — the contraction index is
+//      permuted inside each 16-wide k chunk as k = 4t + s (same permutation on
+//      B's rows, so the product is unchanged);
+//   B: lane (g,t) reads B[4t+s][g] (LDS.64).
+#include "common.cuh"
+#include "scan.cuh"
+
+struct GemmArgs {
+    const double *a_pool, *b_pool;
+    const int32_t *tA, *tB;
+    const int32_t *seg_code, *seg_start, *seg_len;
+    int nseg;
+    double *c_pool;
+    int32_t *c_coord, *c_slot;
+    double *c_leaf_n2;
+    double *trace_part;
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// swizzled double offset of element (r, c) in a B x B row-major tile
+template <int B>
+__device__ __forceinline__ int swz(int r, int c)
+{
+    return r * B + ((((c >> 1) ^ (r & 7))) << 1) + (c & 1);
+}
+
+template <int B, int NT>
+__device__ __forceinline__ void load_tile(double *dst, const double *src)
+{
+    constexpr int CH = B * B / 2;   // 16-byte chunks
+    constexpr int HALF = B / 2;     // chunks per row
+#pragma unroll
+    for (int q = threadIdx.x; q < CH; q += NT) {
+        int r = q / HALF, c = q % HALF;
+        cp_async16(dst + r * B + ((c ^ (r & 7)) << 1), src + 2 * q);
+    }
+}
+
+template <int B, int WM, int WN, int STAGES, int EPI>
+__global__ void __launch_bounds__(32 * WM * WN) k_leaf_gemm(GemmArgs g)
+{
+    constexpr int NT = 32 * WM * WN;
+    constexpr int TM = B / WM, TN = B / WN;
+    constexpr int MF = TM / 8, NF = TN / 8;
+    constexpr int TILE = B * B;
+    extern __shared__ __align__(128) double smem[];
+    __shared__ double s_red[2][NT / 32];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int m0 = (warp / WN) * TM, n0 = (warp % WN) * TN;
+
+    for (int seg = blockIdx.x; seg < g.nseg; seg += gridDim.x) {
+        const int start = g.seg_start[seg], len = g.seg_len[seg];
+        const uint32_t code = g.seg_code[seg];
+
+        double acc[MF][NF][2];
+#pragma unroll
+        for (int i = 0; i < MF; i++)
+#pragma unroll
+            for (int j = 0; j < NF; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+        // prologue
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; s++) {
+            if (s < len) {
+                int ta = g.tA[start + s], tb = g.tB[start + s];
+                load_tile<B, NT>(smem + (2 * s) * TILE, g.a_pool + (int64_t)ta * TILE);
+                load_tile<B, NT>(smem + (2 * s + 1) * TILE, g.b_pool + (int64_t)tb * TILE);
+            }
+            cp_async_commit();
+        }
+        for (int it = 0; it < len; it++) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            {
+                int nx = it + STAGES - 1;
+                if (nx < len) {
+                    int st = nx % STAGES;
+                    int ta = g.tA[start + nx], tb = g.tB[start + nx];
+                    load_tile<B, NT>(smem + (2 * st) * TILE, g.a_pool + (int64_t)ta * TILE);
+                    load_tile<B, NT>(smem + (2 * st + 1) * TILE, g.b_pool + (int64_t)tb * TILE);
+                }
+                cp_async_commit();
+            }
+            const double *As = smem + (2 * (it % STAGES)) * TILE;
+            const double *Bs = As + TILE;
+#pragma unroll
+            for (int kc = 0; kc < B / 16; kc++) {
+                double a[MF][4], bf[NF][4];
+#pragma unroll
+                for (int mf = 0; mf < MF; mf++) {
+                    int r = m0 + 8 * mf + g8;
+                    int c = 8 * kc + 2 * t4;
+                    double2 v0 = *reinterpret_cast<const double2 *>(As + r * B + ((c ^ (r & 7)) << 1));
+                    double2 v1 = *reinterpret_cast<const double2 *>(As + r * B + (((c + 1) ^ (r & 7)) << 1));
+                    a[mf][0] = v0.x; a[mf][1] = v0.y; a[mf][2] = v1.x; a[mf][3] = v1.y;
+                }
+#pragma unroll
+                for (int nf = 0; nf < NF; nf++) {
+                    int col = n0 + 8 * nf + g8;
+#pragma unroll
+                    for (int s = 0; s < 4; s++) bf[nf][s] = Bs[swz<B>(16 * kc + 4 * t4 + s, col)];
+                }
+#pragma unroll
+                for (int s = 0; s < 4; s++)
+#pragma unroll
+                    for (int mf = 0; mf < MF; mf++)
+#pragma unroll
+                        for (int nf = 0; nf < NF; nf++)
+                            dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s], bf[nf][s]);
+            }
+        }
+        cp_async_wait<0>();
+
+        // ------------------------------------------------------ epilogue
+        const int I = morton_i(code), J = morton_j(code);
+        const bool diag = (I == J);
+        double *dst = g.c_pool + (int64_t)seg * TILE;
+        double ss = 0.0, tr = 0.0;
+#pragma unroll
+        for (int mf = 0; mf < MF; mf++)
+#pragma unroll
+            for (int nf = 0; nf < NF; nf++) {
+                int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
+                double y0 = acc[mf][nf][0], y1 = acc[mf][nf][1];
+                if (EPI == EPI_NS_H) {
+                    double d0 = (diag && r == c) ? 1.5 : 0.0, d1 = (diag && r == c + 1) ? 1.5 : 0.0;
+                    if (diag && r == c) tr += y0;
+                    if (diag && r == c + 1) tr += y1;
+                    y0 = d0 - 0.5 * y0;
+                    y1 = d1 - 0.5 * y1;
+                }
+                ss = fma(y0, y0, ss);
+                ss = fma(y1, y1, ss);
+                *reinterpret_cast<double2 *>(dst + r * B + c) = make_double2(y0, y1);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        }
+        if (lane == 0) {
+            s_red[0][warp] = ss;
+            s_red[1][warp] = tr;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0, t = 0.0;
+#pragma unroll
+            for (int w = 0; w < NT / 32; w++) {
+                s += s_red[0][w];
+                t += s_red[1][w];
+            }
+            g.c_leaf_n2[code] = s;
+            g.c_coord[seg] = (int32_t)code;
+            g.c_slot[code] = seg;
+            if (EPI == EPI_NS_H && diag) g.trace_part[I] = t;
+        }
+        __syncthreads();
+    }
+}
+
+template <int B, int WM, int WN, int STAGES, int EPI>
+static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
+{
+    constexpr int NT = 32 * WM * WN;
+    const size_t smem = sizeof(double) * 2 * STAGES * B * B;
+    auto kern = k_leaf_gemm<B, WM, WN, STAGES, EPI>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_done = true;
+    }
+    if (g.nseg == 0) return SPAMM_OK;
+    kern<<<g.nseg, NT, smem, ctx->stream>>>(g);
+    CKL(ctx);
+    return SPAMM_OK;
+}
+
+template <int EPI>
+static spamm_status gemm_dispatch(spamm_ctx ctx, int b, const GemmArgs &g)
+{
+    switch (b) {
+    case 64: return launch_gemm<64, 2, 2, 3, EPI>(ctx, g);
+    case 32: return launch_gemm<32, 2, 2, 4, EPI>(ctx, g);
+    case 16: return launch_gemm<16, 1, 1, 4, EPI>(ctx, g);
+    default: return set_err(ctx, SPAMM_EINVAL, "b=%d", b);
+    }
+}
+
+spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_mat C, int epi,
+                      double *trace_part)
+{
+    GemmArgs g{A->pool, B->pool, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
+               (int)cw->nsegs, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part};
+    if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H>(ctx, A->b, g);
+    return gemm_dispatch<EPI_STORE>(ctx, A->b, g);
+}
+
+// -------------------------------------------------- diagonal fix-up of H
+// H_ii = 1.5 I where X had no surviving task (i,i) (K6): slots appended at
+// nseg.. in ascending i (single-CTA scan, deterministic), then filled in parallel.
+template <int THREADS>
+__global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int64_t base,
+                              int32_t *newslot, int64_t *count_out)
+{
+    __shared__ V1 sw[THREADS / 32];
+    int64_t run = 0;
+    for (int i0 = 0; i0 < nb; i0 += THREADS) {
+        int i = i0 + threadIdx.x;
+        uint32_t code = i < nb ? morton(i, i) : 0;
+        V1 v{(i < nb && slot_map[code] < 0) ? 1 : 0};
+        V1 tot;
+        V1 ex = block_excl_scan<V1, THREADS>(v, &tot, sw);
+        if (i < nb) {
+            int32_t s = v.x ? (int32_t)(base + run + ex.x) : -1;
+            newslot[i] = s;
+            if (v.x) {
+                slot_map[code] = s;
+                coord[s] = (int32_t)code;
+            }
+        }
+        run += tot.x;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count_out = run;
+}
+
+__global__ void k_diag_fill(const int32_t *newslot, double *pool, int b, double value,
+                            double *leaf_n2)
+{
+    int i = blockIdx.x;
+    int s = newslot[i];
+    if (s < 0) return;
+    double *d = pool + (int64_t)s * b * b;
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) d[e] = (e / b == e % b) ? value : 0.0;
+    if (threadIdx.x == 0) {
+        double ss = 0.0;
+        for (int r = 0; r < b; r++) ss += value * value;
+        leaf_n2[morton(i, i)] = ss;
+    }
+}
+
+spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value, int64_t *added)
+{
+    int32_t *newslot = dalloc<int32_t>(ctx, m->nb);
+    if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
+    k_diag_assign<1024><<<1, 1024, 0, ctx->stream>>>(m->slot, m->coord, m->nb, base, newslot,
+                                                    ctx->iscratch);
+    CKL(ctx);
+    k_diag_fill<<<m->nb, 256, 0, ctx->stream>>>(newslot, m->pool, m->b, value, m->norm2 + pyr_off(m->L));
+    CKL(ctx);
+    int64_t h = 0;
+    CK(cudaMemcpyAsync(&h, ctx->iscratch, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    dev_free(ctx, newslot, sizeof(int32_t) * m->nb);
+    *added = h;
+    return SPAMM_OK;
+}
+
+spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg)
+{
+    int64_t added = 0;
+    ST(diag_append(ctx, H, nseg, 1.5, &added));
+    H->nblk = nseg + added;
+    return SPAMM_OK;
+}
+
+// t = (n - sum_i trace_part[i]) / n, fixed-order single-CTA reduction
+__global__ void k_trace_finish(const double *part, int nb, double n, double *t_out)
+{
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 256) s += part[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *t_out = (n - sh[0]) / n;
+}
+
+spamm_status trace_finish(spamm_ctx ctx, const double *trace_part, int nb, int64_t n, double *t_out)
+{
+    k_trace_finish<<<1, 256, 0, ctx->stream>>>(trace_part, nb, (double)n, t_out);
+    CKL(ctx);
+    return SPAMM_OK;
+}

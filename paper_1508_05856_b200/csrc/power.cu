@@ -1,0 +1,176 @@
+// power.cu — c ~ ||s||_2 for the spectral rescale s <- s / s_{N-1} (P:380-381,
+// "easily obtained largest eigenvalue"; reading L12): K power steps from
+// v0 = 1/sqrt(n) * ones, then the Rayleigh quotient c = v^T s v.
+// Block-CSR SpMV (one CTA per block row, blocks in ascending column order,
+// warp-per-row dot products with fixed-order shuffle reductions: deterministic).
+#include "common.cuh"
+#include "scan.cuh"
+
+// per block row: count of present blocks
+__global__ void k_row_count(const int32_t *slot, int nb, int32_t *cnt)
+{
+    __shared__ int sh[256];
+    int i = blockIdx.x, c = 0;
+    for (int j = threadIdx.x; j < nb; j += 256) c += slot[morton(i, j)] >= 0;
+    sh[threadIdx.x] = c;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt[i] = sh[0];
+}
+
+// single CTA exclusive scan of nb row counts -> rowptr[nb+1]
+__global__ void k_row_scan(const int32_t *cnt, int nb, int32_t *rowptr)
+{
+    __shared__ V1 sw[32];
+    int run = 0;
+    for (int i0 = 0; i0 < nb; i0 += 1024) {
+        int i = i0 + threadIdx.x;
+        V1 v{i < nb ? cnt[i] : 0};
+        V1 tot;
+        V1 ex = block_excl_scan<V1, 1024>(v, &tot, sw);
+        if (i < nb) rowptr[i] = run + ex.x;
+        run += tot.x;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) rowptr[nb] = run;
+}
+
+// per block row: slots and column indices of present blocks, ascending j
+__global__ void k_row_fill(const int32_t *slot, int nb, const int32_t *rowptr, int32_t *cols,
+                           int32_t *slots)
+{
+    __shared__ V1 sw[8];
+    int i = blockIdx.x, run = rowptr[i];
+    for (int j0 = 0; j0 < nb; j0 += 256) {
+        int j = j0 + threadIdx.x;
+        int s = j < nb ? slot[morton(i, j)] : -1;
+        V1 v{s >= 0 ? 1 : 0};
+        V1 tot;
+        V1 ex = block_excl_scan<V1, 256>(v, &tot, sw);
+        if (s >= 0) {
+            cols[run + ex.x] = j;
+            slots[run + ex.x] = s;
+        }
+        run += tot.x;
+        __syncthreads();
+    }
+}
+
+// w[I*b + r] = sum over present blocks (I,J), ascending J, of S_IJ[r,:] . v[J*b:]
+template <int B>
+__global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t *rowptr,
+                                              const int32_t *cols, const int32_t *slots,
+                                              const double *v, double *w)
+{
+    constexpr int PER = B / 32 > 0 ? B / 32 : 1;  // elements per lane per row
+    const int I = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p0 = rowptr[I], p1 = rowptr[I + 1];
+    for (int r = warp; r < B; r += 8) {
+        double acc = 0.0;
+        for (int p = p0; p < p1; p++) {
+            const double *row = pool + (int64_t)slots[p] * B * B + r * B;
+            const double *vv = v + (int64_t)cols[p] * B;
+            double s = 0.0;
+#pragma unroll
+            for (int e = 0; e < PER; e++) {
+                int c = lane + 32 * e;
+                if (c < B) s = fma(row[c], vv[c], s);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            acc += s;
+        }
+        if (lane == 0) w[(int64_t)I * B + r] = acc;
+    }
+}
+
+// single CTA: nrm = sqrt(sum w^2) (fixed order); v = w / nrm
+__global__ void k_normalize(const double *w, int64_t n, double *v)
+{
+    __shared__ double sh[1024];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += 1024) s = fma(w[i], w[i], s);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int k = 512; k > 0; k >>= 1) {
+        if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+        __syncthreads();
+    }
+    double nrm = sqrt(sh[0]);
+    for (int64_t i = threadIdx.x; i < n; i += 1024) v[i] = w[i] / nrm;
+}
+
+__global__ void k_fill(double *v, int64_t n, double val)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = val;
+}
+
+__global__ void k_dot(const double *a, const double *b, int64_t n, double *out)
+{
+    __shared__ double sh[1024];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += 1024) s = fma(a[i], b[i], s);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int k = 512; k > 0; k >>= 1) {
+        if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+template <int B>
+static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
+                 const int32_t *slots, const double *v, double *w)
+{
+    k_spmv<B><<<s->nb, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w);
+    ctx->launches++;
+}
+
+spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
+{
+    const int nb = s->nb;
+    const int64_t n = s->n;
+    int64_t nblk = s->nblk > 0 ? s->nblk : 1;
+    int32_t *cnt = dalloc<int32_t>(ctx, nb), *rowptr = dalloc<int32_t>(ctx, nb + 1);
+    int32_t *cols = dalloc<int32_t>(ctx, nblk), *slots = dalloc<int32_t>(ctx, nblk);
+    double *v = dalloc<double>(ctx, n), *w = dalloc<double>(ctx, n), *c = dalloc<double>(ctx, 1);
+    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c) return set_err(ctx, SPAMM_ENOMEM, "power");
+    cudaStream_t st = ctx->stream;
+    k_row_count<<<nb, 256, 0, st>>>(s->slot, nb, cnt);
+    k_row_scan<<<1, 1024, 0, st>>>(cnt, nb, rowptr);
+    k_row_fill<<<nb, 256, 0, st>>>(s->slot, nb, rowptr, cols, slots);
+    k_fill<<<cdiv(n, 256), 256, 0, st>>>(v, n, 1.0 / sqrt((double)n));
+    ctx->launches += 4;
+    auto mv = [&](const double *x, double *y) {
+        switch (s->b) {
+        case 16: spmv<16>(ctx, s, rowptr, cols, slots, x, y); break;
+        case 32: spmv<32>(ctx, s, rowptr, cols, slots, x, y); break;
+        default: spmv<64>(ctx, s, rowptr, cols, slots, x, y); break;
+        }
+    };
+    for (int it = 0; it < K; it++) {
+        mv(v, w);
+        k_normalize<<<1, 1024, 0, st>>>(w, n, v);
+        ctx->launches++;
+    }
+    mv(v, w);
+    k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
+    CKL(ctx);
+    double h = 0;
+    CK(cudaMemcpyAsync(&h, c, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *c_host = h;
+    dev_free(ctx, cnt, sizeof(int32_t) * nb);
+    dev_free(ctx, rowptr, sizeof(int32_t) * (nb + 1));
+    dev_free(ctx, cols, sizeof(int32_t) * nblk);
+    dev_free(ctx, slots, sizeof(int32_t) * nblk);
+    dev_free(ctx, v, sizeof(double) * n);
+    dev_free(ctx, w, sizeof(double) * n);
+    dev_free(ctx, c, sizeof(double));
+    return SPAMM_OK;
+}

@@ -1,0 +1,249 @@
+// spamm.cu — the C ABI entry points: context, SpAMM product, Newton-Schulz.
+//
+//   spamm_multiply : C = A (x)_tau B   (Eq. newspamm)
+//       cull (cull.cu) -> one stream sync for the counts -> DMMA leaf GEMM with
+//       the store epilogue (gemm.cu) -> norm pyramid of C (tree.cu)
+//   spamm_ns_step  : X = Z (x)_tau Y (epilogue writes H = 1/2(3I - X) and tr X
+//       partials), diagonal fix-up, t_k; Y' = Y (x)_tau_s H; Z' = H (x)_tau Z
+//       (Eq. cannonical P:383-389 in the north_star form, reading L8)
+//   spamm_ns_sqrt  : setup (c, Y0 = s/c, Z0 = I) + iters steps + unscale.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+extern "C" spamm_status spamm_ctx_create(int device, void *cuda_stream, const spamm_allocator *allocator,
+                                         spamm_ctx *out)
+{
+    if (!out) return SPAMM_EINVAL;
+    *out = nullptr;
+    spamm_ctx ctx = new spamm_ctx_s();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return SPAMM_ECUDA;
+    }
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (major != 10 || minor != 0) {
+        delete ctx;
+        return SPAMM_ECUDA;   // built for sm_100a only
+    }
+    if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
+    else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete ctx;
+            return SPAMM_ECUDA;
+        }
+        ctx->own_stream = true;
+    }
+    if (allocator && allocator->alloc && allocator->free) {
+        ctx->alloc = *allocator;
+        ctx->has_alloc = true;
+    }
+    ctx->dscratch = dalloc<double>(ctx, 64);
+    ctx->iscratch = dalloc<int64_t>(ctx, 64);
+    if (!ctx->dscratch || !ctx->iscratch) {
+        delete ctx;
+        return SPAMM_ENOMEM;
+    }
+    for (int i = 0; i < 3; i++) ctx->cw[i] = new Cull();
+    *out = ctx;
+    return SPAMM_OK;
+}
+
+extern "C" void spamm_ctx_destroy(spamm_ctx ctx)
+{
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (int i = 0; i < 3; i++) {
+        if (!ctx->cw[i]) continue;
+        cull_free(ctx, ctx->cw[i]);
+        dev_free(ctx, ctx->cw[i]->counters, sizeof(int32_t) * 64);
+        if (ctx->cw[i]->hcnt) cudaFreeHost(ctx->cw[i]->hcnt);
+        delete ctx->cw[i];
+    }
+    dev_free(ctx, ctx->dscratch, sizeof(double) * 64);
+    dev_free(ctx, ctx->iscratch, sizeof(int64_t) * 64);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+extern "C" const char *spamm_last_error(spamm_ctx ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+extern "C" int64_t spamm_kernel_launches(spamm_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+static spamm_status check_pair(spamm_ctx ctx, spamm_mat A, spamm_mat B, double tau)
+{
+    if (!ctx || !A || !B) return set_err(ctx, SPAMM_EINVAL, "NULL argument");
+    if (A->n != B->n || A->b != B->b)
+        return set_err(ctx, SPAMM_ESHAPE, "shape mismatch: (n=%lld,b=%d) vs (n=%lld,b=%d)",
+                       (long long)A->n, A->b, (long long)B->n, B->b);
+    if (!(tau >= 0.0) || !std::isfinite(tau)) return set_err(ctx, SPAMM_EINVAL, "tau must be finite and >= 0");
+    return SPAMM_OK;
+}
+
+// product with a given workspace and epilogue; C allocated here
+static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
+                            double *trace_part, spamm_mat *C)
+{
+    ST(cull_run(ctx, cw, A, B, tau));
+    int64_t extra = (epi == EPI_NS_H) ? A->nb : 0;
+    spamm_mat m;
+    ST(mat_new(ctx, A->n, A->b, cw->nsegs + extra, &m));
+    spamm_status st = mat_reset_pattern(ctx, m);
+    if (!st) st = gemm_run(ctx, cw, A, B, m, epi, trace_part);
+    if (!st) {
+        m->nblk = cw->nsegs;
+        if (epi == EPI_NS_H) st = diag_fixup(ctx, m, cw->nsegs);
+    }
+    if (!st) st = pyramid_build(ctx, m);
+    if (st) {
+        spamm_mat_free(m);
+        return st;
+    }
+    *C = m;
+    return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_multiply(spamm_ctx ctx, spamm_mat A, spamm_mat B, double tau, spamm_mat *C,
+                                       spamm_stats *stats)
+{
+    ST(check_pair(ctx, A, B, tau));
+    if (!C) return set_err(ctx, SPAMM_EINVAL, "NULL output");
+    ST(product(ctx, ctx->cw[0], A, B, tau, EPI_STORE, nullptr, C));
+    if (stats) *stats = ctx->cw[0]->stats;
+    return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_export_tasks(spamm_ctx ctx, int32_t *ikj, int64_t cap, int64_t *n)
+{
+    if (!ctx || !n || (cap > 0 && !ikj)) return set_err(ctx, SPAMM_EINVAL, "bad argument");
+    if (!ctx->last) {
+        *n = 0;
+        return SPAMM_OK;
+    }
+    return cull_export(ctx, ctx->last, ikj, cap, n);
+}
+
+extern "C" spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
+                                      spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
+                                      double *t_k, spamm_stats stats[3])
+{
+    ST(check_pair(ctx, Z, Y, tau));
+    if (!(tau_s >= 0.0) || !std::isfinite(tau_s)) return set_err(ctx, SPAMM_EINVAL, "tau_s must be >= 0");
+    if (!Y_next || !Z_next) return set_err(ctx, SPAMM_EINVAL, "NULL output");
+    const int nb = Y->nb;
+    double *trace_part = dalloc<double>(ctx, nb);
+    if (!trace_part) return set_err(ctx, SPAMM_ENOMEM, "trace partials");
+    CK(cudaMemsetAsync(trace_part, 0, sizeof(double) * nb, ctx->stream));
+    spamm_mat H = nullptr, Yn = nullptr, Zn = nullptr;
+    // X = Z (x)_tau Y  ->  H = 1/2 (3I - X), tr X partials (X never stored)
+    spamm_status st = product(ctx, ctx->cw[0], Z, Y, tau, EPI_NS_H, trace_part, &H);
+    if (!st) st = trace_finish(ctx, trace_part, nb, Y->n, ctx->dscratch);
+    if (!st && stats) stats[0] = ctx->cw[0]->stats;
+    // Y' = Y (x)_tau_s H ; Z' = H (x)_tau Z
+    if (!st) st = product(ctx, ctx->cw[1], Y, H, tau_s, EPI_STORE, nullptr, &Yn);
+    if (!st && stats) stats[1] = ctx->cw[1]->stats;
+    if (!st) st = product(ctx, ctx->cw[2], H, Z, tau, EPI_STORE, nullptr, &Zn);
+    if (!st && stats) stats[2] = ctx->cw[2]->stats;
+    double hv[3] = {0, 0, 0};
+    if (!st) {
+        // t_k and the root norms (non-finite detection)
+        cudaMemcpyAsync(&hv[0], ctx->dscratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&hv[1], Yn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&hv[2], Zn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) st = check_cuda(ctx, e, "ns step");
+    }
+    dev_free(ctx, trace_part, sizeof(double) * nb);
+    if (st) {
+        spamm_mat_free(H);
+        spamm_mat_free(Yn);
+        spamm_mat_free(Zn);
+        return st;
+    }
+    if (t_k) *t_k = hv[0];
+    if (H_out) *H_out = H;
+    else spamm_mat_free(H);
+    *Y_next = Yn;
+    *Z_next = Zn;
+    if (!std::isfinite(hv[0]) || !std::isfinite(hv[1]) || !std::isfinite(hv[2]))
+        return set_err(ctx, SPAMM_ENOTFINITE, "non-finite trace error or root norm");
+    return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_power_scale(spamm_ctx ctx, spamm_mat s, int32_t K, double *c)
+{
+    if (!ctx || !s || !c || K < 0) return set_err(ctx, SPAMM_EINVAL, "bad argument");
+    return power_scale(ctx, s, K, c);
+}
+
+extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, int32_t iters, spamm_mat *Yout,
+                                      spamm_mat *Zout, const spamm_ns_opts *opts)
+{
+    if (!ctx || !s || !Yout || !Zout) return set_err(ctx, SPAMM_EINVAL, "NULL argument");
+    if (iters < 1) return set_err(ctx, SPAMM_EINVAL, "iters must be >= 1");
+    if (!(tau >= 0.0) || !std::isfinite(tau)) return set_err(ctx, SPAMM_EINVAL, "tau must be finite and >= 0");
+    spamm_ns_opts o{};
+    o.tau_s = -1.0;
+    o.power_iters = 100;
+    if (opts) o = *opts;
+    if (o.power_iters <= 0) o.power_iters = 100;
+    double tau_s = o.tau_s < 0.0 ? tau : o.tau_s;
+    double mu = o.mu;
+    if (!(mu >= 0.0)) return set_err(ctx, SPAMM_EINVAL, "mu must be >= 0");
+    double root = 0.0;
+    ST(spamm_norm(ctx, s, &root));
+    if (!(root > 0.0)) return set_err(ctx, SPAMM_EINVAL, "s is zero");
+    double c = o.scale;
+    if (!(c > 0.0)) ST(power_scale(ctx, s, o.power_iters, &c));
+    if (o.c_out) *o.c_out = c;
+    spamm_mat Y = nullptr, Z = nullptr;
+    ST(spamm_ns_y0(ctx, s, c, mu, &Y));
+    spamm_status st = spamm_identity(ctx, s->n, s->b, &Z);
+    for (int k = 0; k < iters && !st; k++) {
+        spamm_mat Yn = nullptr, Zn = nullptr;
+        double t = 0.0;
+        spamm_stats sts[3];
+        st = spamm_ns_step(ctx, Y, Z, tau, tau_s, &Yn, &Zn, nullptr, &t, sts);
+        if (o.t_history && (st == SPAMM_OK || st == SPAMM_ENOTFINITE)) o.t_history[k] = t;
+        if (o.per_product && st == SPAMM_OK) memcpy(o.per_product + 3 * k, sts, sizeof(sts));
+        if (st) {
+            spamm_mat_free(Yn);
+            spamm_mat_free(Zn);
+            break;
+        }
+        spamm_mat_free(Y);
+        spamm_mat_free(Z);
+        Y = Yn;
+        Z = Zn;
+    }
+    std::string err = ctx->err;
+    spamm_status st2 = SPAMM_OK;
+    if (Y && Z) {
+        // unscale: Y * sqrt(c(1+mu)) -> (s + c mu I)^{1/2}, Z / sqrt(c(1+mu)) -> (s + c mu I)^{-1/2}
+        double f = std::sqrt(c * (1.0 + mu));
+        spamm_mat Yf = nullptr, Zf = nullptr;
+        st2 = mat_map(ctx, Y, 2, f, 0.0, &Yf);
+        if (!st2) st2 = mat_map(ctx, Z, 0, f, 0.0, &Zf);
+        spamm_mat_free(Y);
+        spamm_mat_free(Z);
+        if (!st2) {
+            *Yout = Yf;
+            *Zout = Zf;
+        } else {
+            spamm_mat_free(Yf);
+            spamm_mat_free(Zf);
+        }
+    }
+    if (st) {
+        ctx->err = err;
+        return st;
+    }
+    return st2;
+}

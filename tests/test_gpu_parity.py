@@ -1,0 +1,296 @@
+"""GPU (B200) parity of the CUDA path, through the C ABI, against the CPU oracle.
+
+Bars (BASELINE.json north_star, BJ:5):
+  * surviving task sets identical except triples whose norm product lies within
+    1e-12 relative of the threshold;
+  * relative Frobenius error of each product <= 1e-12;
+  * relative Frobenius error of Y and Z after the full iteration <= 1e-10.
+Leaf norms / pyramid: <= 1e-14 relative (different but fixed summation orders).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import spamm_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1508_05856_b200 as sp
+    return sp.spamm_ctx_create(0)
+
+
+def sp():
+    import paper_1508_05856_b200 as m
+    return m
+
+
+def decaying(n, rate, seed, zero_frac=0.0):
+    r = np.random.default_rng(seed)
+    i = np.arange(n)
+    d = np.abs(i[:, None] - i[None, :])
+    m = np.exp(-rate * d) * r.standard_normal((n, n))
+    return m
+
+
+def gpu_to_oracle(ctx, M):
+    """Copy a GPU quadtree to an oracle tree (present blocks only)."""
+    n, b, _ = M.info()
+    nb = n // b
+    L = nb.bit_length() - 1
+    n2 = sp().spamm_level_norms2(ctx, M, L)
+    bi, bj = np.nonzero(n2 > 0)
+    blocks, pres = sp().spamm_get_blocks(ctx, M, bi, bj)
+    assert pres.all()
+    return O.OMat.from_blocks(n, b, bi.astype(np.int32), bj.astype(np.int32), blocks)
+
+
+def build_pair(ctx, kind, payload, b, n):
+    if kind == "dense":
+        d = torch.from_numpy(payload).cuda()
+        return sp().spamm_build_tree(ctx, d, b), O.OMat.from_dense(payload, b)
+    bi, bj, blocks = payload
+    G = sp().spamm_build_tree_blocks(ctx, n, b, torch.from_numpy(bi).cuda(),
+                                     torch.from_numpy(bj).cuda(), torch.from_numpy(blocks).cuda())
+    return G, O.OMat.from_blocks(n, b, bi, bj, blocks)
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def window_set(A_o, B_o, tau):
+    """Triples within 1e-12 relative of the threshold (leaf norms from the oracle)."""
+    na, nb_ = A_o.leaf_norms(), B_o.leaf_norms()
+    thr = tau * A_o.norm() * B_o.norm()
+    prod = na[:, :, None] * nb_[None, :, :]
+    amb = (na[:, :, None] > 0) & (nb_[None, :, :] > 0) & (np.abs(prod - thr) <= 1e-12 * thr)
+    return {tuple(x) for x in np.argwhere(amb)}
+
+
+def check_product(ctx, A, Ao, B, Bo, tau, vals_tol=1e-12):
+    C, st = sp().spamm_multiply(ctx, A, B, tau, want_stats=True)
+    tg = sp().spamm_export_tasks(ctx)
+    Co, to = O.multiply(Ao, Bo, tau, want_tasks=True)
+    sg = {tuple(x) for x in tg}
+    so = {tuple(x) for x in to}
+    assert len(sg) == len(tg) == st["tasks"]
+    diff = sg ^ so
+    assert diff <= window_set(Ao, Bo, tau), f"{len(diff)} task flips outside the window"
+    # tasks grouped by output block (Morton order), k ascending inside a segment
+    if len(tg):
+        ij = tg[:, 0].astype(np.int64) * (1 << 20) + tg[:, 2]
+        change = np.nonzero(np.diff(ij))[0]
+        starts = np.r_[0, change + 1]
+        assert len(np.unique(ij)) == len(starts) == st["segments"]
+        for s0, s1 in zip(starts, np.r_[starts[1:], len(tg)]):
+            assert np.all(np.diff(tg[s0:s1, 1]) > 0)
+    if not diff:
+        Cg = gpu_to_oracle(ctx, C)
+        n = Ao.n
+        if n <= 4096:
+            assert rel(Cg.to_dense(), Co.to_dense()) <= vals_tol
+        else:
+            bi, bj = Co.block_coords()
+            err = 0.0
+            for I, J in zip(bi, bj):
+                g = Cg.block(I, J)
+                o = Co.block(I, J)
+                err += np.sum((g - o) ** 2)
+            assert math.sqrt(err) <= vals_tol * Co.norm()
+        # norms of C: leaf norm^2 from the epilogue
+        L = (n // Ao.b).bit_length() - 1
+        n2 = sp().spamm_level_norms2(ctx, C, L)
+        np.testing.assert_allclose(np.sqrt(n2), Co.leaf_norms(), rtol=1e-12, atol=1e-300)
+    return C, Co
+
+
+# ------------------------------------------------------------------ tree
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_build_norms(ctx, cfg):
+    c = si.CONFIGS[cfg]
+    kind, payload = si.make_input(c)
+    G, Og = build_pair(ctx, kind, payload, c.b, c.n)
+    L = (c.n // c.b).bit_length() - 1
+    for lev in sorted({0, 1, L // 2, L - 1, L}):
+        g = sp().spamm_level_norms2(ctx, G, lev)
+        np.testing.assert_allclose(np.sqrt(g), Og.level_norms(lev), rtol=1e-14, atol=0)
+    assert sp().spamm_norm(ctx, G) == pytest.approx(Og.norm(), rel=1e-14)
+    assert G.nblocks == Og.nblocks()
+    if c.n <= 4096:
+        d = sp().spamm_to_dense(ctx, G).cpu().numpy()
+        assert np.array_equal(d, Og.to_dense())
+
+
+def test_build_host_pointer_and_ld(ctx):
+    m = decaying(256, 0.1, 5)
+    m[16:32, 64:80] = 0.0
+    big = np.zeros((256, 300))
+    big[:, :256] = m
+    G = sp().spamm_build_tree(ctx, big[:, :256].copy(), 16)
+    assert np.array_equal(sp().spamm_to_dense(ctx, G, device=False), m)
+    Gt = sp().spamm_build_tree(ctx, torch.from_numpy(big).cuda()[:, :256].contiguous(), 16)
+    assert np.array_equal(sp().spamm_to_dense(ctx, Gt).cpu().numpy(), m)
+    assert G.nblocks == 255
+
+
+# --------------------------------------------------------------- product
+def test_tiebreak_and_partial_cull_exact(ctx):
+    A = np.ones((32, 32))
+    G, Og = build_pair(ctx, "dense", A, 16, 32)
+    C = sp().spamm_multiply(ctx, G, G, 0.25)
+    assert len(sp().spamm_export_tasks(ctx)) == 8
+    assert np.all(sp().spamm_to_dense(ctx, C).cpu().numpy() == 32.0)
+    C = sp().spamm_multiply(ctx, G, G, np.nextafter(0.25, 1))
+    assert len(sp().spamm_export_tasks(ctx)) == 0
+    assert np.all(sp().spamm_to_dense(ctx, C).cpu().numpy() == 0.0)
+    P = np.ones((16, 16)) / 16
+    e = 1 / 8
+    A = np.block([[P, e * P], [e * P, P]])
+    G, _ = build_pair(ctx, "dense", A, 16, 32)
+    C = sp().spamm_multiply(ctx, G, G, 1 / 32)
+    t = {tuple(x) for x in sp().spamm_export_tasks(ctx)}
+    assert t == {(0, 0, 0), (0, 0, 1), (0, 1, 1), (1, 0, 0), (1, 1, 0), (1, 1, 1)}
+    assert np.array_equal(sp().spamm_to_dense(ctx, C).cpu().numpy(),
+                          np.block([[P, P / 4], [P / 4, P]]))
+
+
+@pytest.mark.parametrize("n,b", [(64, 64), (128, 16), (512, 16), (1024, 32), (2048, 64), (4096, 64)])
+@pytest.mark.parametrize("tau", [0.0, 1e-8, 1e-4])
+def test_multiply_random(ctx, n, b, tau):
+    a = decaying(n, 20.0 / n, n + b)
+    c = decaying(n, 30.0 / n, n + 2 * b)
+    nb = n // b
+    if nb >= 4:   # ragged pattern: absent blocks
+        a[:b, 2 * b:3 * b] = 0.0
+        c[(nb - 1) * b:, :b] = 0.0
+    A, Ao = build_pair(ctx, "dense", a, b, n)
+    B, Bo = build_pair(ctx, "dense", c, b, n)
+    C, Co = check_product(ctx, A, Ao, B, Bo, tau)
+    if tau == 0.0:
+        ref = a @ c
+        assert rel(sp().spamm_to_dense(ctx, C).cpu().numpy(), ref) <= 1e-13
+
+
+def test_multiply_degenerate(ctx):
+    z = np.zeros((128, 128))
+    Z, Zo = build_pair(ctx, "dense", z, 16, 128)
+    a = decaying(128, 0.1, 1)
+    A, Ao = build_pair(ctx, "dense", a, 16, 128)
+    C = sp().spamm_multiply(ctx, Z, A, 0.0)
+    assert C.nblocks == 0 and len(sp().spamm_export_tasks(ctx)) == 0
+    C = sp().spamm_multiply(ctx, A, A, 1.0 + 1e-15)
+    assert C.nblocks == 0
+    with pytest.raises(sp().SpammError) as e:
+        sp().spamm_multiply(ctx, A, A, -1.0)
+    assert e.value.code == 1
+    B16, _ = build_pair(ctx, "dense", decaying(256, 0.1, 2), 16, 256)
+    with pytest.raises(sp().SpammError) as e:
+        sp().spamm_multiply(ctx, A, B16, 0.0)
+    assert e.value.code == 2
+    # n == b: a single leaf (L = 0)
+    s1 = decaying(64, 0.1, 3)
+    S1, S1o = build_pair(ctx, "dense", s1, 64, 64)
+    check_product(ctx, S1, S1o, S1, S1o, 0.0)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_multiply_config_operands(ctx, cfg):
+    """s (x)_tau s and I (x)_tau s on the config inputs."""
+    c = si.CONFIGS[cfg]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    check_product(ctx, S, So, S, So, c.tau)
+    I = sp().spamm_identity(ctx, c.n, c.b)
+    Io = O.OMat.identity(c.n, c.b)
+    check_product(ctx, I, Io, S, So, c.tau)
+
+
+def test_multiply_c3_full_size(ctx):
+    """C3 operands at full size (n = 16384, b = 64): Y0 (x)_tau Y0, sampled blocks."""
+    c = si.CONFIGS["C3"]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    check_product(ctx, S, So, S, So, c.tau)
+
+
+# -------------------------------------------------------------- NS
+def test_power_scale(ctx):
+    for cfg in ("C1", "C2"):
+        c = si.CONFIGS[cfg]
+        kind, payload = si.make_input(c)
+        S, So = build_pair(ctx, kind, payload, c.b, c.n)
+        assert sp().spamm_power_scale(ctx, S, 100) == pytest.approx(O.power_scale(So, 100), rel=1e-12)
+
+
+def test_ns_step_lockstep(ctx):
+    """One dual step from identical inputs: H, t, Y', Z' and the three task counts."""
+    c = si.CONFIGS["C2"]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    cs = O.power_scale(So)
+    Y = sp().spamm_ns_y0(ctx, S, cs)
+    Z = sp().spamm_identity(ctx, c.n, c.b)
+    for k in range(6):
+        Yo, Zo = gpu_to_oracle(ctx, Y), gpu_to_oracle(ctx, Z)
+        Yn, Zn, t, st, H = sp().spamm_ns_step(ctx, Y, Z, c.tau, want_h=True)
+        Yno, Zno, Ho, to, cnt = O.ns_step(Yo, Zo, c.tau)
+        assert [s["tasks"] for s in st] == list(cnt)
+        assert t == pytest.approx(to, abs=1e-13)
+        assert rel(gpu_to_oracle(ctx, H).to_dense(), Ho.to_dense()) <= 1e-12
+        assert rel(gpu_to_oracle(ctx, Yn).to_dense(), Yno.to_dense()) <= 1e-12
+        assert rel(gpu_to_oracle(ctx, Zn).to_dense(), Zno.to_dense()) <= 1e-12
+        Y, Z = Yn, Zn
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_ns_free_run(ctx, cfg):
+    """Full iteration at the config's tau and iters: Y, Z within 1e-10 of the oracle."""
+    c = si.CONFIGS[cfg]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    cs = O.power_scale(So)
+    r = sp().spamm_ns_sqrt(ctx, S, c.tau, c.iters, scale=cs)
+    ro = O.ns_sqrt(So, c.tau, c.iters, scale=cs)
+    Yg, Zg = gpu_to_oracle(ctx, r["Y"]), gpu_to_oracle(ctx, r["Z"])
+    assert rel(Yg.to_dense(), ro["Y"].to_dense()) <= 1e-10
+    assert rel(Zg.to_dense(), ro["Z"].to_dense()) <= 1e-10
+    np.testing.assert_allclose(r["t"], ro["t"], rtol=0, atol=1e-12)
+    counts = np.array([[p["tasks"] for p in k] for k in r["stats"]])
+    assert np.array_equal(counts, ro["counts"])
+
+
+def test_ns_tau0_closed_form(ctx):
+    """tau = 0: Z.Z equals the KMS tridiagonal inverse; Y.Z = I."""
+    n, b, rho = 1024, 32, 0.5
+    s = si.kms(n, rho)
+    S = sp().spamm_build_tree(ctx, torch.from_numpy(s).cuda(), b)
+    r = sp().spamm_ns_sqrt(ctx, S, 0.0, 25)
+    Y = sp().spamm_to_dense(ctx, r["Y"]).cpu().numpy()
+    Z = sp().spamm_to_dense(ctx, r["Z"]).cpu().numpy()
+    k = 1 / (1 - rho ** 2)
+    inv = np.diag(np.full(n, (1 + rho ** 2) * k))
+    inv[0, 0] = inv[-1, -1] = k
+    inv += np.diag(np.full(n - 1, -rho * k), 1) + np.diag(np.full(n - 1, -rho * k), -1)
+    assert rel(Z @ Z, inv) <= 1e-12
+    assert np.linalg.norm(Y @ Z - np.eye(n)) / math.sqrt(n) <= 1e-13
+
+
+def test_ns_mu_shift(ctx):
+    c = si.CONFIGS["C1"]
+    s = si.kms(c.n, 0.7)
+    S, So = build_pair(ctx, "dense", s, c.b, c.n)
+    cs = O.power_scale(So)
+    r = sp().spamm_ns_sqrt(ctx, S, 1e-8, 30, mu=1e-2, scale=cs)
+    ro = O.ns_sqrt(So, 1e-8, 30, mu=1e-2, scale=cs)
+    assert rel(gpu_to_oracle(ctx, r["Y"]).to_dense(), ro["Y"].to_dense()) <= 1e-10
+    assert rel(gpu_to_oracle(ctx, r["Z"]).to_dense(), ro["Z"].to_dense()) <= 1e-10
