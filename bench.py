@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""bench.py — SpAMM dual Newton-Schulz on B200 (arXiv 1508.05856 hot path).
+
+One "step" = one full pass of the hot path over the
+synthetic input: quadtree build of s from its block list, power-iteration
+scale, Y0 = s/c, Z0 = I, `iters` dual NS iterations (3 SpAMM products each:
+cull + FP64 DMMA leaf GEMM + fused epilogues + norm pyramids) and the unscale.
+
+metric (BASELINE.json): culled-leaf FP64 TFLOP/s = sum over products of
+|S| * 2 b^3 / time (only surviving leaf tasks count), plus seconds per NS
+iteration.  `value` is timed with CUDA events on the library stream with the
+inputs already resident in HBM; `e2e` repeats the step through the C ABI with
+pinned HOST input buffers (H2D inside the timed region) and reads Y and Z back
+to the host every step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import spamm_inputs as si  # noqa: E402
+
+METRIC = "SpAMM culled-leaf FP64 TFLOP/s and seconds per Newton-Schulz step, 1/2/4/8 GPU"
+UNIT = "TFLOP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(si.CONFIGS))
+    ap.add_argument("--tau", type=float, default=None, help="override tau (C4 sweep)")
+    ap.add_argument("--iters", type=int, default=None, help="override NS iterations")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-iters", type=int, default=1,
+                    help="NS iterations of one oracle sample step (reference arm / cpu_baseline)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((num(r[3]) or 0) for r in rows)}
+
+
+# --------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_name(cfg, tau, iters):
+    if cfg.kind == "kms":
+        return (f"{cfg.name}: KMS s_ij={cfg.rho}^|i-j|, N={cfg.n}, leaf {cfg.b}, tau={tau:g}, "
+                f"{iters} dual NS iterations")
+    return (f"{cfg.name}: 3-D Gaussian overlap, N={cfg.n} Hilbert-ordered unit-density points, "
+            f"sigma={cfg.sigma}, shift={cfg.shift:g}, mu={cfg.mu:g}, leaf {cfg.b}, tau={tau:g}, "
+            f"{iters} dual NS iterations")
+
+
+def oracle_sample(cfg, payload, tau, iters, scale):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload:
+    build + Y0 (given scale) + `iters` NS iterations.  Returns (seconds, flops)."""
+    import oracle as O
+    t0 = time.perf_counter()
+    if cfg.kind == "kms":
+        So = O.OMat.from_dense(payload, cfg.b)
+    else:
+        So = O.OMat.from_blocks(cfg.n, cfg.b, *payload)
+    r = O.ns_sqrt(So, tau, iters, scale=scale, mu=cfg.mu)
+    dt = time.perf_counter() - t0
+    flops = float(r["counts"].sum()) * 2.0 * cfg.b ** 3
+    return dt, flops, O.num_threads()
+
+
+# ---------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    cfg = si.CONFIGS[args.config]
+    tau = args.tau if args.tau is not None else cfg.tau
+    iters = args.iters if args.iters is not None else cfg.iters
+    kind, payload = si.make_input(cfg)
+    import oracle as O
+    if kind == "dense":
+        So = O.OMat.from_dense(payload, cfg.b)
+    else:
+        So = O.OMat.from_blocks(cfg.n, cfg.b, *payload)
+    # c from the oracle's own power iteration, once (not part of the timed samples)
+    c = O.power_scale(So, 100)
+    del So
+    for _ in range(args.warmup):
+        oracle_sample(cfg, payload, tau, args.ref_iters, c)
+    tot_t, tot_f, cores = 0.0, 0.0, 1
+    for _ in range(args.steps):
+        dt, fl, cores = oracle_sample(cfg, payload, tau, args.ref_iters, c)
+        tot_t += dt
+        tot_f += fl
+    value = tot_f / tot_t / 1e12
+    sample = (f"{args.config} input, oracle quadtree build + Y0 + the first {args.ref_iters} of "
+              f"{iters} NS iterations per step (c given)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": workload_name(cfg, tau, iters), "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import paper_1508_05856_b200 as sp
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    cfg = si.CONFIGS[args.config]
+    tau = args.tau if args.tau is not None else cfg.tau
+    iters = args.iters if args.iters is not None else cfg.iters
+    kind, payload = si.make_input(cfg)
+    assert kind == "blocks" or cfg.kind == "kms"
+    ctx = sp.spamm_ctx_create(local)
+    stream = ctx.stream
+    dev = torch.device(f"cuda:{local}")
+
+    if kind == "dense":
+        d_in = (torch.from_numpy(payload).to(dev),)
+        h_in = (torch.from_numpy(payload).pin_memory(),)
+        in_bytes = payload.nbytes
+    else:
+        bi, bj, blocks = payload
+        d_in = tuple(torch.from_numpy(x).to(dev) for x in (bi, bj, blocks))
+        h_in = tuple(torch.from_numpy(x).pin_memory() for x in (bi, bj, blocks))
+        in_bytes = bi.nbytes + bj.nbytes + blocks.nbytes
+
+    def build(inp):
+        if kind == "dense":
+            return sp.spamm_build_tree(ctx, inp[0], cfg.b)
+        return sp.spamm_build_tree_blocks(ctx, cfg.n, cfg.b, *inp)
+
+    out_host = {}
+
+    def step(inp, readback):
+        S = build(inp)
+        r = sp.spamm_ns_sqrt(ctx, S, tau, iters, mu=cfg.mu)
+        S.free()
+        flops = sum(p["flops"] for k in r["stats"] for p in k)
+        tasks = sum(p["tasks"] for k in r["stats"] for p in k)
+        d2h = 0
+        if readback:
+            for key in ("Y", "Z"):
+                nblk = r[key].nblocks
+                buf = out_host.get(key)
+                if buf is None or buf[0].shape[0] < nblk:
+                    cap = int(nblk * 1.25) + 16
+                    buf = (torch.empty(cap, dtype=torch.int32).pin_memory(),
+                           torch.empty(cap, dtype=torch.int32).pin_memory(),
+                           torch.empty((cap, cfg.b, cfg.b), dtype=torch.float64).pin_memory())
+                    out_host[key] = buf
+                sp.spamm_export_blocks(ctx, r[key], buf)
+                d2h += nblk * (8 + 8 * cfg.b * cfg.b)
+        r["Y"].free()
+        r["Z"].free()
+        return flops, tasks, d2h, r
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- FP64 tensor peak on this GPU (DMMA issue-rate microbenchmark, ~2 s sustained)
+    _, ms1 = sp.spamm_peak_dmma(ctx, 20000)
+    peak_tflops, peak_ms = sp.spamm_peak_dmma(ctx, int(20000 * max(1.0, 2000.0 / max(ms1, 1e-3))))
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        step(d_in, False)
+    torch.cuda.synchronize()
+
+    # ---- timed: inputs resident in HBM (s: block list > L2)
+    clocks = Clocks(local)
+    sp.spamm_profile_enable(ctx, True)
+    l0 = sp.spamm_kernel_launches(ctx)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    flops = tasks = 0.0
+    last = None
+    for _ in range(args.steps):
+        f, t, _, last = step(d_in, False)
+        flops += f
+        tasks += t
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = sp.spamm_kernel_launches(ctx) - l0
+    prof = sp.spamm_profile_read(ctx)
+    sp.spamm_profile_enable(ctx, False)
+    ms_max = max_over_ranks(ms)
+    flops_all = sum_over_ranks(flops)
+    value = flops_all / (ms_max * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (leaf GEMM), algorithmic flops / event time
+    gemm_achieved = prof["gemm_flops"] / (prof["gemm_ms"] * 1e-3) / 1e12 if prof["gemm_ms"] else None
+    roofline = {
+        "bound": "tensor", "achieved": gemm_achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+        "frac": (gemm_achieved / peak_tflops) if gemm_achieved else None, "traffic": None,
+        "kernel": "k_leaf_gemm (FP64 DMMA m8n8k4)",
+        "peak_source": "measured in this run: spamm_peak_dmma (back-to-back DMMA on all SMs, "
+                       f"{peak_ms:.0f} ms); MEASURED_PEAKS.json has no FP64 figure",
+        "launches": prof["gemm_count"], "avg_launch_ms": prof["gemm_ms"] / max(prof["gemm_count"], 1),
+        "gemm_share_of_step": prof["gemm_ms"] / ms if ms else None,
+        "flops_per_launch": prof["gemm_flops"] / max(prof["gemm_count"], 1),
+    }
+    traffic_file = os.path.join(ROOT, "profiles", f"gemm_traffic_{args.config}.json")
+    if os.path.exists(traffic_file):
+        try:
+            roofline["traffic"] = json.load(open(traffic_file)).get("bytes_per_launch")
+        except (OSError, ValueError):
+            pass
+
+    # ---- e2e through the C ABI with HOST buffers
+    e2e = None
+    if not args.no_e2e:
+        step(h_in, True)  # allocate pinned result buffers
+        barrier()
+        torch.cuda.synchronize()
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        ef = 0.0
+        d2h = 0
+        for _ in range(args.steps):
+            f, _, d2h, _ = step(h_in, True)
+            ef += f
+        e3.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(e2.elapsed_time(e3))
+        e2e = {"value": sum_over_ranks(ef) / (ems * 1e-3) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": ems / args.steps}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        S = build(d_in)
+        c = sp.spamm_power_scale(ctx, S, 100)
+        S.free()
+        dt, fl, cores = oracle_sample(cfg, payload, tau, args.ref_iters, c)
+        cpu = {"value": fl / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{args.config} input: oracle quadtree build + Y0 + first {args.ref_iters} "
+                         f"of {iters} NS iterations ({fl:.3g} culled-leaf flop in {dt:.1f} s)"}
+
+    if rank == 0:
+        r = last
+        blocks_mb = in_bytes / 1e6
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": workload_name(cfg, tau, iters), "n": cfg.n, "leaf": cfg.b, "tau": tau,
+                "iters": iters, "parallelism": "replicas" if ws > 1 else "single",
+                "l2": f"inputs larger than L2 (s = {blocks_mb:.0f} MB of blocks, iterates > 126 MB)",
+            },
+            "s_per_ns_iteration": prof["loop_ms"] / args.steps / iters / 1e3,
+            "setup_ms_per_step": prof["setup_ms"] / args.steps,
+            "tasks_per_step": tasks / args.steps,
+            "t_final": float(r["t"][-1]),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "phase_ms_per_step": {k: prof[f"{k}_ms"] / args.steps for k in ("gemm", "cull", "setup", "loop")},
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -150,6 +150,29 @@ spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, int32_t iters
 spamm_status spamm_scale(spamm_ctx ctx, spamm_mat m, double alpha, int32_t divide,
                          spamm_mat *out);
 
+/* Write all stored blocks: bi/bj [cap] (int32), blocks [cap*b*b] (host or device);
+ * *n = number of stored blocks (pool order).  Pass cap = 0 to query *n. */
+spamm_status spamm_export_blocks(spamm_ctx ctx, spamm_mat m, int32_t *bi, int32_t *bj,
+                                 double *blocks, int64_t cap, int64_t *n);
+
+/* ------------------------------------------------- measurement utilities */
+/* Device-side phase timing with CUDA events on the context stream (bench.py
+ * uses it for the roofline of the dominant kernel).  Phases: */
+enum { SPAMM_PH_GEMM = 0, SPAMM_PH_CULL = 1, SPAMM_PH_SETUP = 2, SPAMM_PH_LOOP = 3,
+       SPAMM_PH_OTHER = 4, SPAMM_NPHASE = 5 };
+typedef struct {
+    double ms[SPAMM_NPHASE];        /* summed event time per phase            */
+    int64_t count[SPAMM_NPHASE];    /* number of timed intervals per phase    */
+    double gemm_flops;              /* sum of 2 b^3 |S| over timed GEMMs      */
+    int64_t gemm_tasks;
+    double gemm_operand_bytes;      /* 2 * 8 b^2 |S| + 8 b^2 segments (algorithmic) */
+} spamm_profile_t;
+spamm_status spamm_profile_enable(spamm_ctx ctx, int32_t enable);  /* resets the counters */
+spamm_status spamm_profile_read(spamm_ctx ctx, spamm_profile_t *out); /* syncs */
+/* FP64 DMMA issue-rate microbenchmark: TFLOP/s of back-to-back independent
+ * mma.sync.m8n8k4.f64 on all SMs for `iters` per warp (syncs). */
+spamm_status spamm_peak_dmma(spamm_ctx ctx, int64_t iters, double *tflops, double *ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,7 @@ __all__ = [
     "spamm_norm", "spamm_to_dense", "spamm_level_norms2", "spamm_get_blocks",
     "spamm_multiply", "spamm_export_tasks", "spamm_ns_step", "spamm_power_scale",
     "spamm_ns_y0", "spamm_identity", "spamm_ns_sqrt", "spamm_scale",
+    "spamm_export_blocks", "spamm_profile_enable", "spamm_profile_read", "spamm_peak_dmma",
 ]
 
 STATUS = {0: "SPAMM_OK", 1: "SPAMM_EINVAL", 2: "SPAMM_ESHAPE", 3: "SPAMM_ENOMEM",
@@ -53,6 +54,16 @@ class spamm_ns_opts(C.Structure):
     _fields_ = [("tau_s", C.c_double), ("mu", C.c_double), ("scale", C.c_double),
                 ("power_iters", C.c_int32), ("t_history", C.c_void_p),
                 ("per_product", C.c_void_p), ("c_out", C.c_void_p)]
+
+
+NPHASE = 5
+PHASES = ("gemm", "cull", "setup", "loop", "other")
+
+
+class spamm_profile_t(C.Structure):
+    _fields_ = [("ms", C.c_double * NPHASE), ("count", C.c_int64 * NPHASE),
+                ("gemm_flops", C.c_double), ("gemm_tasks", C.c_int64),
+                ("gemm_operand_bytes", C.c_double)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -98,6 +109,10 @@ def load():
         "spamm_identity": (i32, [vp, i64, i32, P(vp)]),
         "spamm_ns_sqrt": (i32, [vp, vp, dbl, i32, P(vp), P(vp), P(spamm_ns_opts)]),
         "spamm_scale": (i32, [vp, vp, dbl, i32, P(vp)]),
+        "spamm_export_blocks": (i32, [vp, vp, vp, vp, vp, i64, P(i64)]),
+        "spamm_profile_enable": (i32, [vp, i32]),
+        "spamm_profile_read": (i32, [vp, P(spamm_profile_t)]),
+        "spamm_peak_dmma": (i32, [vp, i64, P(dbl), P(dbl)]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -361,3 +376,38 @@ def spamm_ns_sqrt(ctx: Ctx, s: Mat, tau: float, iters: int, tau_s: float | None 
     if want_stats:
         stats = [[sts[3 * k + p].as_dict() for p in range(3)] for k in range(iters)]
     return dict(Y=Mat(ctx, yo), Z=Mat(ctx, zo), t=t, stats=stats, c=c.value)
+
+
+def spamm_export_blocks(ctx: Ctx, m: Mat, out=None):
+    """All stored blocks: (bi, bj, blocks).  out = (bi, bj, blocks) preallocated
+    torch tensors (pinned host or device) or None for numpy."""
+    n = C.c_int64()
+    ctx.check(load().spamm_export_blocks(ctx.h, m.h, None, None, None, 0, C.byref(n)))
+    k = n.value
+    if out is None:
+        b = m.b
+        out = (np.empty(k, dtype=np.int32), np.empty(k, dtype=np.int32), np.empty((k, b, b)))
+    bi, bj, blocks = out
+    ctx.check(load().spamm_export_blocks(ctx.h, m.h, _ptr(bi), _ptr(bj), _ptr(blocks), k,
+                                         C.byref(n)))
+    return bi[:k], bj[:k], blocks[:k]
+
+
+def spamm_profile_enable(ctx: Ctx, enable: bool = True):
+    ctx.check(load().spamm_profile_enable(ctx.h, int(enable)))
+
+
+def spamm_profile_read(ctx: Ctx) -> dict:
+    p = spamm_profile_t()
+    ctx.check(load().spamm_profile_read(ctx.h, C.byref(p)))
+    d = {f"{ph}_ms": p.ms[i] for i, ph in enumerate(PHASES)}
+    d.update({f"{ph}_count": p.count[i] for i, ph in enumerate(PHASES)})
+    d.update(gemm_flops=p.gemm_flops, gemm_tasks=p.gemm_tasks,
+             gemm_operand_bytes=p.gemm_operand_bytes)
+    return d
+
+
+def spamm_peak_dmma(ctx: Ctx, iters: int = 200000):
+    t, ms = C.c_double(), C.c_double()
+    ctx.check(load().spamm_peak_dmma(ctx.h, int(iters), C.byref(t), C.byref(ms)))
+    return t.value, ms.value

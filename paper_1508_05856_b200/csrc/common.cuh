@@ -34,6 +34,7 @@ struct spamm_ctx_s {
     double *dscratch = nullptr;   // small device scratch (norms, trace, t)
     int64_t *iscratch = nullptr;  // small device scratch (counters)
     double *hpinned = nullptr;    // pinned host scratch
+    void *prof = nullptr;         // prof.cu state
 };
 
 struct spamm_mat_s {
@@ -162,6 +163,12 @@ spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg);
 spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value, int64_t *added);
 spamm_status trace_finish(spamm_ctx ctx, const double *trace_part, int nb, int64_t n,
                           double *t_out);
+
+// prof.cu — phase timing (no-ops unless spamm_profile_enable)
+int prof_begin(spamm_ctx ctx, int phase);
+void prof_end(spamm_ctx ctx, int idx);
+void prof_gemm_work(spamm_ctx ctx, int64_t tasks, int64_t segs, int b);
+void prof_destroy(spamm_ctx ctx);
 
 // power.cu
 spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host);

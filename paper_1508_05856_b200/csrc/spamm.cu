@@ -69,6 +69,7 @@ extern "C" void spamm_ctx_destroy(spamm_ctx ctx)
     dev_free(ctx, ctx->dscratch, sizeof(double) * 64);
     dev_free(ctx, ctx->iscratch, sizeof(int64_t) * 64);
     cudaStreamSynchronize(ctx->stream);
+    prof_destroy(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -91,12 +92,20 @@ static spamm_status check_pair(spamm_ctx ctx, spamm_mat A, spamm_mat B, double t
 static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
                             double *trace_part, spamm_mat *C)
 {
-    ST(cull_run(ctx, cw, A, B, tau));
+    int pc = prof_begin(ctx, SPAMM_PH_CULL);
+    spamm_status sc = cull_run(ctx, cw, A, B, tau);
+    prof_end(ctx, pc);
+    if (sc) return sc;
     int64_t extra = (epi == EPI_NS_H) ? A->nb : 0;
     spamm_mat m;
     ST(mat_new(ctx, A->n, A->b, cw->nsegs + extra, &m));
     spamm_status st = mat_reset_pattern(ctx, m);
-    if (!st) st = gemm_run(ctx, cw, A, B, m, epi, trace_part);
+    if (!st) {
+        int pg = prof_begin(ctx, SPAMM_PH_GEMM);
+        st = gemm_run(ctx, cw, A, B, m, epi, trace_part);
+        prof_end(ctx, pg);
+        prof_gemm_work(ctx, cw->ntasks, cw->nsegs, A->b);
+    }
     if (!st) {
         m->nblk = cw->nsegs;
         if (epi == EPI_NS_H) st = diag_fixup(ctx, m, cw->nsegs);
@@ -197,6 +206,7 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
     double tau_s = o.tau_s < 0.0 ? tau : o.tau_s;
     double mu = o.mu;
     if (!(mu >= 0.0)) return set_err(ctx, SPAMM_EINVAL, "mu must be >= 0");
+    int ps = prof_begin(ctx, SPAMM_PH_SETUP);
     double root = 0.0;
     ST(spamm_norm(ctx, s, &root));
     if (!(root > 0.0)) return set_err(ctx, SPAMM_EINVAL, "s is zero");
@@ -206,6 +216,8 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
     spamm_mat Y = nullptr, Z = nullptr;
     ST(spamm_ns_y0(ctx, s, c, mu, &Y));
     spamm_status st = spamm_identity(ctx, s->n, s->b, &Z);
+    prof_end(ctx, ps);
+    int pl = prof_begin(ctx, SPAMM_PH_LOOP);
     for (int k = 0; k < iters && !st; k++) {
         spamm_mat Yn = nullptr, Zn = nullptr;
         double t = 0.0;
@@ -223,6 +235,7 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
         Y = Yn;
         Z = Zn;
     }
+    prof_end(ctx, pl);
     std::string err = ctx->err;
     spamm_status st2 = SPAMM_OK;
     if (Y && Z) {
