@@ -6,7 +6,10 @@
 //           children of node m are the 32-byte sector 4m..4m+3 of level l+1
 //           (P:125-129 stored squared, reading L5).
 //   slot  : int32 [nb*nb] Morton order -> pool slot, -1 = absent block.
-//   pool  : fp64 [cap][b*b], each leaf block row-major, 256-B aligned.
+//   pool  : fp64 [cap][b*b], each leaf block row-major with its 16-byte chunks
+//           XOR-swizzled inside each row (pool_at below), 256-B aligned.  A
+//           linear TMA bulk copy of a block therefore lands in shared memory
+//           already in the bank-conflict-free layout the DMMA fragment loads want.
 //   coord : int32 [cap] Morton code of the block in each pool slot.
 #pragma once
 #include <cuda_runtime.h>
@@ -95,6 +98,24 @@ __host__ __device__ static inline uint32_t morton(uint32_t i, uint32_t j)
 }
 __host__ __device__ static inline uint32_t morton_i(uint32_t m) { return compact_bits(m >> 1); }
 __host__ __device__ static inline uint32_t morton_j(uint32_t m) { return compact_bits(m); }
+
+// ------------------------------------------------------------------ pool swizzle
+// Element (r, c) of a b x b block lives at pool_at(r, c): the 16-byte chunk c/2 of
+// row r is stored at chunk (c/2) ^ swz(r), swz(r) = ((r>>2)&3)<<1 | (r&1) in [0,8).
+// Both DMMA fragment patterns are then conflict-free: A (lane (g,t) reads
+// A[g][4t..4t+3], two LDS.128) and B (lane (g,t) reads B[4t+s][g], LDS.64; rows
+// s, s+4, s+8, s+12 of a half-warp hit four different bank groups).
+__host__ __device__ static inline int swz(int r) { return (((r >> 2) & 3) << 1) | (r & 1); }
+__host__ __device__ static inline int pool_at(int r, int c, int b)
+{
+    return r * b + ((((c >> 1) ^ swz(r)) << 1) | (c & 1));
+}
+// inverse: physical offset e -> logical column of that element
+__host__ __device__ static inline int pool_col(int e, int b)
+{
+    int r = e / b, q = e % b;
+    return ((((q >> 1) ^ swz(r)) << 1) | (q & 1));
+}
 
 // ------------------------------------------------------------------ errors
 spamm_status set_err(spamm_ctx ctx, spamm_status st, const char *fmt, ...);

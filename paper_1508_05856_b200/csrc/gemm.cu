@@ -10,8 +10,8 @@
 //               X itself is never stored.
 // FP64 MMA on sm_100a is warp-level mma.sync m8n8k4 (SASS DMMA.8x8x4); tcgen05
 // has no f64 kind, so operands go shared memory -> registers.  Tiles are staged
-// by a multi-stage cp.async pipeline into a 128-byte XOR swizzle
-// (chunk' = chunk ^ (row & 7)) which makes both fragment patterns conflict-free:
+// by a warp-specialised TMA bulk-copy / mbarrier pipeline; the pool layout is
+// pre-swizzled (common.cuh pool_at) so both fragment patterns are conflict-free:
 //   A: lane (g,t) reads A[g][4t..4t+3] (2 x LDS.128) — the contraction index is
 //      permuted inside each 16-wide k chunk as k = 4t + s (same permutation on
 //      B's rows, so the product is unchanged);
@@ -37,100 +37,154 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
                  : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+// ------------------------------------------------------------ mbarrier / TMA
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
 {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// swizzled double offset of element (r, c) in a B x B row-major tile
-template <int B>
-__device__ __forceinline__ int swz(int r, int c)
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
 {
-    return r * B + ((((c >> 1) ^ (r & 7))) << 1) + (c & 1);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// TMA bulk copy global -> shared (SASS UBLKCP), completion counted on `bar` in bytes
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
-template <int B, int NT>
-__device__ __forceinline__ void load_tile(double *dst, const double *src)
+// Warp-specialised persistent leaf GEMM.
+//   warp CW (producer): one elected lane walks this CTA's segments (static
+//     round-robin) and, per task, waits for a free stage, then TMA-bulk-copies
+//     the A and B tiles (b*b*8 bytes each, pre-swizzled in the pool) into it.
+//   warps 0..CW-1 (consumers): per task wait for the stage, load fragments,
+//     issue DMMAs into register accumulators, release the stage; at the end
+//     of a segment run the fused epilogue.  The producer runs ahead across
+//     segment boundaries, so the next segment's tiles load during an epilogue.
+template <int B, int CW, int WM, int WN, int STAGES, int EPI>
+__global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
 {
-    constexpr int CH = B * B / 2;   // 16-byte chunks
-    constexpr int HALF = B / 2;     // chunks per row
-#pragma unroll
-    for (int q = threadIdx.x; q < CH; q += NT) {
-        int r = q / HALF, c = q % HALF;
-        cp_async16(dst + r * B + ((c ^ (r & 7)) << 1), src + 2 * q);
-    }
-}
-
-template <int B, int WM, int WN, int STAGES, int EPI>
-__global__ void __launch_bounds__(32 * WM * WN) k_leaf_gemm(GemmArgs g)
-{
-    constexpr int NT = 32 * WM * WN;
+    static_assert(WM * WN == CW, "warp grid");
     constexpr int TM = B / WM, TN = B / WN;
     constexpr int MF = TM / 8, NF = TN / 8;
     constexpr int TILE = B * B;
-    extern __shared__ __align__(128) double smem[];
-    __shared__ double s_red[2][NT / 32];
+    constexpr uint32_t TILE_BYTES = TILE * 8;
+    extern __shared__ __align__(1024) double smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + 2 * STAGES * TILE);
+    uint64_t *empty = full + STAGES;
+    double *red = reinterpret_cast<double *>(empty + STAGES);  // [2 parity][2 (ss,tr)][CW]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == CW) {
+        // ------------------------------------------------------- producer
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int seg = blockIdx.x; seg < g.nseg; seg += gridDim.x) {
+            const int start = g.seg_start[seg], len = g.seg_len[seg];
+            for (int t0 = 0; t0 < len; t0 += 32) {
+                const int t = t0 + lane;
+                const int sa = t < len ? g.tA[start + t] : 0;
+                const int sb = t < len ? g.tB[start + t] : 0;
+                const int cnt = len - t0 < 32 ? len - t0 : 32;
+                for (int j = 0; j < cnt; j++) {
+                    const int a = __shfl_sync(0xffffffffu, sa, j);
+                    const int b = __shfl_sync(0xffffffffu, sb, j);
+                    if (lane == 0) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_expect_tx(&full[stage], 2 * TILE_BYTES);
+                        bulk_g2s(smem + (2 * stage) * TILE, g.a_pool + (int64_t)a * TILE, TILE_BYTES, &full[stage]);
+                        bulk_g2s(smem + (2 * stage + 1) * TILE, g.b_pool + (int64_t)b * TILE, TILE_BYTES,
+                                 &full[stage]);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ----------------------------------------------------------- consumers
     const int g8 = lane >> 2, t4 = lane & 3;
     const int m0 = (warp / WN) * TM, n0 = (warp % WN) * TN;
+    // per-thread fragment offsets (doubles) inside a tile; see pool_at / swz
+    int aoff[MF][2];
+#pragma unroll
+    for (int mf = 0; mf < MF; mf++) {
+        const int r = m0 + 8 * mf + g8;
+#pragma unroll
+        for (int h = 0; h < 2; h++) aoff[mf][h] = r * B + (((2 * t4 + h) ^ swz(r)) << 1);
+    }
+    int boff[NF][4];
+#pragma unroll
+    for (int nf = 0; nf < NF; nf++) {
+        const int col = n0 + 8 * nf + g8;
+#pragma unroll
+        for (int s = 0; s < 4; s++) boff[nf][s] = (4 * t4 + s) * B + ((((col >> 1) ^ ((t4 << 1) | (s & 1)))) << 1) + (col & 1);
+    }
 
+    int stage = 0;
+    uint32_t phase = 0;
+    int par = 0;
     for (int seg = blockIdx.x; seg < g.nseg; seg += gridDim.x) {
-        const int start = g.seg_start[seg], len = g.seg_len[seg];
+        const int len = g.seg_len[seg];
         const uint32_t code = g.seg_code[seg];
-
         double acc[MF][NF][2];
 #pragma unroll
         for (int i = 0; i < MF; i++)
 #pragma unroll
             for (int j = 0; j < NF; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-        // prologue
-#pragma unroll
-        for (int s = 0; s < STAGES - 1; s++) {
-            if (s < len) {
-                int ta = g.tA[start + s], tb = g.tB[start + s];
-                load_tile<B, NT>(smem + (2 * s) * TILE, g.a_pool + (int64_t)ta * TILE);
-                load_tile<B, NT>(smem + (2 * s + 1) * TILE, g.b_pool + (int64_t)tb * TILE);
-            }
-            cp_async_commit();
-        }
         for (int it = 0; it < len; it++) {
-            cp_async_wait<STAGES - 2>();
-            __syncthreads();
-            {
-                int nx = it + STAGES - 1;
-                if (nx < len) {
-                    int st = nx % STAGES;
-                    int ta = g.tA[start + nx], tb = g.tB[start + nx];
-                    load_tile<B, NT>(smem + (2 * st) * TILE, g.a_pool + (int64_t)ta * TILE);
-                    load_tile<B, NT>(smem + (2 * st + 1) * TILE, g.b_pool + (int64_t)tb * TILE);
-                }
-                cp_async_commit();
-            }
-            const double *As = smem + (2 * (it % STAGES)) * TILE;
+            mbar_wait(&full[stage], phase);
+            const double *As = smem + (2 * stage) * TILE;
             const double *Bs = As + TILE;
 #pragma unroll
             for (int kc = 0; kc < B / 16; kc++) {
+                // contraction index permuted inside the 16-wide chunk: k = 16kc + 4t + s
                 double a[MF][4], bf[NF][4];
 #pragma unroll
                 for (int mf = 0; mf < MF; mf++) {
-                    int r = m0 + 8 * mf + g8;
-                    int c = 8 * kc + 2 * t4;
-                    double2 v0 = *reinterpret_cast<const double2 *>(As + r * B + ((c ^ (r & 7)) << 1));
-                    double2 v1 = *reinterpret_cast<const double2 *>(As + r * B + (((c + 1) ^ (r & 7)) << 1));
+                    const double2 v0 = *reinterpret_cast<const double2 *>(As + aoff[mf][0] + 16 * kc);
+                    const double2 v1 = *reinterpret_cast<const double2 *>(As + aoff[mf][1] + 16 * kc);
                     a[mf][0] = v0.x; a[mf][1] = v0.y; a[mf][2] = v1.x; a[mf][3] = v1.y;
                 }
 #pragma unroll
-                for (int nf = 0; nf < NF; nf++) {
-                    int col = n0 + 8 * nf + g8;
+                for (int nf = 0; nf < NF; nf++)
 #pragma unroll
-                    for (int s = 0; s < 4; s++) bf[nf][s] = Bs[swz<B>(16 * kc + 4 * t4 + s, col)];
-                }
+                    for (int s = 0; s < 4; s++) bf[nf][s] = Bs[boff[nf][s] + 16 * kc * B];
 #pragma unroll
                 for (int s = 0; s < 4; s++)
 #pragma unroll
@@ -139,10 +193,15 @@ __global__ void __launch_bounds__(32 * WM * WN) k_leaf_gemm(GemmArgs g)
                         for (int nf = 0; nf < NF; nf++)
                             dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s], bf[nf][s]);
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
         }
-        cp_async_wait<0>();
 
-        // ------------------------------------------------------ epilogue
+        // ---------------------------------------------------------- epilogue
         const int I = morton_i(code), J = morton_j(code);
         const bool diag = (I == J);
         double *dst = g.c_pool + (int64_t)seg * TILE;
@@ -151,10 +210,11 @@ __global__ void __launch_bounds__(32 * WM * WN) k_leaf_gemm(GemmArgs g)
         for (int mf = 0; mf < MF; mf++)
 #pragma unroll
             for (int nf = 0; nf < NF; nf++) {
-                int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
+                const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
                 double y0 = acc[mf][nf][0], y1 = acc[mf][nf][1];
                 if (EPI == EPI_NS_H) {
-                    double d0 = (diag && r == c) ? 1.5 : 0.0, d1 = (diag && r == c + 1) ? 1.5 : 0.0;
+                    // H = 1/2 (3 delta - X) written as 1.5 delta - 0.5 x (the 1/2 is exact)
+                    const double d0 = (diag && r == c) ? 1.5 : 0.0, d1 = (diag && r == c + 1) ? 1.5 : 0.0;
                     if (diag && r == c) tr += y0;
                     if (diag && r == c + 1) tr += y1;
                     y0 = d0 - 0.5 * y0;
@@ -162,47 +222,52 @@ __global__ void __launch_bounds__(32 * WM * WN) k_leaf_gemm(GemmArgs g)
                 }
                 ss = fma(y0, y0, ss);
                 ss = fma(y1, y1, ss);
-                *reinterpret_cast<double2 *>(dst + r * B + c) = make_double2(y0, y1);
+                *reinterpret_cast<double2 *>(dst + r * B + ((((c >> 1) ^ swz(r))) << 1)) = make_double2(y0, y1);
             }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             ss += __shfl_xor_sync(0xffffffffu, ss, o);
             tr += __shfl_xor_sync(0xffffffffu, tr, o);
         }
+        double *rp = red + par * 2 * CW;
         if (lane == 0) {
-            s_red[0][warp] = ss;
-            s_red[1][warp] = tr;
+            rp[warp] = ss;
+            rp[CW + warp] = tr;
         }
-        __syncthreads();
+        asm volatile("bar.sync 1, %0;\n" ::"n"(CW * 32) : "memory");
         if (threadIdx.x == 0) {
-            double s = 0.0, t = 0.0;
+            double s2 = 0.0, t2 = 0.0;
 #pragma unroll
-            for (int w = 0; w < NT / 32; w++) {
-                s += s_red[0][w];
-                t += s_red[1][w];
+            for (int w = 0; w < CW; w++) {
+                s2 += rp[w];
+                t2 += rp[CW + w];
             }
-            g.c_leaf_n2[code] = s;
+            g.c_leaf_n2[code] = s2;
             g.c_coord[seg] = (int32_t)code;
             g.c_slot[code] = seg;
-            if (EPI == EPI_NS_H && diag) g.trace_part[I] = t;
+            if (EPI == EPI_NS_H && diag) g.trace_part[I] = t2;
         }
-        __syncthreads();
+        par ^= 1;
     }
 }
 
-template <int B, int WM, int WN, int STAGES, int EPI>
+template <int B, int CW, int WM, int WN, int STAGES, int EPI>
 static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
 {
-    constexpr int NT = 32 * WM * WN;
-    const size_t smem = sizeof(double) * 2 * STAGES * B * B;
-    auto kern = k_leaf_gemm<B, WM, WN, STAGES, EPI>;
-    static bool attr_done = false;
-    if (!attr_done) {
+    constexpr int NT = 32 * (CW + 1);
+    const size_t smem = sizeof(double) * 2 * STAGES * B * B + 2 * STAGES * sizeof(uint64_t) +
+                        4 * CW * sizeof(double);
+    auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI>;
+    static int occ = 0;
+    if (!occ) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_done = true;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
+        if (occ < 1) occ = 1;
     }
     if (g.nseg == 0) return SPAMM_OK;
-    kern<<<g.nseg, NT, smem, ctx->stream>>>(g);
+    int grid = ctx->sm_count * occ;
+    if (grid > g.nseg) grid = g.nseg;
+    kern<<<grid, NT, smem, ctx->stream>>>(g);
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -211,9 +276,9 @@ template <int EPI>
 static spamm_status gemm_dispatch(spamm_ctx ctx, int b, const GemmArgs &g)
 {
     switch (b) {
-    case 64: return launch_gemm<64, 2, 2, 3, EPI>(ctx, g);
-    case 32: return launch_gemm<32, 2, 2, 4, EPI>(ctx, g);
-    case 16: return launch_gemm<16, 1, 1, 4, EPI>(ctx, g);
+    case 64: return launch_gemm<64, 8, 2, 4, 3, EPI>(ctx, g);
+    case 32: return launch_gemm<32, 4, 2, 2, 4, EPI>(ctx, g);
+    case 16: return launch_gemm<16, 1, 1, 1, 4, EPI>(ctx, g);
     default: return set_err(ctx, SPAMM_EINVAL, "b=%d", b);
     }
 }
@@ -263,7 +328,7 @@ __global__ void k_diag_fill(const int32_t *newslot, double *pool, int b, double 
     int s = newslot[i];
     if (s < 0) return;
     double *d = pool + (int64_t)s * b * b;
-    for (int e = threadIdx.x; e < b * b; e += blockDim.x) d[e] = (e / b == e % b) ? value : 0.0;
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) d[e] = (e / b == pool_col(e, b)) ? value : 0.0;
     if (threadIdx.x == 0) {
         double ss = 0.0;
         for (int r = 0; r < b; r++) ss += value * value;

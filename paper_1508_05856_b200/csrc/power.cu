@@ -59,32 +59,43 @@ __global__ void k_row_fill(const int32_t *slot, int nb, const int32_t *rowptr, i
     }
 }
 
-// w[I*b + r] = sum over present blocks (I,J), ascending J, of S_IJ[r,:] . v[J*b:]
+// w[I*b + r] = sum over present blocks (I,J), ascending J, of S_IJ[r,:] . v[J*b:].
+// 256 threads per block row; thread t owns E = b*b/256 consecutive (swizzled)
+// elements of one row of every block, accumulates over the row's blocks in
+// order, and the TPR = b/E threads of a row reduce with a fixed xor tree.
 template <int B>
 __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t *rowptr,
                                               const int32_t *cols, const int32_t *slots,
                                               const double *v, double *w)
 {
-    constexpr int PER = B / 32 > 0 ? B / 32 : 1;  // elements per lane per row
-    const int I = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int E = B * B / 256, TPR = B / E;
+    const int I = blockIdx.x;
     const int p0 = rowptr[I], p1 = rowptr[I + 1];
-    for (int r = warp; r < B; r += 8) {
-        double acc = 0.0;
-        for (int p = p0; p < p1; p++) {
-            const double *row = pool + (int64_t)slots[p] * B * B + r * B;
-            const double *vv = v + (int64_t)cols[p] * B;
-            double s = 0.0;
+    const int e0 = threadIdx.x * E;
+    const int r = e0 / B;
+    int lc[E];
 #pragma unroll
-            for (int e = 0; e < PER; e++) {
-                int c = lane + 32 * e;
-                if (c < B) s = fma(row[c], vv[c], s);
+    for (int i = 0; i < E; i++) lc[i] = pool_col(e0 + i, B);
+    double acc = 0.0;
+    for (int p = p0; p < p1; p++) {
+        const double *blk = pool + (int64_t)slots[p] * B * B + e0;
+        const double *vv = v + (int64_t)cols[p] * B;
+        double s = 0.0;
+        if constexpr (E >= 2) {
+#pragma unroll
+            for (int i = 0; i < E; i += 2) {
+                double2 x = *reinterpret_cast<const double2 *>(blk + i);
+                s = fma(x.x, vv[lc[i]], s);
+                s = fma(x.y, vv[lc[i + 1]], s);
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            acc += s;
+        } else {
+            s = blk[0] * vv[lc[0]];
         }
-        if (lane == 0) w[(int64_t)I * B + r] = acc;
+        acc += s;
     }
+#pragma unroll
+    for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x % TPR) == 0) w[(int64_t)I * B + r] = acc;
 }
 
 // single CTA: nrm = sqrt(sum w^2) (fixed order); v = w / nrm

@@ -160,6 +160,14 @@ __global__ void k_coords_out(const int32_t *coord, int64_t n, int32_t *bi, int32
     bj[t] = morton_j(c);
 }
 
+__global__ void k_unswizzle(const double *pool, int b, double *out)
+{
+    const int64_t blk = blockIdx.x;
+    const double *s = pool + blk * (int64_t)b * b;
+    double *d = out + blk * (int64_t)b * b;
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) d[e] = s[pool_at(e / b, e % b, b)];
+}
+
 extern "C" spamm_status spamm_export_blocks(spamm_ctx ctx, spamm_mat m, int32_t *bi, int32_t *bj,
                                             double *blocks, int64_t cap, int64_t *n)
 {
@@ -177,9 +185,14 @@ extern "C" spamm_status spamm_export_blocks(spamm_ctx ctx, spamm_mat m, int32_t 
         CK(cudaMemcpyAsync(bi, dbi, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaMemcpyAsync(bj, dbj, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, ctx->stream));
     }
-    CK(cudaMemcpyAsync(blocks, m->pool, sizeof(double) * k * b2,
-                       hb ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+    // un-swizzle into row-major blocks (device), then one copy out if the target is host
+    double *dbl = hb ? dalloc<double>(ctx, k * b2) : blocks;
+    if (!dbl) return set_err(ctx, SPAMM_ENOMEM, "export staging");
+    k_unswizzle<<<(int)k, 256, 0, ctx->stream>>>(m->pool, m->b, dbl);
+    CKL(ctx);
+    if (hb) CK(cudaMemcpyAsync(blocks, dbl, sizeof(double) * k * b2, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (hb) dev_free(ctx, dbl, sizeof(double) * k * b2);
     if (hc) {
         dev_free(ctx, dbi, sizeof(int32_t) * k);
         dev_free(ctx, dbj, sizeof(int32_t) * k);

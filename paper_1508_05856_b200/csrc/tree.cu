@@ -205,7 +205,7 @@ __global__ void k_build_scatter(BlockSrc src, int64_t count, const int32_t *slot
     double *dst = pool + (int64_t)s * b * b;
     for (int q = lane; q < b * half; q += 32) {
         int r = q / half, c = (q % half) * 2;
-        *reinterpret_cast<double2 *>(dst + r * b + c) =
+        *reinterpret_cast<double2 *>(dst + pool_at(r, c, b)) =
             *reinterpret_cast<const double2 *>(p + (int64_t)r * ld + c);
     }
     if (lane == 0) {
@@ -427,7 +427,7 @@ __global__ void k_map(const double *src, const int32_t *coord, int64_t nblk, int
     const double *s = src ? src + blk * (int64_t)b * b : nullptr;
     double *d = dst + blk * (int64_t)b * b;
     for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-        int r = e / b, q = e % b;
+        int r = e / b, q = pool_col(e, b);   // logical (row, column) of physical e
         double x = s ? s[e] : 0.0;
         double dl = (diag && r == q) ? 1.0 : 0.0;
         double y;
@@ -495,7 +495,7 @@ __global__ void k_to_dense(const double *pool, const int32_t *coord, int64_t nbl
     int I = morton_i(code), J = morton_j(code);
     const double *s = pool + blk * (int64_t)b * b;
     for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-        int r = e / b, q = e % b;
+        int r = e / b, q = pool_col(e, b);
         dense[(int64_t)(I * b + r) * ld + (J * b + q)] = s[e];
     }
 }
@@ -557,7 +557,8 @@ __global__ void k_get_blocks(const double *pool, const int32_t *slot, int b, int
     if (t >= nreq) return;
     int s = slot[morton(bi[t], bj[t])];
     double *d = out + t * (int64_t)b * b;
-    for (int e = threadIdx.x; e < b * b; e += blockDim.x) d[e] = s >= 0 ? pool[(int64_t)s * b * b + e] : 0.0;
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x)
+        d[e] = s >= 0 ? pool[(int64_t)s * b * b + pool_at(e / b, e % b, b)] : 0.0;
     if (threadIdx.x == 0 && present) present[t] = s >= 0;
 }
 
