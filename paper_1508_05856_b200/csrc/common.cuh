@@ -149,7 +149,7 @@ spamm_status leaf_norms_from_pool(spamm_ctx ctx, spamm_mat m);  // recompute lea
 int is_device_ptr(const void *p);
 
 // cull.cu — the level-by-level two-sided norm query (Eq. newspamm)
-enum { CNT_OVERFLOW = 16, CNT_NSEG = 17, CNT_TICKET = 20 };  // counters[] layout; [0..15] = level counts
+enum { CNT_OVERFLOW = 16, CNT_NSEG = 17, CNT_TICKET = 20, CNT_GEMM_TICKET = 48 };  // counters[] layout; [0..15] = level counts
 struct Cull {
     int64_t cap = 0;              // task capacity of every level
     int64_t cap_segs = 0;         // segment capacity

@@ -28,6 +28,7 @@ struct GemmArgs {
     int32_t *c_coord, *c_slot;
     double *c_leaf_n2;
     double *trace_part;
+    int32_t *ticket;   // dynamic segment scheduler (zeroed before the launch)
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b)
@@ -75,9 +76,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 // Warp-specialised persistent leaf GEMM.
-//   warp CW (producer): one elected lane walks this CTA's segments (static
-//     round-robin) and, per task, waits for a free stage, then TMA-bulk-copies
-//     the A and B tiles (b*b*8 bytes each, pre-swizzled in the pool) into it.
+//   warp CW (producer): one elected lane takes segments from a global ticket
+//     (dynamic scheduling, Morton order: no tail imbalance, deterministic
+//     results since a segment is owned by one CTA), announces each through a
+//     smem queue, and per task waits for a free stage, then TMA-bulk-copies the
+//     A and B tiles (b*b*8 bytes each, pre-swizzled in the pool) into it.
 //   warps 0..CW-1 (consumers): per task wait for the stage, load fragments,
 //     issue DMMAs into register accumulators, release the stage; at the end
 //     of a segment run the fused epilogue.  The producer runs ahead across
@@ -91,9 +94,13 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
     constexpr int TILE = B * B;
     constexpr uint32_t TILE_BYTES = TILE * 8;
     extern __shared__ __align__(1024) double smem[];
+    constexpr int QN = 4;  // segment-queue depth (producer -> consumers)
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + 2 * STAGES * TILE);
     uint64_t *empty = full + STAGES;
-    double *red = reinterpret_cast<double *>(empty + STAGES);  // [2 parity][2 (ss,tr)][CW]
+    uint64_t *qfull = empty + STAGES;
+    uint64_t *qempty = qfull + QN;
+    int *segq = reinterpret_cast<int *>(qempty + QN);
+    double *red = reinterpret_cast<double *>(segq + 2 * QN);  // [2 parity][2 (ss,tr)][CW]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -101,15 +108,35 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], CW);
         }
+        for (int q = 0; q < QN; q++) {
+            mbar_init(&qfull[q], 1);
+            mbar_init(&qempty[q], CW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
     if (warp == CW) {
         // ------------------------------------------------------- producer
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int seg = blockIdx.x; seg < g.nseg; seg += gridDim.x) {
+        // Dynamic scheduling: segments (Morton order) are taken from a global
+        // ticket and announced to the consumers through a QN-deep smem queue.
+        int stage = 0, q = 0;
+        uint32_t phase = 0, qphase = 0;
+        for (;;) {
+            int seg = 0;
+            if (lane == 0) {
+                seg = atomicAdd(g.ticket, 1);
+                if (seg >= g.nseg) seg = -1;
+                mbar_wait(&qempty[q], qphase ^ 1);
+                segq[q] = seg;
+                mbar_arrive(&qfull[q]);
+            }
+            seg = __shfl_sync(0xffffffffu, seg, 0);
+            if (++q == QN) {
+                q = 0;
+                qphase ^= 1;
+            }
+            if (seg < 0) break;
             const int start = g.seg_start[seg], len = g.seg_len[seg];
             for (int t0 = 0; t0 < len; t0 += 32) {
                 const int t = t0 + lane;
@@ -155,10 +182,19 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
         for (int s = 0; s < 4; s++) boff[nf][s] = (4 * t4 + s) * B + ((((col >> 1) ^ ((t4 << 1) | (s & 1)))) << 1) + (col & 1);
     }
 
-    int stage = 0;
-    uint32_t phase = 0;
+    int stage = 0, q = 0;
+    uint32_t phase = 0, qphase = 0;
     int par = 0;
-    for (int seg = blockIdx.x; seg < g.nseg; seg += gridDim.x) {
+    for (;;) {
+        mbar_wait(&qfull[q], qphase);
+        const int seg = segq[q];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&qempty[q]);
+        if (++q == QN) {
+            q = 0;
+            qphase ^= 1;
+        }
+        if (seg < 0) break;
         const int len = g.seg_len[seg];
         const uint32_t code = g.seg_code[seg];
         double acc[MF][NF][2];
@@ -256,7 +292,7 @@ static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
 {
     constexpr int NT = 32 * (CW + 1);
     const size_t smem = sizeof(double) * 2 * STAGES * B * B + 2 * STAGES * sizeof(uint64_t) +
-                        4 * CW * sizeof(double);
+                        2 * 4 * sizeof(uint64_t) + 2 * 4 * sizeof(int) + 4 * CW * sizeof(double);
     auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI>;
     static int occ = 0;
     if (!occ) {
@@ -287,7 +323,8 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_m
                       double *trace_part)
 {
     GemmArgs g{A->pool, B->pool, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
-               (int)cw->nsegs, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part};
+               (int)cw->nsegs, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
+               cw->counters + CNT_GEMM_TICKET};
     if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H>(ctx, A->b, g);
     return gemm_dispatch<EPI_STORE>(ctx, A->b, g);
 }

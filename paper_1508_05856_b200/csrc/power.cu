@@ -77,21 +77,37 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
 #pragma unroll
     for (int i = 0; i < E; i++) lc[i] = pool_col(e0 + i, B);
     double acc = 0.0;
-    for (int p = p0; p < p1; p++) {
-        const double *blk = pool + (int64_t)slots[p] * B * B + e0;
-        const double *vv = v + (int64_t)cols[p] * B;
-        double s = 0.0;
-        if constexpr (E >= 2) {
+    constexpr int U = 4;  // blocks in flight per thread
+    for (int p = p0; p < p1; p += U) {
+        double x[U][E], vx[U][E];
 #pragma unroll
-            for (int i = 0; i < E; i += 2) {
-                double2 x = *reinterpret_cast<const double2 *>(blk + i);
-                s = fma(x.x, vv[lc[i]], s);
-                s = fma(x.y, vv[lc[i + 1]], s);
+        for (int u = 0; u < U; u++) {
+            if (p + u < p1) {
+                const double *blk = pool + (int64_t)slots[p + u] * B * B + e0;
+                const double *vv = v + (int64_t)cols[p + u] * B;
+                if constexpr (E >= 2) {
+#pragma unroll
+                    for (int i = 0; i < E; i += 2) {
+                        double2 t = __ldg(reinterpret_cast<const double2 *>(blk + i));
+                        x[u][i] = t.x;
+                        x[u][i + 1] = t.y;
+                    }
+                } else {
+                    x[u][0] = __ldg(blk);
+                }
+#pragma unroll
+                for (int i = 0; i < E; i++) vx[u][i] = __ldg(vv + lc[i]);
             }
-        } else {
-            s = blk[0] * vv[lc[0]];
         }
-        acc += s;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (p + u < p1) {
+                double s = 0.0;
+#pragma unroll
+                for (int i = 0; i < E; i++) s = fma(x[u][i], vx[u][i], s);
+                acc += s;
+            }
+        }
     }
 #pragma unroll
     for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

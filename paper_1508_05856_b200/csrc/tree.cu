@@ -119,6 +119,7 @@ __device__ __forceinline__ double warp_block_sumsq(const double *blk, int b, int
 {
     double s0 = 0.0, s1 = 0.0;
     const int half = b / 2;  // double2 per row
+#pragma unroll 8
     for (int q = lane; q < b * half; q += 32) {
         int r = q / half, c = (q % half) * 2;
         double2 v = *reinterpret_cast<const double2 *>(blk + (int64_t)r * ld + c);
