@@ -153,7 +153,10 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
         }
         int4 tot;
         int4 ex = block_excl_scan<int4, CT>(c, &tot, sw);
-        if (threadIdx.x == 0) s_excl = tile_lookback(st, tile, tot);
+        if (threadIdx.x < 32) {
+            int4 e = tile_lookback(st, tile, tot);
+            if (threadIdx.x == 0) s_excl = e;
+        }
         __syncthreads();
         int4 p = vadd(s_excl, ex);
         if (t < n) pre[t] = p;
@@ -252,7 +255,10 @@ __global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, in
         V1 h{(t < n && r.z == t) ? 1 : 0};
         V1 tot;
         V1 ex = block_excl_scan<V1, CT>(h, &tot, sw);
-        if (threadIdx.x == 0) s_excl = tile_lookback(st, tile, tot).x;
+        if (threadIdx.x < 32) {
+            int e = tile_lookback(st, tile, tot).x;
+            if (threadIdx.x == 0) s_excl = e;
+        }
         __syncthreads();
         int s = s_excl + ex.x;
         if (h.x && s < cap_segs) {

@@ -60,19 +60,20 @@ __global__ void k_row_fill(const int32_t *slot, int nb, const int32_t *rowptr, i
 }
 
 // w[I*b + r] = sum over present blocks (I,J), ascending J, of S_IJ[r,:] . v[J*b:].
-// 256 threads per block row; thread t owns E = b*b/256 consecutive (swizzled)
-// elements of one row of every block, accumulates over the row's blocks in
-// order, and the TPR = b/E threads of a row reduce with a fixed xor tree.
+// Thread t owns E consecutive (swizzled) elements of one row; TPR = b/E threads
+// per row, RG = 256/TPR rows per CTA, b/RG CTAs per block row.  Each thread
+// accumulates its partial dot products over the row's blocks in order (U blocks
+// in flight), then the TPR threads of a row reduce with a fixed xor tree.
 template <int B>
 __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t *rowptr,
                                               const int32_t *cols, const int32_t *slots,
                                               const double *v, double *w)
 {
-    constexpr int E = B * B / 256, TPR = B / E;
-    const int I = blockIdx.x;
+    constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
+    const int I = blockIdx.x / CPR, rg = blockIdx.x % CPR;
     const int p0 = rowptr[I], p1 = rowptr[I + 1];
-    const int e0 = threadIdx.x * E;
-    const int r = e0 / B;
+    const int r = rg * RG + threadIdx.x / TPR;
+    const int e0 = r * B + (threadIdx.x % TPR) * E;   // physical offset inside a block
     int lc[E];
 #pragma unroll
     for (int i = 0; i < E; i++) lc[i] = pool_col(e0 + i, B);
@@ -154,7 +155,8 @@ template <int B>
 static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
                  const int32_t *slots, const double *v, double *w)
 {
-    k_spmv<B><<<s->nb, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w);
+    constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
+    k_spmv<B><<<s->nb * CPR, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w);
     ctx->launches++;
 }
 

@@ -77,35 +77,57 @@ __device__ __forceinline__ T block_excl_scan(T v, T *total, T *smem_warp /*[THRE
     return vadd(wpre, ex);
 }
 
-// Look-back: called by thread 0 only; returns the exclusive prefix of `tile`.
+__device__ __forceinline__ V1 vshfl_xor(V1 a, int d) { return V1{__shfl_xor_sync(0xffffffffu, a.x, d)}; }
+__device__ __forceinline__ int4 vshfl_xor(int4 a, int d)
+{
+    return make_int4(__shfl_xor_sync(0xffffffffu, a.x, d), __shfl_xor_sync(0xffffffffu, a.y, d),
+                     __shfl_xor_sync(0xffffffffu, a.z, d), __shfl_xor_sync(0xffffffffu, a.w, d));
+}
+
+// Warp-parallel look-back: called by all 32 lanes of ONE warp; returns (in every
+// lane) the exclusive prefix of `tile`.  Each round inspects the 32 nearest
+// unresolved predecessors with one round trip: it waits until all of them have
+// published at least their aggregate, sums the aggregates down to the nearest
+// inclusive prefix (flag 2) and stops there, else moves the window back.
 template <typename T>
 __device__ __forceinline__ T tile_lookback(ScanTiles<T> st, int tile, T agg)
 {
+    const int lane = threadIdx.x & 31;
     T excl = vzero(agg);
     if (tile == 0) {
-        vstore_volatile(&st.pre[0], agg);
-        __threadfence();
-        *(volatile int32_t *)&st.flag[0] = 2;
+        if (lane == 0) {
+            vstore_volatile(&st.pre[0], agg);
+            __threadfence();
+            *(volatile int32_t *)&st.flag[0] = 2;
+        }
         return excl;
     }
-    vstore_volatile(&st.agg[tile], agg);
-    __threadfence();
-    *(volatile int32_t *)&st.flag[tile] = 1;
-    int j = tile - 1;
-    while (true) {
-        int f = *(volatile int32_t *)&st.flag[j];
-        if (f == 0) continue;
+    if (lane == 0) {
+        vstore_volatile(&st.agg[tile], agg);
         __threadfence();
-        if (f == 2) {
-            excl = vadd(excl, vload_volatile(&st.pre[j]));
-            break;
-        }
-        excl = vadd(excl, vload_volatile(&st.agg[j]));
-        j--;
+        *(volatile int32_t *)&st.flag[tile] = 1;
     }
-    vstore_volatile(&st.pre[tile], vadd(excl, agg));
-    __threadfence();
-    *(volatile int32_t *)&st.flag[tile] = 2;
+    int j = tile - 1 - lane;
+    while (true) {
+        int f = j >= 0 ? *(volatile int32_t *)&st.flag[j] : 2;
+        if (__any_sync(0xffffffffu, f == 0)) continue;
+        __threadfence();
+        T v = vzero(agg);
+        if (j >= 0) v = (f == 2) ? vload_volatile(&st.pre[j]) : vload_volatile(&st.agg[j]);
+        const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
+        const int stop = m2 ? __ffs(m2) - 1 : 31;
+        if (lane > stop) v = vzero(agg);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v = vadd(v, vshfl_xor(v, d));
+        excl = vadd(excl, v);
+        if (m2) break;
+        j -= 32;
+    }
+    if (lane == 0) {
+        vstore_volatile(&st.pre[tile], vadd(excl, agg));
+        __threadfence();
+        *(volatile int32_t *)&st.flag[tile] = 2;
+    }
     return excl;
 }
 

@@ -181,7 +181,10 @@ __global__ void __launch_bounds__(THREADS) k_build_scan(const double *n2, int64_
         V1 v{(t < count && n2[t] > 0.0) ? 1 : 0};
         V1 tot;
         V1 ex = block_excl_scan<V1, THREADS>(v, &tot, sw);
-        if (threadIdx.x == 0) s_excl = tile_lookback(st, tile, tot).x;
+        if (threadIdx.x < 32) {
+            int e = tile_lookback(st, tile, tot).x;
+            if (threadIdx.x == 0) s_excl = e;
+        }
         __syncthreads();
         if (t < count) slot_of[t] = v.x ? s_excl + ex.x : -1;
         __syncthreads();
