@@ -42,6 +42,7 @@ extern "C" {
 
 typedef struct spamm_ctx_s *spamm_ctx;
 typedef struct spamm_mat_s *spamm_mat;
+typedef struct spamm_comm_s *spamm_comm;
 
 typedef enum {
     SPAMM_OK = 0,
@@ -49,7 +50,7 @@ typedef enum {
     SPAMM_ESHAPE = 2,      /* operands differ in n or b                                 */
     SPAMM_ENOMEM = 3,      /* allocator returned NULL                                   */
     SPAMM_ECUDA = 4,       /* CUDA runtime / launch error                               */
-    SPAMM_ENCCL = 5,       /* reserved (multi-GPU)                                      */
+    SPAMM_ENCCL = 5,       /* NCCL unavailable or a collective failed                   */
     SPAMM_ENOTFINITE = 6,  /* non-finite root norm or trace error (history is kept)     */
     SPAMM_ECAPACITY = 7    /* internal capacity could not be grown                      */
 } spamm_status;
@@ -91,6 +92,60 @@ void spamm_ctx_destroy(spamm_ctx ctx);
 const char *spamm_last_error(spamm_ctx ctx);
 /* number of library kernels launched on this context since creation */
 int64_t spamm_kernel_launches(spamm_ctx ctx);
+
+/* ------------------------------------------------- row-partitioned path */
+/* SURVEY.md §8(e) / BASELINE.json north_star ("output block-rows are partitioned
+ * over GPUs; NCCL over NVLink all-gathers the operand blocks and norms each shard
+ * needs").  Output block rows are independent given (i) the complete leaf-norm
+ * arrays of both operands and (ii) the right operand's blocks the local tasks
+ * use (Eq. newspamm: C_ij = sum_k A_ik B_kj, k over all rows).  On a
+ * context with a communicator:
+ *   - every matrix stores only the rank's block rows [r0, r1) (pool, slot map),
+ *     while its squared-norm pyramid is complete and bitwise identical on all
+ *     ranks (leaf rows all-gathered after every build / product, pyramid summed
+ *     in the fixed order of the single-device path);
+ *   - spamm_multiply / spamm_ns_step / spamm_ns_sqrt cull only the local output
+ *     rows, fetch the remote right-operand blocks their tasks use (request lists
+ *     + grouped send/recv of packed blocks), run the leaf GEMM on local segments,
+ *     and all-gather the new leaf norms and the trace partials;
+ *   - spamm_build_tree* accept the full input (or any superset of the local rows)
+ *     and keep the local rows; readers (spamm_to_dense, spamm_export_blocks,
+ *     spamm_get_blocks, spamm_export_tasks, spamm_mat_info) see local rows only;
+ *     spamm_norm and spamm_level_norms2 are global.
+ * Each output block is computed by exactly one rank with the same k-order, so Y
+ * and Z are bitwise identical for every world size (tests/test_gpu_dist.py).
+ * All ranks must issue the same sequence of calls (SPMD); a failing rank leaves
+ * its peers blocked in the next collective. */
+
+/* NCCL unique id (128 opaque bytes) for spamm_comm_nccl_create; rank 0 draws it
+ * and the caller broadcasts it (the Python layer uses torch.distributed).  NCCL
+ * is loaded with dlopen (the libnccl.so.2 already in the process, else
+ * $SPAMM_NCCL_LIB, else the system one).  Errors: ENCCL. */
+spamm_status spamm_comm_nccl_unique_id(void *id128);
+/* One rank of an NCCL communicator on CUDA device `device` (owned by the
+ * returned handle; destroyed by spamm_comm_destroy). */
+spamm_status spamm_comm_nccl_create(const void *id128, int32_t rank, int32_t world, int32_t device,
+                                    spamm_comm *out);
+/* An in-process group of `world` ranks (comms[0..world-1]) for host threads that
+ * each drive their own context, possibly on the same device: collectives are
+ * stream-ordered device copies joined by host barriers and CUDA events (no
+ * kernel ever waits on another rank's kernel).  Used to check the partitioned
+ * path on one GPU; the arithmetic is the same as with NCCL. */
+spamm_status spamm_comm_local_group(int32_t world, spamm_comm *comms);
+void spamm_comm_destroy(spamm_comm comm);
+/* Attach a communicator (borrowed; NULL detaches) and the row partition:
+ * row_start[world+1] in leaf block rows, ascending, row_start[0] = 0,
+ * row_start[world] = nb of every matrix used (host pointer, copied; NULL =>
+ * equal split floor(p*nb/world) per matrix).  Matrices created before the
+ * call keep their partition.  Errors: EINVAL (bad partition / world). */
+spamm_status spamm_ctx_set_comm(spamm_ctx ctx, spamm_comm comm, const int32_t *row_start);
+/* Local block-row range [r0, r1) of m on this rank (single device: [0, nb)). */
+spamm_status spamm_mat_rows(spamm_mat m, int32_t *r0, int32_t *r1);
+/* Per-block-row leaf task counts of A (x)_tau B (rows i of the whole matrix, from
+ * the replicated norms only; no GEMM).  counts: [nb] int64, host.  For
+ * balancing a row partition on measured work. */
+spamm_status spamm_row_task_counts(spamm_ctx ctx, spamm_mat A, spamm_mat B, double tau,
+                                   int64_t *counts);
 
 /* ------------------------------------------------------------ quadtree */
 /* Build the quadtree of a dense n x n row-major matrix (host or device pointer):

@@ -29,6 +29,8 @@ __all__ = [
     "spamm_multiply", "spamm_export_tasks", "spamm_ns_step", "spamm_power_scale",
     "spamm_ns_y0", "spamm_identity", "spamm_ns_sqrt", "spamm_scale",
     "spamm_export_blocks", "spamm_profile_enable", "spamm_profile_read", "spamm_peak_dmma",
+    "Comm", "spamm_comm_nccl_unique_id", "spamm_comm_nccl_create", "spamm_comm_local_group",
+    "spamm_comm_destroy", "spamm_ctx_set_comm", "spamm_mat_rows", "spamm_row_task_counts",
 ]
 
 STATUS = {0: "SPAMM_OK", 1: "SPAMM_EINVAL", 2: "SPAMM_ESHAPE", 3: "SPAMM_ENOMEM",
@@ -113,6 +115,13 @@ def load():
         "spamm_profile_enable": (i32, [vp, i32]),
         "spamm_profile_read": (i32, [vp, P(spamm_profile_t)]),
         "spamm_peak_dmma": (i32, [vp, i64, P(dbl), P(dbl)]),
+        "spamm_comm_nccl_unique_id": (i32, [vp]),
+        "spamm_comm_nccl_create": (i32, [vp, i32, i32, i32, P(vp)]),
+        "spamm_comm_local_group": (i32, [i32, vp]),
+        "spamm_comm_destroy": (None, [vp]),
+        "spamm_ctx_set_comm": (i32, [vp, vp, vp]),
+        "spamm_mat_rows": (i32, [vp, P(i32), P(i32)]),
+        "spamm_row_task_counts": (i32, [vp, vp, vp, dbl, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -141,17 +150,25 @@ def _ptr(x):
 
 
 class Ctx:
-    """A library context bound to a CUDA device and (torch's current) stream."""
+    """A library context bound to a CUDA device and (torch's current) stream.
 
-    def __init__(self, device: int = 0, stream=None, torch_allocator: bool = True):
+    library_stream=True gives the context its own stream and the library's
+    cudaMallocAsync allocator (used when several host threads drive one device
+    each with its own context, e.g. the in-process rank group)."""
+
+    def __init__(self, device: int = 0, stream=None, torch_allocator: bool = True,
+                 library_stream: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise SpammError(4, "no CUDA device: the SpAMM library has no CPU path")
         L = load()
         self.torch = torch
         self.device = device
+        self.comm = None
         torch.cuda.set_device(device)
-        if stream is None:
+        if library_stream:
+            stream, torch_allocator = None, False
+        elif stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
         self._keep = []
@@ -173,7 +190,8 @@ class Ctx:
             self._keep = [a, _alloc, _free]
             alloc_p = C.byref(a)
         h = C.c_void_p()
-        rc = L.spamm_ctx_create(device, C.c_void_p(stream.cuda_stream), alloc_p, C.byref(h))
+        rc = L.spamm_ctx_create(device, C.c_void_p(stream.cuda_stream if stream is not None else None),
+                                alloc_p, C.byref(h))
         if rc:
             raise SpammError(rc, "spamm_ctx_create failed (device must be sm_100)")
         self.h = h
@@ -230,9 +248,76 @@ class Mat:
         return self.info()[2]
 
 
+class Comm:
+    """Owning handle of one rank of a communicator (NCCL or in-process group)."""
+
+    def __init__(self, h, rank: int, world: int, kind: str):
+        self.h, self.rank, self.world, self.kind = h, rank, world, kind
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            load().spamm_comm_destroy(self.h)
+            self.h = None
+
+
 # ------------------------------------------------------------------- calls
-def spamm_ctx_create(device: int = 0, stream=None, torch_allocator: bool = True) -> Ctx:
-    return Ctx(device, stream, torch_allocator)
+def spamm_ctx_create(device: int = 0, stream=None, torch_allocator: bool = True,
+                     library_stream: bool = False) -> Ctx:
+    return Ctx(device, stream, torch_allocator, library_stream)
+
+
+def spamm_comm_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = load().spamm_comm_nccl_unique_id(buf)
+    if rc:
+        raise SpammError(rc, "ncclGetUniqueId failed (NCCL not loadable?)")
+    return buf.raw
+
+
+def spamm_comm_nccl_create(uid: bytes, rank: int, world: int, device: int) -> Comm:
+    assert len(uid) == 128
+    h = C.c_void_p()
+    buf = C.create_string_buffer(uid, 128)
+    rc = load().spamm_comm_nccl_create(buf, rank, world, device, C.byref(h))
+    if rc:
+        raise SpammError(rc, f"ncclCommInitRank failed (rank {rank} of {world})")
+    return Comm(h, rank, world, "nccl")
+
+
+def spamm_comm_local_group(world: int) -> list:
+    hs = (C.c_void_p * world)()
+    rc = load().spamm_comm_local_group(world, hs)
+    if rc:
+        raise SpammError(rc, "spamm_comm_local_group failed")
+    return [Comm(C.c_void_p(hs[r]), r, world, "local") for r in range(world)]
+
+
+def spamm_comm_destroy(comm: Comm):
+    comm.destroy()
+
+
+def spamm_ctx_set_comm(ctx: Ctx, comm: Comm | None, row_start=None):
+    """Attach a communicator and the block-row partition (row_start[world+1], or
+    None for the equal split) to ctx; matrices built afterwards are row-partitioned."""
+    rs = None
+    if row_start is not None:
+        rs = np.ascontiguousarray(row_start, dtype=np.int32)
+        assert comm is not None and rs.shape == (comm.world + 1,)
+    ctx.check(load().spamm_ctx_set_comm(ctx.h, comm.h if comm is not None else None, _ptr(rs)))
+    ctx.comm = comm
+
+
+def spamm_mat_rows(m: Mat):
+    r0, r1 = C.c_int32(), C.c_int32()
+    m.ctx.check(load().spamm_mat_rows(m.h, C.byref(r0), C.byref(r1)))
+    return r0.value, r1.value
+
+
+def spamm_row_task_counts(ctx: Ctx, A: Mat, B: Mat, tau: float) -> np.ndarray:
+    nb = A.n // A.b
+    out = np.zeros(nb, dtype=np.int64)
+    ctx.check(load().spamm_row_task_counts(ctx.h, A.h, B.h, float(tau), _ptr(out)))
+    return out
 
 
 def spamm_ctx_destroy(ctx: Ctx):

@@ -20,6 +20,31 @@
 #include "../../include/spamm.h"
 
 #define SPAMM_MAX_L 15
+#define SPAMM_MAX_WORLD 64
+
+// Row partition of the leaf block rows over the ranks of a communicator
+// (SURVEY.md §8(e)): rank p owns block rows [rs[p], rs[p+1]).
+struct Parts {
+    int world;
+    int rs[SPAMM_MAX_WORLD + 1];
+};
+
+// Transport of the row-partitioned path (comm.cu): NCCL over NVLink, or an
+// in-process group of host threads (one context per thread) used to run G
+// ranks on one device for the determinism tests.  Both are stream-ordered on
+// the calling context's stream.
+struct spamm_comm_s {
+    int rank = 0, world = 1;
+    virtual ~spamm_comm_s() {}
+    // recv[p*bytes .. (p+1)*bytes) <- rank p's send (all ranks, rank order)
+    virtual spamm_status allgather(spamm_ctx ctx, const void *send, void *recv, size_t bytes) = 0;
+    // rank p receives scnt[p] bytes from send + soff[p]; from rank p, rcnt[p]
+    // bytes arrive at recv + roff[p] (offsets / counts in bytes, host arrays)
+    virtual spamm_status alltoallv(spamm_ctx ctx, const void *send, const size_t *soff,
+                                   const size_t *scnt, void *recv, const size_t *roff,
+                                   const size_t *rcnt) = 0;
+    virtual const char *kind() const = 0;
+};
 
 struct spamm_ctx_s {
     int device = 0;
@@ -38,6 +63,10 @@ struct spamm_ctx_s {
     int64_t *iscratch = nullptr;  // small device scratch (counters)
     double *hpinned = nullptr;    // pinned host scratch
     void *prof = nullptr;         // prof.cu state
+    // row-partitioned execution (dist.cu); comm == nullptr => single device
+    spamm_comm comm = nullptr;
+    std::vector<int> row_start;   // [world+1] block rows; empty => equal split per nb
+    struct Dist *dist = nullptr;  // exchange workspaces
 };
 
 struct spamm_mat_s {
@@ -49,6 +78,11 @@ struct spamm_mat_s {
     double *pool = nullptr;    // cap * b*b
     int32_t *coord = nullptr;  // cap
     int64_t nblk = 0, cap = 0;
+    // row partition: this rank stores block rows [r0, r1); the norm pyramid and
+    // the leaf-norm level are complete (replicated) on every rank.
+    int r0 = 0, r1 = 0;
+    bool dist = false;
+    Parts parts{};
 };
 
 // ------------------------------------------------------------------ memory
@@ -148,6 +182,17 @@ spamm_status mat_map(spamm_ctx ctx, spamm_mat src, int op, double c, double mu, 
 spamm_status leaf_norms_from_pool(spamm_ctx ctx, spamm_mat m);  // recompute leaf norm2 from pool
 int is_device_ptr(const void *p);
 
+// dist.cu — the row-partitioned path
+spamm_status mat_parts(spamm_ctx ctx, int nb, Parts *p);          // partition of nb block rows
+// leaf norms of the local rows -> replicated on all ranks, then the pyramid
+spamm_status norms_finish(spamm_ctx ctx, spamm_mat m);
+// gather rows of a vector laid out as nb rows x width (row-major) across ranks
+spamm_status gather_rows(spamm_ctx ctx, const Parts &p, double *vec, int width);
+// fetch the remote right-operand blocks the local tasks of cw use; patches
+// cw->tB (remote => -(h+1), h = halo slot) and returns the halo pool
+spamm_status halo_exchange(spamm_ctx ctx, struct Cull *cw, spamm_mat B, double **halo, int64_t *nhalo);
+void dist_free(spamm_ctx ctx);
+
 // cull.cu — the level-by-level two-sided norm query (Eq. newspamm)
 enum { CNT_OVERFLOW = 16, CNT_NSEG = 17, CNT_TICKET = 20, CNT_GEMM_TICKET = 48 };  // counters[] layout; [0..15] = level counts
 struct Cull {
@@ -171,14 +216,14 @@ struct Cull {
 };
 // Enqueue the query, synchronise once to read the counts, and grow + re-run
 // on capacity overflow.
-spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau);
+spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1);
 void cull_free(spamm_ctx ctx, Cull *cw);
 spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj_host, int64_t cap, int64_t *n);
 
 // gemm.cu — FP64 DMMA leaf GEMM with fused epilogues
 enum { EPI_STORE = 0, EPI_NS_H = 1 };
-spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_mat C, int epi,
-                      double *trace_part);
+spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
+                      spamm_mat C, int epi, double *trace_part);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg);
 // append value*I blocks for absent diagonal positions at slots base..; *added = count (syncs)
 spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value, int64_t *added);

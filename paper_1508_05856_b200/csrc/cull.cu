@@ -29,7 +29,16 @@ struct CullArgs {
     const int32_t *a_slot, *b_slot;
     double tau;
     int64_t cap;
+    int L, r0, r1;               // leaf level; output block rows [r0, r1) (row partition, §8(e))
 };
+
+// level-`lev` row index I covers leaf rows [I << (L-lev), (I+1) << (L-lev)); keep the
+// sub-volume only if that range meets the local output rows
+__device__ __forceinline__ bool rows_meet(const CullArgs &g, int I, int lev)
+{
+    const int sh = g.L - lev;
+    return ((I + 1) << sh) > g.r0 && (I << sh) < g.r1;
+}
 
 __device__ __forceinline__ double cull_T(const CullArgs &g)
 {
@@ -69,7 +78,7 @@ __global__ void __launch_bounds__(1024) k_cull_init(CullArgs g, int l0, int4 *re
             uint32_t code = idx / S;
             int K = idx % S;
             int I = morton_i(code), J = morton_j(code);
-            f[e] = keep(an[morton(I, K)], bn[morton(K, J)], T);
+            f[e] = rows_meet(g, I, l0) && keep(an[morton(I, K)], bn[morton(K, J)], T);
         }
         mycount += f[e];
     }
@@ -141,12 +150,14 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
             double pa[2][2] = {{a01.x, a01.y}, {a23.x, a23.y}};  // [di][dk]
             double pb[2][2] = {{b01.x, b01.y}, {b23.x, b23.y}};  // [dk][dj]
 #pragma unroll
-            for (int di = 0; di < 2; di++)
+            for (int di = 0; di < 2; di++) {
+                if (!rows_meet(g, 2 * I + di, l + 1)) continue;
 #pragma unroll
                 for (int dj = 0; dj < 2; dj++)
 #pragma unroll
                     for (int dk = 0; dk < 2; dk++)
                         if (keep(pa[di][dk], pb[dk][dj], T)) m |= 1u << (2 * ((di << 1) | dj) + dk);
+            }
             c = make_int4(__popc(m & 3u), __popc((m >> 2) & 3u), __popc((m >> 4) & 3u),
                           __popc((m >> 6) & 3u));
             mask[t] = (uint8_t)m;
@@ -330,14 +341,15 @@ static spamm_status cull_alloc(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap
 }
 
 // Enqueue the whole query (no host sync).
-static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau)
+static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0,
+                                 int r1)
 {
     const int L = A->L;
     const int l0 = L < 4 ? L : 4;
     cw->L = L;
     cw->l0 = l0;
     cw->b = A->b;
-    CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap};
+    CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap, L, r0, r1};
     cudaStream_t s = ctx->stream;
     CK(cudaMemsetAsync(cw->counters, 0, sizeof(int32_t) * 64, s));
     CK(cudaMemsetAsync(cw->tile_flag, 0, sizeof(int32_t) * (SPAMM_MAX_L + 2) * cw->tiles, s));
@@ -378,7 +390,7 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     return SPAMM_OK;
 }
 
-spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau)
+spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1)
 {
     int64_t nb = A->nb;
     int64_t want = cw->hint > 0 ? cw->hint : (int64_t)1 << 16;
@@ -387,7 +399,7 @@ spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double 
         ST(cull_alloc(ctx, cw, cap, nb * nb));
     }
     for (int attempt = 0; attempt < 8; attempt++) {
-        ST(cull_enqueue(ctx, cw, A, B, tau));
+        ST(cull_enqueue(ctx, cw, A, B, tau, r0, r1));
         CK(cudaMemcpyAsync(cw->hcnt, cw->counters, sizeof(int32_t) * 64, cudaMemcpyDeviceToHost,
                            ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -438,4 +450,33 @@ spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj, int64_t cap, int
     }
     cudaFreeHost(h);
     return SPAMM_OK;
+}
+
+// Per-row leaf task counts of A (x)_tau B over ALL rows (norms are replicated on
+// every rank), for balancing a row partition on measured work.
+extern "C" spamm_status spamm_row_task_counts(spamm_ctx ctx, spamm_mat A, spamm_mat B, double tau,
+                                              int64_t *counts)
+{
+    if (!ctx || !A || !B || !counts) return set_err(ctx, SPAMM_EINVAL, "NULL argument");
+    if (A->n != B->n || A->b != B->b) return set_err(ctx, SPAMM_ESHAPE, "shape mismatch");
+    if (!(tau >= 0.0)) return set_err(ctx, SPAMM_EINVAL, "tau must be >= 0");
+    Cull *cw = new Cull();
+    spamm_status st = cull_run(ctx, cw, A, B, tau, 0, A->nb);
+    if (ctx->last == cw) ctx->last = nullptr;
+    std::vector<int32_t> code(cw->nsegs), len(cw->nsegs);
+    if (!st && cw->nsegs) {
+        cudaMemcpyAsync(code.data(), cw->seg_code, sizeof(int32_t) * cw->nsegs, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(len.data(), cw->seg_len, sizeof(int32_t) * cw->nsegs, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) st = check_cuda(ctx, e, "row task counts");
+    }
+    if (!st) {
+        for (int i = 0; i < A->nb; i++) counts[i] = 0;
+        for (int64_t t = 0; t < cw->nsegs; t++) counts[morton_i((uint32_t)code[t])] += len[t];
+    }
+    cull_free(ctx, cw);
+    dev_free(ctx, cw->counters, sizeof(int32_t) * 64);
+    if (cw->hcnt) cudaFreeHost(cw->hcnt);
+    delete cw;
+    return st;
 }

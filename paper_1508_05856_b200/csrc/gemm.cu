@@ -21,6 +21,7 @@
 
 struct GemmArgs {
     const double *a_pool, *b_pool;
+    const double *b_halo;   // remote right-operand tiles (row partition): tB = -(h+1)
     const int32_t *tA, *tB;
     const int32_t *seg_code, *seg_start, *seg_len;
     int nseg;
@@ -150,8 +151,9 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
                         mbar_wait(&empty[stage], phase ^ 1);
                         mbar_expect_tx(&full[stage], 2 * TILE_BYTES);
                         bulk_g2s(smem + (2 * stage) * TILE, g.a_pool + (int64_t)a * TILE, TILE_BYTES, &full[stage]);
-                        bulk_g2s(smem + (2 * stage + 1) * TILE, g.b_pool + (int64_t)b * TILE, TILE_BYTES,
-                                 &full[stage]);
+                        const double *bsrc = b >= 0 ? g.b_pool + (int64_t)b * TILE
+                                                    : g.b_halo + (int64_t)(-b - 1) * TILE;
+                        bulk_g2s(smem + (2 * stage + 1) * TILE, bsrc, TILE_BYTES, &full[stage]);
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -319,10 +321,10 @@ static spamm_status gemm_dispatch(spamm_ctx ctx, int b, const GemmArgs &g)
     }
 }
 
-spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_mat C, int epi,
-                      double *trace_part)
+spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
+                      spamm_mat C, int epi, double *trace_part)
 {
-    GemmArgs g{A->pool, B->pool, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
+    GemmArgs g{A->pool, B->pool, b_halo, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
                (int)cw->nsegs, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
                cw->counters + CNT_GEMM_TICKET};
     if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H>(ctx, A->b, g);
@@ -333,7 +335,7 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_m
 // H_ii = 1.5 I where X had no surviving task (i,i) (K6): slots appended at
 // nseg.. in ascending i (single-CTA scan, deterministic), then filled in parallel.
 template <int THREADS>
-__global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int64_t base,
+__global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int r0, int r1, int64_t base,
                               int32_t *newslot, int64_t *count_out)
 {
     __shared__ V1 sw[THREADS / 32];
@@ -341,7 +343,7 @@ __global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int64_t
     for (int i0 = 0; i0 < nb; i0 += THREADS) {
         int i = i0 + threadIdx.x;
         uint32_t code = i < nb ? morton(i, i) : 0;
-        V1 v{(i < nb && slot_map[code] < 0) ? 1 : 0};
+        V1 v{(i >= r0 && i < r1 && slot_map[code] < 0) ? 1 : 0};
         V1 tot;
         V1 ex = block_excl_scan<V1, THREADS>(v, &tot, sw);
         if (i < nb) {
@@ -377,7 +379,7 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
 {
     int32_t *newslot = dalloc<int32_t>(ctx, m->nb);
     if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
-    k_diag_assign<1024><<<1, 1024, 0, ctx->stream>>>(m->slot, m->coord, m->nb, base, newslot,
+    k_diag_assign<1024><<<1, 1024, 0, ctx->stream>>>(m->slot, m->coord, m->nb, m->r0, m->r1, base, newslot,
                                                     ctx->iscratch);
     CKL(ctx);
     k_diag_fill<<<m->nb, 256, 0, ctx->stream>>>(newslot, m->pool, m->b, value, m->norm2 + pyr_off(m->L));

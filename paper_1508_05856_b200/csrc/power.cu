@@ -175,19 +175,22 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     k_row_fill<<<nb, 256, 0, st>>>(s->slot, nb, rowptr, cols, slots);
     k_fill<<<cdiv(n, 256), 256, 0, st>>>(v, n, 1.0 / sqrt((double)n));
     ctx->launches += 4;
-    auto mv = [&](const double *x, double *y) {
+    // row partition: local block rows of w = s v, then all ranks gather the full w
+    // (each row is computed by one rank with the single-device kernel: bitwise G-invariant)
+    auto mv = [&](const double *x, double *y) -> spamm_status {
         switch (s->b) {
         case 16: spmv<16>(ctx, s, rowptr, cols, slots, x, y); break;
         case 32: spmv<32>(ctx, s, rowptr, cols, slots, x, y); break;
         default: spmv<64>(ctx, s, rowptr, cols, slots, x, y); break;
         }
+        return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
     };
     for (int it = 0; it < K; it++) {
-        mv(v, w);
+        ST(mv(v, w));
         k_normalize<<<1, 1024, 0, st>>>(w, n, v);
         ctx->launches++;
     }
-    mv(v, w);
+    ST(mv(v, w));
     k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
     CKL(ctx);
     double h = 0;

@@ -59,6 +59,7 @@ extern "C" void spamm_ctx_destroy(spamm_ctx ctx)
 {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
+    dist_free(ctx);
     for (int i = 0; i < 3; i++) {
         if (!ctx->cw[i]) continue;
         cull_free(ctx, ctx->cw[i]);
@@ -92,25 +93,45 @@ static spamm_status check_pair(spamm_ctx ctx, spamm_mat A, spamm_mat B, double t
 static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
                             double *trace_part, spamm_mat *C)
 {
+    if (A->dist != B->dist || A->r0 != B->r0 || A->r1 != B->r1)
+        return set_err(ctx, SPAMM_ESHAPE, "operands have different row partitions");
     int pc = prof_begin(ctx, SPAMM_PH_CULL);
-    spamm_status sc = cull_run(ctx, cw, A, B, tau);
+    spamm_status sc = cull_run(ctx, cw, A, B, tau, A->r0, A->r1);
     prof_end(ctx, pc);
     if (sc) return sc;
+    // row partition: fetch the remote right-operand tiles the local tasks use
+    double *halo = nullptr;
+    int64_t nhalo = 0;
+    if (A->dist) {
+        int px = prof_begin(ctx, SPAMM_PH_OTHER);
+        sc = halo_exchange(ctx, cw, B, &halo, &nhalo);
+        prof_end(ctx, px);
+        if (sc) return sc;
+    }
     int64_t extra = (epi == EPI_NS_H) ? A->nb : 0;
     spamm_mat m;
-    ST(mat_new(ctx, A->n, A->b, cw->nsegs + extra, &m));
-    spamm_status st = mat_reset_pattern(ctx, m);
+    spamm_status st = mat_new(ctx, A->n, A->b, cw->nsegs + extra, &m);
+    if (!st && (m->r0 != A->r0 || m->r1 != A->r1)) {
+        spamm_mat_free(m);
+        st = set_err(ctx, SPAMM_EINVAL, "context partition changed since the operands were built");
+    }
+    if (st) {
+        dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
+        return st;
+    }
+    st = mat_reset_pattern(ctx, m);
     if (!st) {
         int pg = prof_begin(ctx, SPAMM_PH_GEMM);
-        st = gemm_run(ctx, cw, A, B, m, epi, trace_part);
+        st = gemm_run(ctx, cw, A, B, halo, m, epi, trace_part);
         prof_end(ctx, pg);
         prof_gemm_work(ctx, cw->ntasks, cw->nsegs, A->b);
     }
+    dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
     if (!st) {
         m->nblk = cw->nsegs;
         if (epi == EPI_NS_H) st = diag_fixup(ctx, m, cw->nsegs);
     }
-    if (!st) st = pyramid_build(ctx, m);
+    if (!st) st = norms_finish(ctx, m);
     if (st) {
         spamm_mat_free(m);
         return st;
@@ -153,6 +174,8 @@ extern "C" spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, d
     spamm_mat H = nullptr, Yn = nullptr, Zn = nullptr;
     // X = Z (x)_tau Y  ->  H = 1/2 (3I - X), tr X partials (X never stored)
     spamm_status st = product(ctx, ctx->cw[0], Z, Y, tau, EPI_NS_H, trace_part, &H);
+    // row partition: every rank gets all tr(X_ii) partials, summed in the fixed order
+    if (!st && H->dist) st = gather_rows(ctx, H->parts, trace_part, 1);
     if (!st) st = trace_finish(ctx, trace_part, nb, Y->n, ctx->dscratch);
     if (!st && stats) stats[0] = ctx->cw[0]->stats;
     // Y' = Y (x)_tau_s H ; Z' = H (x)_tau Z

@@ -77,10 +77,16 @@ spamm_status mat_new(spamm_ctx ctx, int64_t n, int b, int64_t cap, spamm_mat *ou
     int L = 0;
     while ((int64_t(1) << L) < nb) L++;
     if (L > SPAMM_MAX_L) return set_err(ctx, SPAMM_EINVAL, "n/b too large");
+    Parts parts;
+    ST(mat_parts(ctx, (int)nb, &parts));
     spamm_mat m = new spamm_mat_s();
     m->ctx = ctx;
     m->n = n; m->b = b; m->nb = (int)nb; m->L = L;
     m->cap = cap;
+    m->parts = parts;
+    m->dist = ctx->comm != nullptr;
+    m->r0 = m->dist ? parts.rs[ctx->comm->rank] : 0;
+    m->r1 = m->dist ? parts.rs[ctx->comm->rank + 1] : (int)nb;
     m->norm2 = dalloc<double>(ctx, pyr_size(L));
     m->slot = dalloc<int32_t>(ctx, nb * nb);
     m->pool = dalloc<double>(ctx, cap * b * b);
@@ -170,15 +176,18 @@ __global__ void k_block_norm2(BlockSrc src, int64_t count, double *n2)
 // Order-preserving compaction of present blocks (n2 > 0): exclusive scan of the
 // present flags gives the pool slot; the block is copied and registered.
 template <int THREADS>
-__global__ void __launch_bounds__(THREADS) k_build_scan(const double *n2, int64_t count,
-                                                        ScanTiles<V1> st, int32_t *slot_of)
+__global__ void __launch_bounds__(THREADS) k_build_scan(BlockSrc src, const double *n2, int64_t count,
+                                                        int r0, int r1, ScanTiles<V1> st, int32_t *slot_of)
 {
     __shared__ V1 sw[THREADS / 32];
     __shared__ int s_tile, s_excl;
     int tile;
     while ((tile = next_tile(st.ticket, count, THREADS, &s_tile)) >= 0) {
         int64_t t = (int64_t)tile * THREADS + threadIdx.x;
-        V1 v{(t < count && n2[t] > 0.0) ? 1 : 0};
+        int I = 0, J = 0;
+        if (t < count) src.coords(t, I, J);
+        // present (reading L6) and in the local block rows (row partition, §8(e))
+        V1 v{(t < count && n2[t] > 0.0 && I >= r0 && I < r1) ? 1 : 0};
         V1 tot;
         V1 ex = block_excl_scan<V1, THREADS>(v, &tot, sw);
         if (threadIdx.x < 32) {
@@ -278,6 +287,10 @@ spamm_status pyramid_build(spamm_ctx ctx, spamm_mat m) { return pyramid_kernels(
 static spamm_status build_common(spamm_ctx ctx, BlockSrc src, int64_t count, int64_t n, int b,
                                  spamm_mat *out)
 {
+    Parts parts;
+    ST(mat_parts(ctx, (int)(n / b), &parts));
+    const int r0 = ctx->comm ? parts.rs[ctx->comm->rank] : 0;
+    const int r1 = ctx->comm ? parts.rs[ctx->comm->rank + 1] : (int)(n / b);
     // 1. per-candidate squared norms
     double *n2 = dalloc<double>(ctx, count);
     int32_t *slot_of = dalloc<int32_t>(ctx, count);
@@ -298,7 +311,7 @@ static spamm_status build_common(spamm_ctx ctx, BlockSrc src, int64_t count, int
             }
             ScanTiles<V1> tiles{flags, agg, pre, flags + ntiles};
             int grid = ntiles < 2 * ctx->sm_count ? ntiles : 2 * ctx->sm_count;
-            k_build_scan<512><<<grid, 512, 0, ctx->stream>>>(n2, count, tiles, slot_of);
+            k_build_scan<512><<<grid, 512, 0, ctx->stream>>>(src, n2, count, r0, r1, tiles, slot_of);
             ctx->launches++;
             // total present = last tile inclusive prefix
             V1 last;
@@ -320,7 +333,7 @@ static spamm_status build_common(spamm_ctx ctx, BlockSrc src, int64_t count, int
                 src, count, slot_of, n2, m->L, m->pool, m->coord, m->slot, m->norm2 + pyr_off(m->L));
             ctx->launches++;
         }
-        st = pyramid_build(ctx, m);
+        st = norms_finish(ctx, m);
     } while (0);
     dev_free(ctx, n2, sizeof(double) * count);
     dev_free(ctx, slot_of, sizeof(int32_t) * count);
@@ -480,7 +493,7 @@ spamm_status mat_map(spamm_ctx ctx, spamm_mat src, int op, double c, double mu, 
             st = leaf_norms_from_pool(ctx, m);
         }
         if (st) break;
-        st = pyramid_build(ctx, m);
+        st = norms_finish(ctx, m);
     } while (0);
     if (st) {
         spamm_mat_free(m);
