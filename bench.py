@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", default="equal", choices=["equal", "balanced"],
+                    help="row partition for --gpus > 1 (balanced: on s (x) s per-row task counts)")
+    ap.add_argument("--dist-world1", action="store_true",
+                    help="run the row-partitioned NCCL path even at world size 1 (path check)")
     ap.add_argument("--ref-iters", type=int, default=1,
                     help="NS iterations of one oracle sample step (reference arm / cpu_baseline)")
     return ap.parse_args()
@@ -124,7 +128,7 @@ def workload_name(cfg, tau, iters):
             f"{iters} dual NS iterations")
 
 
-def oracle_sample(cfg, payload, tau, iters, scale):
+def oracle_sample(cfg, payload, tau, iters, scale, tau_s=None):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload:
     build + Y0 (given scale) + `iters` NS iterations.  Returns (seconds, flops)."""
     import oracle as O
@@ -133,7 +137,7 @@ def oracle_sample(cfg, payload, tau, iters, scale):
         So = O.OMat.from_dense(payload, cfg.b)
     else:
         So = O.OMat.from_blocks(cfg.n, cfg.b, *payload)
-    r = O.ns_sqrt(So, tau, iters, scale=scale, mu=cfg.mu)
+    r = O.ns_sqrt(So, tau, iters, tau_s=tau_s, scale=scale, mu=cfg.mu)
     dt = time.perf_counter() - t0
     flops = float(r["counts"].sum()) * 2.0 * cfg.b ** 3
     return dt, flops, O.num_threads()
@@ -157,10 +161,10 @@ def run_reference(args):
     c = O.power_scale(So, 100)
     del So
     for _ in range(args.warmup):
-        oracle_sample(cfg, payload, tau, args.ref_iters, c)
+        oracle_sample(cfg, payload, tau, args.ref_iters, c, tau * cfg.tau_s_factor)
     tot_t, tot_f, cores = 0.0, 0.0, 1
     for _ in range(args.steps):
-        dt, fl, cores = oracle_sample(cfg, payload, tau, args.ref_iters, c)
+        dt, fl, cores = oracle_sample(cfg, payload, tau, args.ref_iters, c, tau * cfg.tau_s_factor)
         tot_t += dt
         tot_f += fl
     value = tot_f / tot_t / 1e12
@@ -169,7 +173,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": workload_name(cfg, tau, iters), "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -183,22 +187,49 @@ def run_reference(args):
 def run_ours(args):
     import torch
     import paper_1508_05856_b200 as sp
+    from paper_1508_05856_b200 import dist as D
 
     ws, rank, local = dist_env()
     dist = None
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if ws > 1 or args.dist_world1:
+        import torch.distributed as dist
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        dist.init_process_group("nccl", device_id=dev)
     cfg = si.CONFIGS[args.config]
     tau = args.tau if args.tau is not None else cfg.tau
     iters = args.iters if args.iters is not None else cfg.iters
-    kind, payload = si.make_input(cfg)
-    assert kind == "blocks" or cfg.kind == "kms"
+    tau_s = tau * cfg.tau_s_factor
+    t_stop = cfg.t_stop
+    nb = cfg.n // cfg.b
+
+    # ---- row partition over the ranks; fixed for the run
+    comm, row_start, rows = None, None, (0, nb)
+    if dist is not None:
+        comm = D.init_nccl_comm(local)
+        if args.partition == "balanced":
+            # per-row leaf task counts of s (x)_tau s from the replicated norms (setup, untimed)
+            kind, full = si.make_input(cfg)
+            c0 = sp.spamm_ctx_create(local)
+            S0 = (sp.spamm_build_tree(c0, torch.from_numpy(full).to(dev), cfg.b) if kind == "dense" else
+                  sp.spamm_build_tree_blocks(c0, cfg.n, cfg.b, *(torch.from_numpy(x).to(dev) for x in full)))
+            row_start = D.balanced_partition(sp.spamm_row_task_counts(c0, S0, S0, tau), ws)
+            S0.free()
+            c0.close()
+            del full
+        else:
+            row_start = D.equal_partition(nb, ws)
+        rows = (row_start[rank], row_start[rank + 1])
+    kind, payload = si.make_input(cfg, rows=rows if comm is not None else None)
     ctx = sp.spamm_ctx_create(local)
+    if comm is not None:
+        sp.spamm_ctx_set_comm(ctx, comm, row_start)
     stream = ctx.stream
-    dev = torch.device(f"cuda:{local}")
 
     if kind == "dense":
         d_in = (torch.from_numpy(payload).to(dev),)
@@ -219,7 +250,7 @@ def run_ours(args):
 
     def step(inp, readback):
         S = build(inp)
-        r = sp.spamm_ns_sqrt(ctx, S, tau, iters, mu=cfg.mu)
+        r = sp.spamm_ns_sqrt(ctx, S, tau, iters, tau_s=tau_s, mu=cfg.mu, t_stop=t_stop)
         S.free()
         flops = sum(p["flops"] for k in r["stats"] for p in k)
         tasks = sum(p["tasks"] for k in r["stats"] for p in k)
@@ -243,20 +274,6 @@ def run_ours(args):
     def barrier():
         if dist is not None:
             dist.barrier()
-
-    def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
 
     # ---- FP64 tensor peak on this GPU (DMMA issue-rate microbenchmark, ~2 s sustained)
     _, ms1 = sp.spamm_peak_dmma(ctx, 20000)
@@ -291,9 +308,11 @@ def run_ours(args):
     launches = sp.spamm_kernel_launches(ctx) - l0
     prof = sp.spamm_profile_read(ctx)
     sp.spamm_profile_enable(ctx, False)
-    ms_max = max_over_ranks(ms)
-    flops_all = sum_over_ranks(flops)
+    ms_max = D.max_over_ranks(ms, dev)
+    flops_all = D.sum_over_ranks(flops, dev)
+    tasks_all = D.sum_over_ranks(tasks, dev)
     value = flops_all / (ms_max * 1e-3) / 1e12
+    rank_tasks = D.gather_to_rank0(tasks / args.steps)
 
     # ---- roofline of the dominant kernel (leaf GEMM), algorithmic flops / event time
     gemm_achieved = prof["gemm_flops"] / (prof["gemm_ms"] * 1e-3) / 1e12 if prof["gemm_ms"] else None
@@ -310,7 +329,9 @@ def run_ours(args):
     traffic_file = os.path.join(ROOT, "profiles", f"gemm_traffic_{args.config}.json")
     if os.path.exists(traffic_file):
         try:
-            roofline["traffic"] = json.load(open(traffic_file)).get("bytes_per_launch")
+            tf = json.load(open(traffic_file))
+            roofline["traffic"] = tf.get("bytes_per_launch")
+            roofline["traffic_source"] = tf.get("source")
         except (OSError, ValueError):
             pass
 
@@ -331,9 +352,10 @@ def run_ours(args):
         e3.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ems = max_over_ranks(e2.elapsed_time(e3))
-        e2e = {"value": sum_over_ranks(ef) / (ems * 1e-3) / 1e12, "unit": UNIT,
-               "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(d2h),
+        ems = D.max_over_ranks(e2.elapsed_time(e3), dev)
+        e2e = {"value": D.sum_over_ranks(ef, dev) / (ems * 1e-3) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": int(D.sum_over_ranks(in_bytes, dev)),
+               "d2h_bytes_per_step": int(D.sum_over_ranks(d2h, dev)),
                "ms_per_step": ems / args.steps}
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
@@ -342,35 +364,45 @@ def run_ours(args):
         S = build(d_in)
         c = sp.spamm_power_scale(ctx, S, 100)
         S.free()
-        dt, fl, cores = oracle_sample(cfg, payload, tau, args.ref_iters, c)
+        dt, fl, cores = oracle_sample(cfg, payload, tau, args.ref_iters, c, tau_s)
         cpu = {"value": fl / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{args.config} input: oracle quadtree build + Y0 + first {args.ref_iters} "
                          f"of {iters} NS iterations ({fl:.3g} culled-leaf flop in {dt:.1f} s)"}
 
+    blocks_mb = D.sum_over_ranks(in_bytes, dev) / 1e6
     if rank == 0:
         r = last
-        blocks_mb = in_bytes / 1e6
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
                 "workload": workload_name(cfg, tau, iters), "n": cfg.n, "leaf": cfg.b, "tau": tau,
-                "iters": iters, "parallelism": "replicas" if ws > 1 else "single",
-                "l2": f"inputs larger than L2 (s = {blocks_mb:.0f} MB of blocks, iterates > 126 MB)",
+                "tau_s": tau_s, "iters": iters, "t_stop": t_stop,
+                "parallelism": (f"row-partitioned over {ws} GPUs ({args.partition} split), NCCL halo "
+                                "exchange + norm all-gather") if comm is not None else "single",
+                "l2": f"inputs larger than L2 (s ~ {blocks_mb:.0f} MB of blocks, iterates > 126 MB)",
             },
-            "s_per_ns_iteration": prof["loop_ms"] / args.steps / iters / 1e3,
+            "iters_run": int(r["iters"]),
+            "s_per_ns_iteration": prof["loop_ms"] / args.steps / max(int(r["iters"]), 1) / 1e3,
             "setup_ms_per_step": prof["setup_ms"] / args.steps,
-            "tasks_per_step": tasks / args.steps,
-            "t_final": float(r["t"][-1]),
+            "tasks_per_step": tasks_all / args.steps,
+            "t_final": float(r["t"][-1]) if len(r["t"]) else None,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
-            "phase_ms_per_step": {k: prof[f"{k}_ms"] / args.steps for k in ("gemm", "cull", "setup", "loop")},
+            "phase_ms_per_step": {k: prof[f"{k}_ms"] / args.steps
+                                  for k in ("gemm", "cull", "setup", "loop", "other")},
         }
+        if comm is not None:
+            line["partition"] = {"row_start": row_start, "tasks_per_rank": rank_tasks,
+                                 "imbalance": max(rank_tasks) / (sum(rank_tasks) / ws)}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        ctx.close()
+        comm.destroy()
     if dist is not None:
         dist.destroy_process_group()
     return 0

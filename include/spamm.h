@@ -81,6 +81,12 @@ typedef struct {
     double *t_history;      /* [iters] trace errors t_k, nullable                        */
     spamm_stats *per_product;/* [3*iters] stats of X, Y', Z' per k, nullable             */
     double *c_out;          /* scale actually used, nullable                             */
+    double t_stop;          /* > 0 => stop after the first k with |t_k| <= t_stop (convergence
+                               monitored by the trace error); 0 => run all iters  */
+    int32_t *iters_done;    /* number of NS steps actually run, nullable                 */
+    int32_t map;            /* 0: H = 1/2 (3I - X) (north_star, alpha = 1, eps = 0);
+                               1: scaled + stabilised H = h_alpha[(1-2eps) X + eps I] with the
+                               paper's sigmoids alpha(t_k), eps(t_k)             */
 } spamm_ns_opts;
 
 /* ---------------------------------------------------------------- context */
@@ -190,6 +196,16 @@ spamm_status spamm_export_tasks(spamm_ctx ctx, int32_t *ikj, int64_t cap, int64_
 spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
                            spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
                            double *t_k /* host, nullable */, spamm_stats stats[3] /* nullable */);
+/* spamm_ns_step with a choice of NS map (see spamm_ns_opts.map):
+ *   map 1: x~ = (1 - 2 eps) X + eps I, H = sqrt(alpha)/2 (3I - alpha x~), with
+ *   alpha(t) = 1 + 1.85/(1 + e^{-50(t-.35)}), eps(t) = .1/(1 + e^{-75(t-.30)}) evaluated
+ *   on the device at t = t_k.  X is stored by the GEMM epilogue and mapped
+ *   in place by a second pass (the coefficients need the complete trace).
+ *   alpha_eps: host [2] (alpha, eps) used, nullable.  Errors as spamm_ns_step, plus
+ *   EINVAL for map not in {0, 1}. */
+spamm_status spamm_ns_step_map(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
+                               int32_t map, spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
+                               double *t_k, spamm_stats stats[3], double *alpha_eps);
 /* Scale estimate c ~ ||s||_2: K power steps from 1/sqrt(n) * ones, Rayleigh quotient. */
 spamm_status spamm_power_scale(spamm_ctx ctx, spamm_mat s, int32_t K, double *c);
 /* Y0 = s/c (mu = 0) or (s/c + mu I)/(1+mu). */

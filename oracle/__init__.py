@@ -68,8 +68,11 @@ def lib():
             "or_power_scale": (dbl, [vp, i32]),
             "or_ns_step": (i32, [vp, vp, dbl, dbl, P(vp), P(vp), P(vp), P(dbl), vp]),
             "or_ns_y0": (vp, [vp, dbl, dbl]),
-            "or_ns_sqrt": (i32, [vp, dbl, dbl, i32, dbl, i32, dbl, P(vp), P(vp), vp, vp,
-                                 P(dbl)]),
+            "or_ns_sqrt": (i32, [vp, dbl, dbl, i32, dbl, i32, dbl, dbl, i32, P(vp), P(vp), vp, vp,
+                                 P(dbl), P(C.c_int)]),
+            "or_ns_step_map": (i32, [vp, vp, dbl, dbl, i32, P(vp), P(vp), P(vp), P(dbl), vp]),
+            "or_alpha": (dbl, [dbl]),
+            "or_eps": (dbl, [dbl]),
             "or_num_threads": (i32, []),
         }
         for name, (res, args) in sig.items():
@@ -195,13 +198,13 @@ def ns_y0(s: OMat, c: float, mu: float = 0.0) -> OMat:
     return OMat(lib().or_ns_y0(s.h, c, mu))
 
 
-def ns_step(Y: OMat, Z: OMat, tau: float, tau_s: float | None = None):
+def ns_step(Y: OMat, Z: OMat, tau: float, tau_s: float | None = None, scaled: bool = False):
     """One dual NS step (north_star form). Returns (Y', Z', H, t, counts[3])."""
     tau_s = tau if tau_s is None else tau_s
     yn, zn, hn = C.c_void_p(), C.c_void_p(), C.c_void_p()
     t = C.c_double(0)
     counts = np.zeros(3, dtype=np.int64)
-    rc = lib().or_ns_step(Y.h, Z.h, tau, tau_s, C.byref(yn), C.byref(zn), C.byref(hn),
+    rc = lib().or_ns_step_map(Y.h, Z.h, tau, tau_s, int(scaled), C.byref(yn), C.byref(zn), C.byref(hn),
                           C.byref(t), _ptr(counts))
     out = (OMat(yn.value), OMat(zn.value), OMat(hn.value), t.value, counts)
     if rc:
@@ -210,18 +213,32 @@ def ns_step(Y: OMat, Z: OMat, tau: float, tau_s: float | None = None):
 
 
 def ns_sqrt(s: OMat, tau: float, iters: int, tau_s: float | None = None,
-            scale: float = 0.0, mu: float = 0.0, power_iters: int = 100):
-    """Full dual NS run. Returns dict(Y, Z, t, counts, c, rc)."""
+            scale: float = 0.0, mu: float = 0.0, power_iters: int = 100, t_stop: float = 0.0,
+            scaled: bool = False):
+    """Full dual NS run. Returns dict(Y, Z, t, counts, c, rc, iters); t_stop > 0 stops
+    after the first k with |t_k| <= t_stop (t, counts then cover the steps run)."""
     tau_s = tau if tau_s is None else tau_s
     yo, zo = C.c_void_p(), C.c_void_p()
     t = np.zeros(iters)
     counts = np.zeros(3 * iters, dtype=np.int64)
     c = C.c_double(0)
-    rc = lib().or_ns_sqrt(s.h, tau, tau_s, iters, scale, power_iters, mu, C.byref(yo),
-                          C.byref(zo), _ptr(t), _ptr(counts), C.byref(c))
-    return dict(Y=OMat(yo.value), Z=OMat(zo.value), t=t, counts=counts.reshape(iters, 3),
-                c=c.value, rc=rc)
+    done = C.c_int(0)
+    rc = lib().or_ns_sqrt(s.h, tau, tau_s, iters, scale, power_iters, mu, t_stop, int(scaled), C.byref(yo),
+                          C.byref(zo), _ptr(t), _ptr(counts), C.byref(c), C.byref(done))
+    k = done.value if rc == 0 else done.value + 1   # keep the failing step's t_k
+    return dict(Y=OMat(yo.value), Z=OMat(zo.value), t=t[:k], counts=counts.reshape(iters, 3)[:k],
+                c=c.value, rc=rc, iters=k)
 
 
 def num_threads() -> int:
     return lib().or_num_threads()
+
+
+def alpha(t: float) -> float:
+    """Scaling sigmoid alpha(t) of P:442-445."""
+    return lib().or_alpha(float(t))
+
+
+def eps(t: float) -> float:
+    """Stabilisation sigmoid eps(t) of P:446-448."""
+    return lib().or_eps(float(t))

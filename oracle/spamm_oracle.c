@@ -416,12 +416,15 @@ omat *or_copy(const omat *m)
 /* op 0: y = x / c ;  op 1: y = (x / c + mu*delta) / (1 + mu) ;
  * op 2: y = x * c  ;  op 3: y = x / c  (same as 0; kept for clarity)
  * op 4: H = 1/2 (3 delta - x)  written as 1.5*delta - 0.5*x (exactly equal, the
- *       1/2 scale is exact).  Diagonal blocks absent from x become 1.5 I. */
+ *       1/2 scale is exact).  Diagonal blocks absent from x become 1.5 I.
+ * op 6: scaled + stabilised map with alpha = c, eps = mu:
+ *       x~ = (1 - 2 eps) x + eps delta   ([0,1] -> [eps, 1-eps], "prior to the logistic")
+ *       H  = h_alpha[x~] = sqrt(alpha)/2 (3 delta - alpha x~). */
 static onode *map_rec(const onode *p, int lev, int L, int b, int I, int J, int op,
                       double c, double mu)
 {
     int diag = (I == J);
-    int fill = (op == 1 || op == 4 || op == 5);   /* ops that create absent diagonal blocks */
+    int fill = (op == 1 || op == 4 || op == 5 || op == 6);   /* ops that create absent diagonal blocks */
     if (!p && !(diag && fill)) return NULL;
     if (!p && lev < L && diag && fill) {
         onode *q = new_interior();
@@ -442,6 +445,11 @@ static onode *map_rec(const onode *p, int lev, int L, int b, int I, int J, int o
                 case 1: y = (x / c + mu * d) / (1.0 + mu); break;
                 case 2: y = x * c; break;
                 case 5: y = d; break;
+                case 6: {
+                    double xt = (1.0 - 2.0 * mu) * x + mu * d;
+                    y = (sqrt(c) / 2.0) * (3.0 * d - c * xt);
+                    break;
+                }
                 default: y = 1.5 * d - 0.5 * x; break;
                 }
                 q->blk[(size_t)r * b + s] = y;
@@ -534,14 +542,22 @@ double or_power_scale(const omat *s, int K)
  *   Y' = Y (x)_tau_s H ; Z' = H (x)_tau Z.
  * counts (nullable): leaf tasks of the 3 products [X, Y', Z'].
  * Returns 0, or -1 on a non-finite t / norm. */
-int or_ns_step(const omat *Y, const omat *Z, double tau, double tau_s,
-               omat **Yn, omat **Zn, omat **Hout, double *t, int64_t counts[3])
+/* The paper's damping sigmoids, functions of the trace error t_k:
+ *   alpha(t) = 1 + 1.85 (1 + e^{-50 (t - .35)})^{-1},
+ *   eps(t)   = .1 (1 + e^{-75 (t - .30)})^{-1}. */
+double or_alpha(double t) { return 1.0 + 1.85 * (1.0 / (1.0 + exp(-50.0 * (t - 0.35)))); }
+double or_eps(double t) { return 0.1 * (1.0 / (1.0 + exp(-75.0 * (t - 0.30)))); }
+
+/* map 0: H = 1/2 (3I - X) (alpha = 1, eps = 0: the north_star form);
+ * map 1: H = h_alpha[(1 - 2 eps) X + eps I] with alpha(t_k), eps(t_k). */
+int or_ns_step_map(const omat *Y, const omat *Z, double tau, double tau_s, int map,
+                   omat **Yn, omat **Zn, omat **Hout, double *t, int64_t counts[3])
 {
     int64_t c0 = 0, c1 = 0, c2 = 0;
     omat *X = or_multiply(Z, Y, tau, NULL, 0, &c0);
     double tr = or_trace(X);
     *t = ((double)X->n - tr) / (double)X->n;
-    omat *H = map_mat(X, 4, 0.0, 0.0);
+    omat *H = map ? map_mat(X, 6, or_alpha(*t), or_eps(*t)) : map_mat(X, 4, 0.0, 0.0);
     or_free(X);
     *Yn = or_multiply(Y, H, tau_s, NULL, 0, &c1);
     *Zn = or_multiply(H, Z, tau, NULL, 0, &c2);
@@ -549,6 +565,12 @@ int or_ns_step(const omat *Y, const omat *Z, double tau, double tau_s,
     if (Hout) *Hout = H; else or_free(H);
     if (!isfinite(*t) || !isfinite(or_norm(*Yn)) || !isfinite(or_norm(*Zn))) return -1;
     return 0;
+}
+
+int or_ns_step(const omat *Y, const omat *Z, double tau, double tau_s,
+               omat **Yn, omat **Zn, omat **Hout, double *t, int64_t counts[3])
+{
+    return or_ns_step_map(Y, Z, tau, tau_s, 0, Yn, Zn, Hout, t, counts);
 }
 
 /* Y0 = s/c (mu = 0) or (s/c + mu I)/(1+mu) (reading L13); Z0 = I. */
@@ -563,22 +585,26 @@ omat *or_ns_y0(const omat *s, double c, double mu)
  * (unscaled by sqrt(c (1+mu))).  t_hist [iters], counts [3*iters] nullable.
  * Returns 0 or -1 (non-finite; Y/Z hold the last finite iterates). */
 int or_ns_sqrt(const omat *s, double tau, double tau_s, int iters, double scale,
-               int power_iters, double mu, omat **Yout, omat **Zout,
-               double *t_hist, int64_t *counts, double *c_used)
+               int power_iters, double mu, double t_stop, int map, omat **Yout, omat **Zout,
+               double *t_hist, int64_t *counts, double *c_used, int *iters_done)
 {
     double c = scale > 0.0 ? scale : or_power_scale(s, power_iters);
     if (c_used) *c_used = c;
     omat *Y = or_ns_y0(s, c, mu);
     omat *Z = or_identity(s->n, s->b);
     int rc = 0;
+    if (iters_done) *iters_done = 0;
     for (int k = 0; k < iters; k++) {
         omat *Yn, *Zn;
         double t;
-        rc = or_ns_step(Y, Z, tau, tau_s, &Yn, &Zn, NULL, &t, counts ? counts + 3 * k : NULL);
+        rc = or_ns_step_map(Y, Z, tau, tau_s, map, &Yn, &Zn, NULL, &t, counts ? counts + 3 * k : NULL);
         if (t_hist) t_hist[k] = t;
         if (rc) { or_free(Yn); or_free(Zn); break; }
         or_free(Y); or_free(Z);
         Y = Yn; Z = Zn;
+        if (iters_done) *iters_done = k + 1;
+        /* convergence monitored by the relative trace error */
+        if (t_stop > 0.0 && fabs(t) <= t_stop) break;
     }
     double f = sqrt(c * (1.0 + mu));
     *Yout = map_mat(Y, 2, f, 0.0);

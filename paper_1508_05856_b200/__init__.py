@@ -26,7 +26,7 @@ __all__ = [
     "spamm_ctx_create", "spamm_ctx_destroy", "spamm_last_error", "spamm_kernel_launches",
     "spamm_build_tree", "spamm_build_tree_blocks", "spamm_mat_free", "spamm_mat_info",
     "spamm_norm", "spamm_to_dense", "spamm_level_norms2", "spamm_get_blocks",
-    "spamm_multiply", "spamm_export_tasks", "spamm_ns_step", "spamm_power_scale",
+    "spamm_multiply", "spamm_export_tasks", "spamm_ns_step", "spamm_ns_step_map", "spamm_power_scale",
     "spamm_ns_y0", "spamm_identity", "spamm_ns_sqrt", "spamm_scale",
     "spamm_export_blocks", "spamm_profile_enable", "spamm_profile_read", "spamm_peak_dmma",
     "Comm", "spamm_comm_nccl_unique_id", "spamm_comm_nccl_create", "spamm_comm_local_group",
@@ -55,7 +55,8 @@ class spamm_stats(C.Structure):
 class spamm_ns_opts(C.Structure):
     _fields_ = [("tau_s", C.c_double), ("mu", C.c_double), ("scale", C.c_double),
                 ("power_iters", C.c_int32), ("t_history", C.c_void_p),
-                ("per_product", C.c_void_p), ("c_out", C.c_void_p)]
+                ("per_product", C.c_void_p), ("c_out", C.c_void_p), ("t_stop", C.c_double),
+                ("iters_done", C.c_void_p), ("map", C.c_int32)]
 
 
 NPHASE = 5
@@ -106,6 +107,7 @@ def load():
         "spamm_multiply": (i32, [vp, vp, vp, dbl, P(vp), P(spamm_stats)]),
         "spamm_export_tasks": (i32, [vp, vp, i64, P(i64)]),
         "spamm_ns_step": (i32, [vp, vp, vp, dbl, dbl, P(vp), P(vp), P(vp), P(dbl), vp]),
+        "spamm_ns_step_map": (i32, [vp, vp, vp, dbl, dbl, i32, P(vp), P(vp), P(vp), P(dbl), vp, vp]),
         "spamm_power_scale": (i32, [vp, vp, i32, P(dbl)]),
         "spamm_ns_y0": (i32, [vp, vp, dbl, dbl, P(vp)]),
         "spamm_identity": (i32, [vp, i64, i32, P(vp)]),
@@ -420,6 +422,20 @@ def spamm_ns_step(ctx: Ctx, Y: Mat, Z: Mat, tau: float, tau_s: float | None = No
     return out + (Mat(ctx, hn),) if want_h else out
 
 
+def spamm_ns_step_map(ctx: Ctx, Y: Mat, Z: Mat, tau: float, tau_s: float | None = None,
+                      scaled: bool = True, want_h: bool = False):
+    """One dual NS step with the chosen map; returns (Y', Z', t_k, stats, (alpha, eps) [, H])."""
+    tau_s = tau if tau_s is None else tau_s
+    yn, zn, hn = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    t = C.c_double()
+    ae = (C.c_double * 2)()
+    sts = (spamm_stats * 3)()
+    ctx.check(load().spamm_ns_step_map(ctx.h, Y.h, Z.h, float(tau), float(tau_s), int(scaled), C.byref(yn),
+                                       C.byref(zn), C.byref(hn) if want_h else None, C.byref(t), sts, ae))
+    out = (Mat(ctx, yn), Mat(ctx, zn), t.value, [s.as_dict() for s in sts], (ae[0], ae[1]))
+    return out + (Mat(ctx, hn),) if want_h else out
+
+
 def spamm_power_scale(ctx: Ctx, s: Mat, K: int = 100) -> float:
     c = C.c_double()
     ctx.check(load().spamm_power_scale(ctx.h, s.h, K, C.byref(c)))
@@ -446,21 +462,25 @@ def spamm_scale(ctx: Ctx, m: Mat, alpha: float, divide: bool = False) -> Mat:
 
 def spamm_ns_sqrt(ctx: Ctx, s: Mat, tau: float, iters: int, tau_s: float | None = None,
                   mu: float = 0.0, scale: float = 0.0, power_iters: int = 100,
-                  want_stats: bool = True):
-    """Full dual NS run: returns dict(Y, Z, t, stats, c)."""
+                  want_stats: bool = True, t_stop: float = 0.0, scaled: bool = False):
+    """Full dual NS run: returns dict(Y, Z, t, stats, c, iters).  t_stop > 0 ends the
+    run after the first k with |t_k| <= t_stop (t, stats then cover the steps run)."""
     t = np.zeros(iters)
     sts = (spamm_stats * (3 * iters))() if want_stats else None
     c = C.c_double()
+    done = C.c_int32(0)
     o = spamm_ns_opts(-1.0 if tau_s is None else float(tau_s), float(mu), float(scale),
                       int(power_iters), t.ctypes.data, C.cast(sts, C.c_void_p) if want_stats else None,
-                      C.cast(C.pointer(c), C.c_void_p))
+                      C.cast(C.pointer(c), C.c_void_p), float(t_stop),
+                      C.cast(C.pointer(done), C.c_void_p), int(scaled))
     yo, zo = C.c_void_p(), C.c_void_p()
     ctx.check(load().spamm_ns_sqrt(ctx.h, s.h, float(tau), int(iters), C.byref(yo), C.byref(zo),
                                    C.byref(o)))
+    k = done.value
     stats = None
     if want_stats:
-        stats = [[sts[3 * k + p].as_dict() for p in range(3)] for k in range(iters)]
-    return dict(Y=Mat(ctx, yo), Z=Mat(ctx, zo), t=t, stats=stats, c=c.value)
+        stats = [[sts[3 * j + p].as_dict() for p in range(3)] for j in range(k)]
+    return dict(Y=Mat(ctx, yo), Z=Mat(ctx, zo), t=t[:k], stats=stats, c=c.value, iters=k)
 
 
 def spamm_export_blocks(ctx: Ctx, m: Mat, out=None):

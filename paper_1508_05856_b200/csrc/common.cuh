@@ -221,10 +221,12 @@ void cull_free(spamm_ctx ctx, Cull *cw);
 spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj_host, int64_t cap, int64_t *n);
 
 // gemm.cu — FP64 DMMA leaf GEMM with fused epilogues
-enum { EPI_STORE = 0, EPI_NS_H = 1 };
+enum { EPI_STORE = 0, EPI_NS_H = 1, EPI_NS_X = 2 };
 spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
                       spamm_mat C, int epi, double *trace_part);
-spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg);
+spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
+// scaled / stabilised NS map in place over X: coef <- {alpha, eps, sqrt(alpha)/2}(t)
+spamm_status ns_scaled_map(spamm_ctx ctx, spamm_mat X, const double *t, double *coef);
 // append value*I blocks for absent diagonal positions at slots base..; *added = count (syncs)
 spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value, int64_t *added);
 spamm_status trace_finish(spamm_ctx ctx, const double *trace_part, int nb, int64_t n,

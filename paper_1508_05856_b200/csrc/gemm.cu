@@ -8,6 +8,9 @@
 //   EPI_NS_H  : H_ij = 1/2 (3 delta_ij I - X_ij) (alpha = 1) -> pool,
 //               ||H_ij||^2, and tr(X_ii) partials for t_k;
 //               X itself is never stored.
+//   EPI_NS_X  : X_ij -> pool, ||X_ij||^2, tr(X_ii) partials (scaled map: the
+//               coefficients alpha(t_k), eps(t_k) need the full trace first, so
+//               k_ns_map applies H = h_alpha[(1-2eps)X + eps I] in a second pass).
 // FP64 MMA on sm_100a is warp-level mma.sync m8n8k4 (SASS DMMA.8x8x4); tcgen05
 // has no f64 kind, so operands go shared memory -> registers.  Tiles are staged
 // by a warp-specialised TMA bulk-copy / mbarrier pipeline; the pool layout is
@@ -250,11 +253,13 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
             for (int nf = 0; nf < NF; nf++) {
                 const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
                 double y0 = acc[mf][nf][0], y1 = acc[mf][nf][1];
+                if (EPI != EPI_STORE) {
+                    if (diag && r == c) tr += y0;
+                    if (diag && r == c + 1) tr += y1;
+                }
                 if (EPI == EPI_NS_H) {
                     // H = 1/2 (3 delta - X) written as 1.5 delta - 0.5 x (the 1/2 is exact)
                     const double d0 = (diag && r == c) ? 1.5 : 0.0, d1 = (diag && r == c + 1) ? 1.5 : 0.0;
-                    if (diag && r == c) tr += y0;
-                    if (diag && r == c + 1) tr += y1;
                     y0 = d0 - 0.5 * y0;
                     y1 = d1 - 0.5 * y1;
                 }
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
             g.c_leaf_n2[code] = s2;
             g.c_coord[seg] = (int32_t)code;
             g.c_slot[code] = seg;
-            if (EPI == EPI_NS_H && diag) g.trace_part[I] = t2;
+            if (EPI != EPI_STORE && diag) g.trace_part[I] = t2;
         }
         par ^= 1;
     }
@@ -328,6 +333,7 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
                (int)cw->nsegs, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
                cw->counters + CNT_GEMM_TICKET};
     if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H>(ctx, A->b, g);
+    if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X>(ctx, A->b, g);
     return gemm_dispatch<EPI_STORE>(ctx, A->b, g);
 }
 
@@ -392,10 +398,10 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
     return SPAMM_OK;
 }
 
-spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg)
+spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value)
 {
     int64_t added = 0;
-    ST(diag_append(ctx, H, nseg, 1.5, &added));
+    ST(diag_append(ctx, H, nseg, value, &added));
     H->nblk = nseg + added;
     return SPAMM_OK;
 }
@@ -419,5 +425,59 @@ spamm_status trace_finish(spamm_ctx ctx, const double *trace_part, int nb, int64
 {
     k_trace_finish<<<1, 256, 0, ctx->stream>>>(trace_part, nb, (double)n, t_out);
     CKL(ctx);
+    return SPAMM_OK;
+}
+
+// ------------------------------------------- scaled / stabilised NS map
+// alpha(t) = 1 + 1.85 (1 + e^{-50(t-.35)})^{-1}, eps(t) = .1 (1 + e^{-75(t-.30)})^{-1},
+// computed on the device from t_k (no host round trip).  coef = {alpha, eps, sqrt(alpha)/2}.
+__global__ void k_ns_coef(const double *t, double *coef)
+{
+    const double tk = *t;
+    const double a = 1.0 + 1.85 * (1.0 / (1.0 + exp(-50.0 * (tk - 0.35))));
+    const double e = 0.1 * (1.0 / (1.0 + exp(-75.0 * (tk - 0.30))));
+    coef[0] = a;
+    coef[1] = e;
+    coef[2] = sqrt(a) / 2.0;
+}
+
+// In place over the stored X blocks: x~ = (1 - 2 eps) x + eps delta ("[0,1] -> [eps, 1-eps]
+// prior to the logistic"), H = sqrt(alpha)/2 (3 delta - alpha x~); ||H_ij||^2 to the leaf
+// level (thread partials in element order, then a fixed tree: deterministic).
+__global__ void __launch_bounds__(256) k_ns_map(double *pool, const int32_t *coord, int b, const double *coef,
+                                                double *leaf_n2)
+{
+    __shared__ double red[256];
+    const int64_t blk = blockIdx.x;
+    const uint32_t code = coord[blk];
+    const bool diag = morton_i(code) == morton_j(code);
+    const double a = coef[0], e = coef[1], sa = coef[2];
+    double *p = pool + blk * (int64_t)b * b;
+    double ss = 0.0;
+    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+        const int r = idx / b, q = pool_col(idx, b);
+        const double d = (diag && r == q) ? 1.0 : 0.0;
+        const double xt = (1.0 - 2.0 * e) * p[idx] + e * d;
+        const double h = sa * (3.0 * d - a * xt);
+        p[idx] = h;
+        ss = fma(h, h, ss);
+    }
+    red[threadIdx.x] = ss;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) leaf_n2[code] = red[0];
+}
+
+spamm_status ns_scaled_map(spamm_ctx ctx, spamm_mat X, const double *t, double *coef)
+{
+    k_ns_coef<<<1, 1, 0, ctx->stream>>>(t, coef);
+    CKL(ctx);
+    if (X->nblk > 0) {
+        k_ns_map<<<(int)X->nblk, 256, 0, ctx->stream>>>(X->pool, X->coord, X->b, coef, X->norm2 + pyr_off(X->L));
+        CKL(ctx);
+    }
     return SPAMM_OK;
 }

@@ -108,7 +108,7 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
         prof_end(ctx, px);
         if (sc) return sc;
     }
-    int64_t extra = (epi == EPI_NS_H) ? A->nb : 0;
+    int64_t extra = (epi != EPI_STORE) ? A->nb : 0;
     spamm_mat m;
     spamm_status st = mat_new(ctx, A->n, A->b, cw->nsegs + extra, &m);
     if (!st && (m->r0 != A->r0 || m->r1 != A->r1)) {
@@ -129,9 +129,12 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
     dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
     if (!st) {
         m->nblk = cw->nsegs;
-        if (epi == EPI_NS_H) st = diag_fixup(ctx, m, cw->nsegs);
+        // absent diagonal blocks of X: H_ii = 1.5 I (plain map) or X_ii = 0 (scaled map,
+        // mapped with the other blocks once alpha(t_k), eps(t_k) are known)
+        if (epi == EPI_NS_H) st = diag_fixup(ctx, m, cw->nsegs, 1.5);
+        if (epi == EPI_NS_X) st = diag_fixup(ctx, m, cw->nsegs, 0.0);
     }
-    if (!st) st = norms_finish(ctx, m);
+    if (!st && epi != EPI_NS_X) st = norms_finish(ctx, m);
     if (st) {
         spamm_mat_free(m);
         return st;
@@ -160,10 +163,11 @@ extern "C" spamm_status spamm_export_tasks(spamm_ctx ctx, int32_t *ikj, int64_t 
     return cull_export(ctx, ctx->last, ikj, cap, n);
 }
 
-extern "C" spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
-                                      spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
-                                      double *t_k, spamm_stats stats[3])
+extern "C" spamm_status spamm_ns_step_map(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
+                                          int32_t map, spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
+                                          double *t_k, spamm_stats stats[3], double *alpha_eps)
 {
+    if (map != 0 && map != 1) return set_err(ctx, SPAMM_EINVAL, "map must be 0 or 1");
     ST(check_pair(ctx, Z, Y, tau));
     if (!(tau_s >= 0.0) || !std::isfinite(tau_s)) return set_err(ctx, SPAMM_EINVAL, "tau_s must be >= 0");
     if (!Y_next || !Z_next) return set_err(ctx, SPAMM_EINVAL, "NULL output");
@@ -172,20 +176,24 @@ extern "C" spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, d
     if (!trace_part) return set_err(ctx, SPAMM_ENOMEM, "trace partials");
     CK(cudaMemsetAsync(trace_part, 0, sizeof(double) * nb, ctx->stream));
     spamm_mat H = nullptr, Yn = nullptr, Zn = nullptr;
-    // X = Z (x)_tau Y  ->  H = 1/2 (3I - X), tr X partials (X never stored)
-    spamm_status st = product(ctx, ctx->cw[0], Z, Y, tau, EPI_NS_H, trace_part, &H);
+    // X = Z (x)_tau Y  ->  H = 1/2 (3I - X), tr X partials (X never stored); scaled map:
+    // X stored, then H = h_alpha[(1-2eps)X + eps I] in place once t_k is known
+    spamm_status st = product(ctx, ctx->cw[0], Z, Y, tau, map ? EPI_NS_X : EPI_NS_H, trace_part, &H);
     // row partition: every rank gets all tr(X_ii) partials, summed in the fixed order
     if (!st && H->dist) st = gather_rows(ctx, H->parts, trace_part, 1);
     if (!st) st = trace_finish(ctx, trace_part, nb, Y->n, ctx->dscratch);
+    if (!st && map) st = ns_scaled_map(ctx, H, ctx->dscratch, ctx->dscratch + 8);
+    if (!st && map) st = norms_finish(ctx, H);
     if (!st && stats) stats[0] = ctx->cw[0]->stats;
     // Y' = Y (x)_tau_s H ; Z' = H (x)_tau Z
     if (!st) st = product(ctx, ctx->cw[1], Y, H, tau_s, EPI_STORE, nullptr, &Yn);
     if (!st && stats) stats[1] = ctx->cw[1]->stats;
     if (!st) st = product(ctx, ctx->cw[2], H, Z, tau, EPI_STORE, nullptr, &Zn);
     if (!st && stats) stats[2] = ctx->cw[2]->stats;
-    double hv[3] = {0, 0, 0};
+    double hv[3] = {0, 0, 0}, ae[2] = {1.0, 0.0};
     if (!st) {
         // t_k and the root norms (non-finite detection)
+        if (map) cudaMemcpyAsync(ae, ctx->dscratch + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
         cudaMemcpyAsync(&hv[0], ctx->dscratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
         cudaMemcpyAsync(&hv[1], Yn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
         cudaMemcpyAsync(&hv[2], Zn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
@@ -200,6 +208,10 @@ extern "C" spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, d
         return st;
     }
     if (t_k) *t_k = hv[0];
+    if (alpha_eps) {
+        alpha_eps[0] = ae[0];
+        alpha_eps[1] = ae[1];
+    }
     if (H_out) *H_out = H;
     else spamm_mat_free(H);
     *Y_next = Yn;
@@ -207,6 +219,13 @@ extern "C" spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, d
     if (!std::isfinite(hv[0]) || !std::isfinite(hv[1]) || !std::isfinite(hv[2]))
         return set_err(ctx, SPAMM_ENOTFINITE, "non-finite trace error or root norm");
     return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
+                                      spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
+                                      double *t_k, spamm_stats stats[3])
+{
+    return spamm_ns_step_map(ctx, Y, Z, tau, tau_s, 0, Y_next, Z_next, H_out, t_k, stats, nullptr);
 }
 
 extern "C" spamm_status spamm_power_scale(spamm_ctx ctx, spamm_mat s, int32_t K, double *c)
@@ -236,6 +255,7 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
     double c = o.scale;
     if (!(c > 0.0)) ST(power_scale(ctx, s, o.power_iters, &c));
     if (o.c_out) *o.c_out = c;
+    if (o.iters_done) *o.iters_done = 0;
     spamm_mat Y = nullptr, Z = nullptr;
     ST(spamm_ns_y0(ctx, s, c, mu, &Y));
     spamm_status st = spamm_identity(ctx, s->n, s->b, &Z);
@@ -245,7 +265,7 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
         spamm_mat Yn = nullptr, Zn = nullptr;
         double t = 0.0;
         spamm_stats sts[3];
-        st = spamm_ns_step(ctx, Y, Z, tau, tau_s, &Yn, &Zn, nullptr, &t, sts);
+        st = spamm_ns_step_map(ctx, Y, Z, tau, tau_s, o.map, &Yn, &Zn, nullptr, &t, sts, nullptr);
         if (o.t_history && (st == SPAMM_OK || st == SPAMM_ENOTFINITE)) o.t_history[k] = t;
         if (o.per_product && st == SPAMM_OK) memcpy(o.per_product + 3 * k, sts, sizeof(sts));
         if (st) {
@@ -257,6 +277,8 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
         spamm_mat_free(Z);
         Y = Yn;
         Z = Zn;
+        if (o.iters_done) *o.iters_done = k + 1;
+        if (o.t_stop > 0.0 && std::fabs(t) <= o.t_stop) break;
     }
     prof_end(ctx, pl);
     std::string err = ctx->err;

@@ -127,14 +127,16 @@ def _block_bboxes(pts: np.ndarray, b: int):
 
 
 def gaussian_blocks(points: np.ndarray, b: int, sigma: float, shift: float,
-                    delta: float):
+                    delta: float, rows=None):
     """Block-sparse Gaussian overlap s_IJ (b x b blocks) for Hilbert-ordered points.
 
     Candidate block pair (I,J) is skipped when b*exp(-dmin^2/(2 sigma^2)) < delta
     (dmin: distance between the blocks' point bounding boxes, an upper bound on
     every |s_ij| of the block, so ||s_IJ||_F <= b*max|s_ij| < delta), otherwise it
     is computed and kept iff ||s_IJ||_F >= delta.  Returns (bi, bj, blocks) with
-    blocks [nblk, b, b] fp64, ordered by (bi, bj)."""
+    blocks [nblk, b, b] fp64, ordered by (bi, bj).  rows = (r0, r1) generates only
+    block rows r0 <= I < r1 (a rank's shard of the row partition; the blocks are
+    bitwise those of the full generation)."""
     n = points.shape[0]
     assert n % b == 0
     nb = n // b
@@ -142,7 +144,8 @@ def gaussian_blocks(points: np.ndarray, b: int, sigma: float, shift: float,
     inv2s2 = 1.0 / (2.0 * sigma * sigma)
     out_i, out_j, out_b = [], [], []
     P = points.reshape(nb, b, 3)
-    for I in range(nb):
+    r0, r1 = (0, nb) if rows is None else rows
+    for I in range(r0, r1):
         gap = np.maximum(0.0, np.maximum(lo[I][None, :] - hi, lo - hi[I][None, :]))
         dmin2 = np.sum(gap * gap, axis=1)
         cand = np.nonzero(b * np.exp(-dmin2 * inv2s2) >= delta)[0]
@@ -162,6 +165,8 @@ def gaussian_blocks(points: np.ndarray, b: int, sigma: float, shift: float,
             out_i.append(np.full(int(keep.sum()), I, dtype=np.int32))
             out_j.append(cand[keep].astype(np.int32))
             out_b.append(blk[keep])
+    if not out_i:
+        return np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, b, b))
     bi = np.concatenate(out_i)
     bj = np.concatenate(out_j)
     blocks = np.ascontiguousarray(np.concatenate(out_b, axis=0))
@@ -197,6 +202,10 @@ class Config:
     mu: float = 0.0
     seed: int = 0
     tau_min: float = 0.0  # smallest tau the input must serve (drop rule)
+    # run options (readings L9, L15): tau_s = tau_s_factor * tau; t_stop > 0
+    # ends the run at convergence (|t_k| <= t_stop) instead of after `iters`
+    tau_s_factor: float = 1.0
+    t_stop: float = 0.0
 
 
 # BASELINE.json configs[0..4] (BJ:7-11); C4's tau sweep is {1e-4,1e-6,1e-8}.
@@ -205,17 +214,21 @@ CONFIGS = {
     "C2": Config("C2", "kms", 4096, 32, 1e-8, 30, rho=0.9),
     "C3": Config("C3", "gauss", 16384, 64, 1e-7, 30, sigma=0.8, shift=1e-3,
                  seed=150805856, tau_min=1e-7),
+    # C4 / C5: with tau_s = tau the plain dual iteration diverges (C4 tau = 1e-6 at
+    # k = 14, C5 at k = 10; profiles/r01_diag), so these use the paper's default
+    # sensitive threshold tau_s = .01 tau and stop at convergence.
     "C4": Config("C4", "gauss", 32768, 64, 1e-6, 40, sigma=1.2, shift=0.0,
-                 mu=1e-2, seed=150805857, tau_min=1e-8),
+                 mu=1e-2, seed=150805857, tau_min=1e-8, tau_s_factor=0.01, t_stop=1e-5),
     "C5": Config("C5", "gauss", 131072, 64, 1e-7, 30, sigma=0.8, shift=1e-3,
-                 seed=150805858, tau_min=1e-7),
+                 seed=150805858, tau_min=1e-7, tau_s_factor=0.01, t_stop=1e-5),
 }
 
 
-def make_input(cfg: Config, n: int | None = None):
+def make_input(cfg: Config, n: int | None = None, rows=None):
     """Return ("dense", s) for KMS configs or ("blocks", (bi, bj, blocks)) for the
     Gaussian configs.  `n` overrides the dimension (scaled-down parity cases);
-    the box keeps unit density, L = n^(1/3)."""
+    the box keeps unit density, L = n^(1/3).  `rows` = (r0, r1) restricts the
+    Gaussian block list to block rows [r0, r1) (KMS inputs are returned whole)."""
     n = cfg.n if n is None else n
     if cfg.kind == "kms":
         return "dense", kms(n, cfg.rho)
@@ -223,4 +236,4 @@ def make_input(cfg: Config, n: int | None = None):
     pts = uniform_points(n, cfg.seed, box)
     pts = np.ascontiguousarray(pts[hilbert_order(pts, box)])
     delta = 1e-2 * cfg.tau_min * math.sqrt(n)
-    return "blocks", gaussian_blocks(pts, cfg.b, cfg.sigma, cfg.shift, delta)
+    return "blocks", gaussian_blocks(pts, cfg.b, cfg.sigma, cfg.shift, delta, rows)

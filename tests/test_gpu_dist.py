@@ -220,3 +220,31 @@ def test_partition_errors(gpu):
     ctx.close()
     for c in comms:
         c.destroy()
+
+
+def test_ns_scaled_dist_bitwise(gpu):
+    """The scaled map's second pass and the device-side alpha(t_k), eps(t_k) are
+    replicated identically on every rank."""
+    n, b = 4096, 64
+    payload = gaussian(n, b)
+
+    def run(ctx):
+        S = build(ctx, n, b, payload)
+        r = sp().spamm_ns_sqrt(ctx, S, 1e-7, 12, tau_s=1e-9, scaled=True)
+        out = dict(Y=blocks_of(ctx, r["Y"]), Z=blocks_of(ctx, r["Z"]), t=r["t"].copy())
+        for m in (S, r["Y"], r["Z"]):
+            m.free()
+        return out
+    ref = run(sp().spamm_ctx_create(0))
+
+    def fn(rank, comm):
+        ctx = sp().spamm_ctx_create(0, library_stream=True)
+        sp().spamm_ctx_set_comm(ctx, comm)
+        out = run(ctx)
+        ctx.close()
+        return out
+    res = dist().run_rank_threads(3, fn)
+    assert_bitwise(merged(res, "Y"), ref["Y"])
+    assert_bitwise(merged(res, "Z"), ref["Z"])
+    for r in res:
+        assert np.array_equal(r["t"].view(np.uint64), ref["t"].view(np.uint64))

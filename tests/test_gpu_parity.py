@@ -294,3 +294,42 @@ def test_ns_mu_shift(ctx):
     ro = O.ns_sqrt(So, 1e-8, 30, mu=1e-2, scale=cs)
     assert rel(gpu_to_oracle(ctx, r["Y"]).to_dense(), ro["Y"].to_dense()) <= 1e-10
     assert rel(gpu_to_oracle(ctx, r["Z"]).to_dense(), ro["Z"].to_dense()) <= 1e-10
+
+
+# ------------------------------------------- scaled / stabilised map (§8(f) f1)
+def test_ns_scaled_lockstep(ctx):
+    """Scaled + stabilised map from identical inputs: t_k, (alpha, eps), H,
+    Y', Z' and the task counts against the oracle."""
+    c = si.CONFIGS["C2"]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    cs = O.power_scale(So)
+    Y = sp().spamm_ns_y0(ctx, S, cs)
+    Z = sp().spamm_identity(ctx, c.n, c.b)
+    for k in range(6):
+        Yo, Zo = gpu_to_oracle(ctx, Y), gpu_to_oracle(ctx, Z)
+        Yn, Zn, t, st, (a, e), H = sp().spamm_ns_step_map(ctx, Y, Z, c.tau, scaled=True, want_h=True)
+        Yno, Zno, Ho, to, cnt = O.ns_step(Yo, Zo, c.tau, scaled=True)
+        assert t == pytest.approx(to, abs=1e-13)
+        assert a == pytest.approx(O.alpha(to), rel=1e-12) and e == pytest.approx(O.eps(to), rel=1e-10, abs=1e-300)
+        assert [s["tasks"] for s in st] == list(cnt)
+        assert rel(gpu_to_oracle(ctx, H).to_dense(), Ho.to_dense()) <= 1e-12
+        assert rel(gpu_to_oracle(ctx, Yn).to_dense(), Yno.to_dense()) <= 1e-12
+        assert rel(gpu_to_oracle(ctx, Zn).to_dense(), Zno.to_dense()) <= 1e-12
+        Y, Z = Yn, Zn
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_ns_scaled_free_run_and_t_stop(ctx, cfg):
+    c = si.CONFIGS[cfg]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    cs = O.power_scale(So)
+    r = sp().spamm_ns_sqrt(ctx, S, c.tau, c.iters, scale=cs, scaled=True, t_stop=1e-9)
+    ro = O.ns_sqrt(So, c.tau, c.iters, scale=cs, scaled=True, t_stop=1e-9)
+    assert r["iters"] == ro["iters"] < c.iters
+    assert rel(gpu_to_oracle(ctx, r["Y"]).to_dense(), ro["Y"].to_dense()) <= 1e-10
+    assert rel(gpu_to_oracle(ctx, r["Z"]).to_dense(), ro["Z"].to_dense()) <= 1e-10
+    np.testing.assert_allclose(r["t"], ro["t"], rtol=0, atol=1e-12)
+    counts = np.array([[p["tasks"] for p in k] for k in r["stats"]])
+    assert np.array_equal(counts, ro["counts"])

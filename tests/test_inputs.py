@@ -64,3 +64,18 @@ def test_gaussian_blocks_symmetric_and_lossless():
                 assert f < delta * (1 + 1e-12)
     # drop tolerance is below tau * ||s|| (lossless: dropped blocks can never survive)
     assert delta <= tau * np.linalg.norm(dense)
+
+
+def test_gaussian_row_shards_equal_full_generation():
+    """A rank's row shard (rows=(r0, r1)) is bitwise the matching slice of the full list."""
+    cfg = si.Config("t", "gauss", 2048, 64, 1e-7, 30, sigma=0.8, shift=1e-3, seed=150805858, tau_min=1e-7)
+    _, (bi, bj, blocks) = si.make_input(cfg)
+    nb = 2048 // 64
+    got = []
+    for r0, r1 in [(0, 7), (7, 7), (7, 20), (20, nb)]:
+        _, (si_, sj_, sb_) = si.make_input(cfg, rows=(r0, r1))
+        assert np.all((si_ >= r0) & (si_ < r1))
+        got.append((si_, sj_, sb_))
+    assert np.array_equal(np.concatenate([g[0] for g in got]), bi)
+    assert np.array_equal(np.concatenate([g[1] for g in got]), bj)
+    assert np.array_equal(np.concatenate([g[2] for g in got]), blocks)

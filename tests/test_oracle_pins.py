@@ -359,3 +359,77 @@ def test_power_scale():
     lmax = np.linalg.eigvalsh(s)[-1]
     assert c <= lmax * (1 + 1e-15)
     assert c >= 0.99 * lmax
+
+
+# ------------------------------------------- scaled / stabilised map (§8(f) f1)
+def test_scaled_map_sigmoids_paper_values():
+    """P:442-448: alpha(t) = 1 + 1.85/(1 + e^{-50(t-.35)}), eps(t) = .1/(1 + e^{-75(t-.30)}):
+    midpoints alpha(.35) = 1.925, eps(.30) = .05; saturation alpha -> 2.85, eps -> .1 for
+    t -> 1; both damped to (1, 0) as t -> 0."""
+    assert O.alpha(0.35) == pytest.approx(1.925, rel=1e-15)
+    assert O.eps(0.30) == pytest.approx(0.05, rel=1e-15)
+    assert O.alpha(1.0) == pytest.approx(2.85, rel=1e-12)
+    assert O.eps(1.0) == pytest.approx(0.1, rel=1e-15)
+    assert 1.0 < O.alpha(0.0) < 1.0 + 1e-7 and 0.0 < O.eps(0.0) < 1e-10
+    ts = np.linspace(0, 1, 101)
+    assert np.all(np.diff([O.alpha(t) for t in ts]) >= 0)
+    assert np.all(np.diff([O.eps(t) for t in ts]) >= 0)
+    ts = np.linspace(0.1, 0.6, 51)          # strictly increasing away from saturation
+    assert np.all(np.diff([O.alpha(t) for t in ts]) > 0)
+    assert np.all(np.diff([O.eps(t) for t in ts]) > 0)
+
+
+def test_scaled_map_h_of_x():
+    """H = sqrt(alpha)/2 (3I - alpha((1-2eps) X + eps I)) with alpha(t_k), eps(t_k): for a
+    diagonal X the map is the scalar logistic h_alpha of the shifted-scaled eigenvalue,
+    whose fixed-point product h^2 x equals the standard NS map g(u) = u(3-u)^2/4 at
+    u = alpha x~ scaled by x / x~."""
+    n, b = 64, 16
+    lam = np.linspace(0.02, 1.0, n)
+    S = O.OMat.from_dense(np.diag(lam), b)
+    Y, Z = O.ns_y0(S, 1.0), O.OMat.identity(n, b)
+    Yn, Zn, H, t, _ = O.ns_step(Y, Z, 0.0, scaled=True)
+    a, e = O.alpha(t), O.eps(t)
+    x = lam
+    xt = (1 - 2 * e) * x + e
+    u = a * xt
+    h = np.diag(H.to_dense())
+    assert a > 2.5 and e > 0.09      # t_0 ~ .49: strongly scaled, stabilised
+    # h^2 x~ = g(u): the NS logistic in the scaled variable u = alpha x~
+    np.testing.assert_allclose(h * h * xt, u * (3 - u) ** 2 / 4, rtol=1e-14)
+    assert t == pytest.approx(1 - lam.mean(), abs=1e-15)
+    assert np.count_nonzero(H.to_dense() - np.diag(h)) == 0
+
+
+def test_scaled_converges_to_eig_and_accelerates():
+    """At tau = 0 the scaled/stabilised iteration still converges to s^{+-1/2}
+    (eigendecomposition; the sigmoids leave alpha - 1 ~ 5e-8, eps ~ 2e-11 at t = 0, so
+    the fixed point is shifted by O(eps)), and reaches t_k < 1e-10 in fewer steps than
+    the plain map on an ill-conditioned s (the purpose of the scaling)."""
+    n, b = 128, 16
+    g = _rng(5).standard_normal((n, n)) * np.exp(-0.05 * np.abs(np.subtract.outer(np.arange(n), np.arange(n))))
+    s = g @ g.T / n
+    w, V = np.linalg.eigh(s)
+    w = np.geomspace(1e-4, 1.0, n)                    # kappa = 1e4
+    s = (V * w) @ V.T
+    s = 0.5 * (s + s.T)
+    S = O.OMat.from_dense(s, b)
+    plain = O.ns_sqrt(S, 0.0, 60, scale=1.0, t_stop=1e-10)
+    scaled = O.ns_sqrt(S, 0.0, 60, scale=1.0, t_stop=1e-10, scaled=True)
+    assert scaled["iters"] < plain["iters"] <= 60
+    for M, p in ((scaled["Y"], 0.5), (scaled["Z"], -0.5)):
+        ref = _eig_pow(s, p)
+        assert np.linalg.norm(M.to_dense() - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+def test_t_stop_prefix():
+    """t_stop ends the run at the first k with |t_k| <= t_stop; the history
+    is the prefix of the fixed-count run."""
+    cfg = si.CONFIGS["C1"]
+    S = O.OMat.from_dense(si.kms(cfg.n, cfg.rho), cfg.b)
+    full = O.ns_sqrt(S, cfg.tau, cfg.iters, scale=3.0)
+    stop = O.ns_sqrt(S, cfg.tau, cfg.iters, scale=3.0, t_stop=1e-6)
+    k = stop["iters"]
+    assert 0 < k < cfg.iters
+    assert np.array_equal(stop["t"], full["t"][:k])
+    assert abs(stop["t"][-1]) <= 1e-6 and np.all(np.abs(full["t"][:k - 1]) > 1e-6)
