@@ -234,6 +234,9 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
                         for (int nf = 0; nf < NF; nf++)
                             dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s], bf[nf][s]);
             }
+            // The stage is refilled by TMA (async proxy) after this release: order this
+            // thread's generic-proxy reads of it before those writes (cross-proxy WAR).
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) {

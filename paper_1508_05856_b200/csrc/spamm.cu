@@ -8,6 +8,8 @@
 //       (Eq. cannonical P:383-389 in the north_star form, reading L8)
 //   spamm_ns_sqrt  : setup (c, Y0 = s/c, Z0 = I) + iters steps + unscale.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -89,6 +91,98 @@ static spamm_status check_pair(spamm_ctx ctx, spamm_mat A, spamm_mat B, double t
     return SPAMM_OK;
 }
 
+// ------------------------------------------------------------ self-check
+// SPAMM_SELFCHECK=1 (debug): every product re-runs its cull and its leaf GEMM and
+// compares the task lists / output blocks bitwise (both are deterministic by
+// construction); mismatches are reported on stderr.
+static int selfcheck_mode()
+{
+    static int m = -1;
+    if (m < 0) {
+        const char *e = getenv("SPAMM_SELFCHECK");
+        m = (e && *e == '1') ? 1 : 0;
+    }
+    return m;
+}
+
+__global__ void k_cmp_words(const uint32_t *a, const uint32_t *b, int64_t n, unsigned long long *mism,
+                            unsigned long long *first)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (a[i] != b[i]) {
+            atomicAdd(mism, 1ull);
+            atomicMin(first, (unsigned long long)i);
+        }
+}
+
+static long long cmp_words(spamm_ctx ctx, const void *a, const void *b, int64_t bytes, long long *first_word)
+{
+    unsigned long long *d = dalloc<unsigned long long>(ctx, 2);
+    unsigned long long h[2] = {0, ~0ull};
+    cudaMemcpyAsync(d, h, sizeof h, cudaMemcpyHostToDevice, ctx->stream);
+    k_cmp_words<<<296, 256, 0, ctx->stream>>>((const uint32_t *)a, (const uint32_t *)b, bytes / 4, d, d + 1);
+    cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    dev_free(ctx, d, 16);
+    *first_word = (long long)h[1];
+    return (long long)h[0];
+}
+
+static void *snapshot(spamm_ctx ctx, const void *src, int64_t bytes)
+{
+    void *p = dev_alloc(ctx, bytes > 0 ? bytes : 1);
+    if (bytes > 0) cudaMemcpyAsync(p, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream);
+    return p;
+}
+
+static int64_t g_product_id = 0;
+
+static void selfcheck_cull(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau)
+{
+    const int64_t nt = cw->ntasks, ns = cw->nsegs;
+    void *tA = snapshot(ctx, cw->tA, 4 * nt), *tB = snapshot(ctx, cw->tB, 4 * nt);
+    void *sc = snapshot(ctx, cw->seg_code, 4 * ns), *ss = snapshot(ctx, cw->seg_start, 4 * ns),
+         *sl = snapshot(ctx, cw->seg_len, 4 * ns);
+    cull_run(ctx, cw, A, B, tau, A->r0, A->r1);
+    long long f[5], m[5];
+    m[0] = cw->ntasks == nt && cw->nsegs == ns ? 0 : -1;
+    if (!m[0]) {
+        m[0] = cmp_words(ctx, tA, cw->tA, 4 * nt, &f[0]);
+        m[1] = cmp_words(ctx, tB, cw->tB, 4 * nt, &f[1]);
+        m[2] = cmp_words(ctx, sc, cw->seg_code, 4 * ns, &f[2]);
+        m[3] = cmp_words(ctx, ss, cw->seg_start, 4 * ns, &f[3]);
+        m[4] = cmp_words(ctx, sl, cw->seg_len, 4 * ns, &f[4]);
+    } else {
+        m[1] = m[2] = m[3] = m[4] = 0;
+    }
+    if (m[0] || m[1] || m[2] || m[3] || m[4])
+        fprintf(stderr, "SELFCHECK cull mismatch product %lld: counts %lld/%lld vs %lld/%lld, tA %lld tB %lld code %lld start %lld len %lld\n",
+                (long long)g_product_id, (long long)nt, (long long)ns, (long long)cw->ntasks, (long long)cw->nsegs,
+                m[0], m[1], m[2], m[3], m[4]);
+    for (void *q : {tA, tB, sc, ss, sl}) dev_free(ctx, q, 1);
+}
+
+static void selfcheck_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *halo, spamm_mat C,
+                           int epi)
+{
+    spamm_mat m2 = nullptr;
+    if (mat_new(ctx, A->n, A->b, cw->nsegs + A->nb, &m2)) return;
+    mat_reset_pattern(ctx, m2);
+    double *tr = dalloc<double>(ctx, A->nb);
+    cudaMemsetAsync(tr, 0, sizeof(double) * A->nb, ctx->stream);
+    cudaMemsetAsync(cw->counters + CNT_GEMM_TICKET, 0, sizeof(int32_t), ctx->stream);
+    gemm_run(ctx, cw, A, B, halo, m2, epi, tr);
+    const int64_t b2 = (int64_t)A->b * A->b;
+    long long f0, f1;
+    long long m0 = cmp_words(ctx, C->pool, m2->pool, 8 * b2 * cw->nsegs, &f0);
+    long long m1 = cmp_words(ctx, C->norm2 + pyr_off(C->L), m2->norm2 + pyr_off(C->L), 8 * (int64_t)A->nb * A->nb, &f1);
+    if (m0 || m1)
+        fprintf(stderr, "SELFCHECK gemm mismatch product %lld epi %d: pool words %lld (first block %lld), leaf n2 words %lld; tasks %lld segs %lld\n",
+                (long long)g_product_id, epi, m0, f0 / (2 * b2), m1, (long long)cw->ntasks, (long long)cw->nsegs);
+    dev_free(ctx, tr, 8 * A->nb);
+    spamm_mat_free(m2);
+}
+
 // product with a given workspace and epilogue; C allocated here
 static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
                             double *trace_part, spamm_mat *C)
@@ -99,6 +193,8 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
     spamm_status sc = cull_run(ctx, cw, A, B, tau, A->r0, A->r1);
     prof_end(ctx, pc);
     if (sc) return sc;
+    g_product_id++;
+    if (selfcheck_mode()) selfcheck_cull(ctx, cw, A, B, tau);
     // row partition: fetch the remote right-operand tiles the local tasks use
     double *halo = nullptr;
     int64_t nhalo = 0;
@@ -125,6 +221,7 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
         st = gemm_run(ctx, cw, A, B, halo, m, epi, trace_part);
         prof_end(ctx, pg);
         prof_gemm_work(ctx, cw->ntasks, cw->nsegs, A->b);
+        if (!st && selfcheck_mode()) selfcheck_gemm(ctx, cw, A, B, halo, m, epi);
     }
     dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
     if (!st) {

@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -37,15 +38,29 @@ spamm_status check_cuda(spamm_ctx ctx, cudaError_t e, const char *what)
 }
 
 // ---------------------------------------------------------------- memory
+// SPAMM_POISON=1 (debug): every allocation is filled with 0xFF bytes (NaN doubles,
+// -1 ints) so a read of memory no kernel wrote shows up as NaN / a bad slot.
+static int poison_mode()
+{
+    static int m = -1;
+    if (m < 0) {
+        const char *e = getenv("SPAMM_POISON");
+        m = (e && *e == '1') ? 1 : 0;
+    }
+    return m;
+}
+
 void *dev_alloc(spamm_ctx ctx, size_t bytes)
 {
     bytes = (bytes + 255) & ~size_t(255);
-    if (ctx->has_alloc) return ctx->alloc.alloc(bytes, (void *)ctx->stream, ctx->alloc.user);
     void *p = nullptr;
-    if (cudaMallocAsync(&p, bytes, ctx->stream) != cudaSuccess) {
+    if (ctx->has_alloc) {
+        p = ctx->alloc.alloc(bytes, (void *)ctx->stream, ctx->alloc.user);
+    } else if (cudaMallocAsync(&p, bytes, ctx->stream) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
+    if (p && poison_mode()) cudaMemsetAsync(p, 0xFF, bytes, ctx->stream);
     return p;
 }
 

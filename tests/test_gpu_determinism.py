@@ -1,0 +1,78 @@
+"""Run-to-run determinism of the CUDA path (B200).
+
+Every product is deterministic by construction (one CTA owns an output block and
+accumulates its tasks in ascending k; fixed-order reductions), so repeated runs
+must agree bitwise.  This caught a cross-proxy race in the leaf GEMM (generic
+shared-memory reads of a stage vs. the TMA refill of that stage, fixed with
+fence.proxy.async before the consumer's release), which corrupted ~1 product in
+20 by a few ulps.  SPAMM_SELFCHECK=1 re-runs each cull and GEMM inside the
+library and reports any bitwise mismatch on stderr."""
+import hashlib
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import spamm_inputs as si
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def sp():
+    import paper_1508_05856_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def _hash(ctx, M):
+    bi, bj, blk = sp().spamm_export_blocks(ctx, M)
+    o = np.lexsort((bj, bi))
+    return hashlib.sha1(bi[o].tobytes() + bj[o].tobytes() + blk[o].tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("library_stream", [False, True])
+def test_repeated_products_bitwise(gpu, library_stream):
+    n, b = 4096, 64
+    cfg = si.Config("t", "gauss", n, b, 1e-7, 30, sigma=0.8, shift=1e-3, seed=150805856, tau_min=1e-7)
+    payload = si.make_input(cfg)[1]
+    ctx = sp().spamm_ctx_create(0, library_stream=library_stream)
+    S = sp().spamm_build_tree_blocks(ctx, n, b, *payload)
+    Y, Z = sp().spamm_ns_y0(ctx, S, 11.0), sp().spamm_identity(ctx, n, b)
+    for _ in range(4):
+        Y, Z, _, _ = sp().spamm_ns_step(ctx, Y, Z, 1e-7, 1e-9)
+    seen = {"X": set(), "Hs": set(), "Ys": set(), "H": set()}
+    for _ in range(25):
+        X = sp().spamm_multiply(ctx, Z, Y, 1e-7)
+        seen["X"].add(_hash(ctx, X))
+        X.free()
+        Yn, Zn, _, _, _, H = sp().spamm_ns_step_map(ctx, Y, Z, 1e-7, 1e-9, scaled=True, want_h=True)
+        seen["Hs"].add(_hash(ctx, H))
+        seen["Ys"].add(_hash(ctx, Yn))
+        for m in (Yn, Zn, H):
+            m.free()
+        Yn, Zn, _, _, H = sp().spamm_ns_step(ctx, Y, Z, 1e-7, 1e-9, want_h=True)
+        seen["H"].add(_hash(ctx, H))
+        for m in (Yn, Zn, H):
+            m.free()
+    assert all(len(v) == 1 for v in seen.values()), {k: len(v) for k, v in seen.items()}
+
+
+def test_selfcheck_reports_no_mismatch(gpu):
+    code = ("import sys; sys.path.insert(0, %r); import paper_1508_05856_b200 as sp, spamm_inputs as si\n"
+            "c = si.CONFIGS['C2']; s = si.kms(c.n, c.rho); ctx = sp.spamm_ctx_create(0)\n"
+            "S = sp.spamm_build_tree(ctx, s, c.b); r = sp.spamm_ns_sqrt(ctx, S, c.tau, 12)\n"
+            "print('ok', r['iters'])\n") % ROOT
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "SPAMM_SELFCHECK": "1"})
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert "ok 12" in p.stdout
+    assert "SELFCHECK" not in p.stderr, p.stderr[-2000:]
