@@ -172,6 +172,10 @@ class Ctx:
             stream, torch_allocator = None, False
         elif stream is None:
             stream = torch.cuda.current_stream(device)
+            if stream.cuda_stream == 0:
+                # the legacy default stream: give the library a real torch stream so
+                # that events recorded on ctx.stream bracket the library's own work
+                stream = torch.cuda.Stream(device)
         self.stream = stream
         self._keep = []
         alloc_p = None
@@ -197,6 +201,16 @@ class Ctx:
         if rc:
             raise SpammError(rc, "spamm_ctx_create failed (device must be sm_100)")
         self.h = h
+
+    def sync_in(self):
+        """Order the library stream after torch's current stream (device inputs)."""
+        if self.stream is not None:
+            self.stream.wait_stream(self.torch.cuda.current_stream(self.device))
+
+    def sync_out(self):
+        """Order torch's current stream after the library stream (device outputs)."""
+        if self.stream is not None:
+            self.torch.cuda.current_stream(self.device).wait_stream(self.stream)
 
     def check(self, rc):
         if rc:
@@ -338,12 +352,14 @@ def spamm_build_tree(ctx: Ctx, dense, b: int) -> Mat:
     """dense: n x n row-major fp64 torch tensor (cuda or cpu) or numpy array."""
     n = dense.shape[0]
     h = C.c_void_p()
+    ctx.sync_in()
     ctx.check(load().spamm_build_tree(ctx.h, _ptr(dense), n, dense.shape[1], b, C.byref(h)))
     return Mat(ctx, h)
 
 
 def spamm_build_tree_blocks(ctx: Ctx, n: int, b: int, bi, bj, blocks) -> Mat:
     h = C.c_void_p()
+    ctx.sync_in()
     ctx.check(load().spamm_build_tree_blocks(ctx.h, n, b, len(bi), _ptr(bi), _ptr(bj),
                                              _ptr(blocks), C.byref(h)))
     return Mat(ctx, h)
@@ -371,7 +387,11 @@ def spamm_to_dense(ctx: Ctx, m: Mat, out=None, device: bool = True):
             out = ctx.torch.empty((n, n), dtype=ctx.torch.float64, device=f"cuda:{ctx.device}")
         else:
             out = np.empty((n, n))
+    if not isinstance(out, np.ndarray):
+        ctx.sync_in()          # the output buffer was allocated on torch's stream
     ctx.check(load().spamm_to_dense(ctx.h, m.h, _ptr(out), out.shape[1]))
+    if not isinstance(out, np.ndarray):
+        ctx.sync_out()
     return out
 
 
@@ -493,8 +513,10 @@ def spamm_export_blocks(ctx: Ctx, m: Mat, out=None):
         b = m.b
         out = (np.empty(k, dtype=np.int32), np.empty(k, dtype=np.int32), np.empty((k, b, b)))
     bi, bj, blocks = out
+    ctx.sync_in()
     ctx.check(load().spamm_export_blocks(ctx.h, m.h, _ptr(bi), _ptr(bj), _ptr(blocks), k,
                                          C.byref(n)))
+    ctx.sync_out()
     return bi[:k], bj[:k], blocks[:k]
 
 
