@@ -67,6 +67,8 @@ struct spamm_ctx_s {
     spamm_comm comm = nullptr;
     std::vector<int> row_start;   // [world+1] block rows; empty => equal split per nb
     struct Dist *dist = nullptr;  // exchange workspaces
+    cudaStream_t comm_stream = nullptr;   // halo exchange overlapped with the local GEMM
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
 
 struct spamm_mat_s {
@@ -159,11 +161,14 @@ spamm_status check_cuda(spamm_ctx ctx, cudaError_t e, const char *what);
         cudaError_t _e = (call);                                              \
         if (_e != cudaSuccess) return check_cuda(ctx, _e, #call);             \
     } while (0)
+#define SPAMM_STR2(x) #x
+#define SPAMM_STR(x) SPAMM_STR2(x)
 #define CKL(ctx)                                                              \
     do {                                                                      \
         (ctx)->launches++;                                                    \
         cudaError_t _e = cudaGetLastError();                                  \
-        if (_e != cudaSuccess) return check_cuda(ctx, _e, "kernel launch");   \
+        if (_e != cudaSuccess)                                                \
+            return check_cuda(ctx, _e, "kernel launch at " __FILE__ ":" SPAMM_STR(__LINE__)); \
     } while (0)
 #define ST(call)                                                              \
     do {                                                                      \
@@ -191,6 +196,9 @@ spamm_status gather_rows(spamm_ctx ctx, const Parts &p, double *vec, int width);
 // fetch the remote right-operand blocks the local tasks of cw use; patches
 // cw->tB (remote => -(h+1), h = halo slot) and returns the halo pool
 spamm_status halo_exchange(spamm_ctx ctx, struct Cull *cw, spamm_mat B, double **halo, int64_t *nhalo);
+// stable split of the segments into all-local (every task's B block is row-local)
+// then remote-using ones: order[nsegs] (device, caller frees), *nlocal (host)
+spamm_status seg_split(spamm_ctx ctx, struct Cull *cw, int32_t **order, int64_t *nlocal);
 void dist_free(spamm_ctx ctx);
 
 // cull.cu — the level-by-level two-sided norm query (Eq. newspamm)
@@ -222,8 +230,11 @@ spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj_host, int64_t cap
 
 // gemm.cu — FP64 DMMA leaf GEMM with fused epilogues
 enum { EPI_STORE = 0, EPI_NS_H = 1, EPI_NS_X = 2 };
+// seg_order (nullable) / nseg (< 0 => all cw->nsegs) select the segments of this launch;
+// ticket = which of the GEMM ticket counters (zeroed by the cull) the launch uses
 spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
-                      spamm_mat C, int epi, double *trace_part);
+                      spamm_mat C, int epi, double *trace_part, const int32_t *seg_order = nullptr,
+                      int64_t nseg = -1, int ticket = 0);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
 // scaled / stabilised NS map in place over X: coef <- {alpha, eps, sqrt(alpha)/2}(t)
 spamm_status ns_scaled_map(spamm_ctx ctx, spamm_mat X, const double *t, double *coef);

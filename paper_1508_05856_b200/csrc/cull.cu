@@ -132,6 +132,9 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
     __shared__ int4 sw[CT / 32];
     __shared__ int s_tile;
     __shared__ int4 s_excl;
+    // after a capacity overflow the truncated level's group indices point past the
+    // arrays: skip the rest of the query (the host grows the workspace and re-runs)
+    if (*(volatile int32_t *)&cnt[CNT_OVERFLOW]) return;
     const int n = clamp_n(cnt, l, g.cap);
     const double T = cull_T(g);
     const double *an = g.a_n2 + pyr_off(l + 1), *bn = g.b_n2 + pyr_off(l + 1);
@@ -195,6 +198,7 @@ __global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const i
                                                       int4 *rec_out, int32_t *tA, int32_t *tB,
                                                       int32_t *tK, const int32_t *cnt)
 {
+    if (cnt[CNT_OVERFLOW]) return;   // see k_cull_scan
     const int n = clamp_n(cnt, l, g.cap);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         uint32_t m = mask[t];
@@ -239,6 +243,7 @@ __global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const i
 __global__ void k_cull_leaf_direct(CullArgs g, int l, const int4 *rec, int32_t *tA, int32_t *tB,
                                    int32_t *tK, const int32_t *cnt)
 {
+    if (cnt[CNT_OVERFLOW]) return;
     const int n = clamp_n(cnt, l, g.cap);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         int4 r = rec[t];
@@ -257,6 +262,7 @@ __global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, in
 {
     __shared__ V1 sw[CT / 32];
     __shared__ int s_tile, s_excl;
+    if (*(volatile int32_t *)&cnt[CNT_OVERFLOW]) return;
     const int n = clamp_n(cnt, L, cap);
     int tile;
     while ((tile = next_tile(st.ticket, n, CT, &s_tile)) >= 0) {

@@ -310,7 +310,80 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
     return SPAMM_OK;
 }
 
-void dist_free(spamm_ctx) {}
+// ------------------------------------------------- local-first segment order
+// flag[s] = 1 iff every task of segment s reads a row-local B block (tB >= 0); those
+// segments can run while the halo is in flight (overlap at
+// segment granularity, never splitting a segment, so the k order is unchanged).
+__global__ void k_seg_local(const int32_t *seg_start, const int32_t *seg_len, const int32_t *tB, int64_t nseg,
+                            int32_t *flag)
+{
+    int64_t s = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s >= nseg) return;
+    const int st = seg_start[s], len = seg_len[s];
+    bool remote = false;
+    for (int t = lane; t < len; t += 32) remote |= tB[st + t] < 0;
+    remote = __any_sync(0xffffffffu, remote);
+    if (lane == 0) flag[s] = remote ? 0 : 1;
+}
+
+// stable partition: local segments first (ascending), then the others (ascending)
+__global__ void k_seg_order(const int32_t *flag, const int32_t *excl, int64_t nseg, int32_t *order)
+{
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    const int64_t nloc = excl[nseg];
+    const int64_t pos = flag[s] ? excl[s] : nloc + (s - excl[s]);
+    order[pos] = (int32_t)s;
+}
+
+spamm_status seg_split(spamm_ctx ctx, Cull *cw, int32_t **order, int64_t *nlocal)
+{
+    const int64_t ns = cw->nsegs;
+    *order = nullptr;
+    *nlocal = 0;
+    cudaStream_t s = ctx->stream;
+    int32_t *flag = dalloc<int32_t>(ctx, ns), *excl = dalloc<int32_t>(ctx, ns + 1);
+    int32_t *ord = dalloc<int32_t>(ctx, ns);
+    const int ntiles = cdiv(std::max<int64_t>(ns, 1), 512);
+    int32_t *flags = dalloc<int32_t>(ctx, ntiles + 1);
+    V1 *agg = dalloc<V1>(ctx, ntiles), *pre = dalloc<V1>(ctx, ntiles);
+    if (!flag || !excl || !ord || !flags || !agg || !pre) return set_err(ctx, SPAMM_ENOMEM, "segment split");
+    spamm_status st = SPAMM_OK;
+    int32_t h = 0;
+    if (ns > 0) {
+        k_seg_local<<<cdiv(ns, 8), 256, 0, s>>>(cw->seg_start, cw->seg_len, cw->tB, ns, flag);
+        ctx->launches++;
+        cudaMemsetAsync(flags, 0, sizeof(int32_t) * (ntiles + 1), s);
+        ScanTiles<V1> tiles{flags, agg, pre, flags + ntiles};
+        k_need_scan<512><<<std::min(ntiles, 2 * ctx->sm_count), 512, 0, s>>>(flag, ns, tiles, excl);
+        k_seg_order<<<cdiv(ns, 256), 256, 0, s>>>(flag, excl, ns, ord);
+        ctx->launches += 2;
+        cudaMemcpyAsync(&h, excl + ns, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = check_cuda(ctx, e, "segment split");
+    }
+    dev_free(ctx, flag, sizeof(int32_t) * ns);
+    dev_free(ctx, excl, sizeof(int32_t) * (ns + 1));
+    dev_free(ctx, flags, sizeof(int32_t) * (ntiles + 1));
+    dev_free(ctx, agg, sizeof(V1) * ntiles);
+    dev_free(ctx, pre, sizeof(V1) * ntiles);
+    if (st) {
+        dev_free(ctx, ord, sizeof(int32_t) * ns);
+        return st;
+    }
+    *order = ord;
+    *nlocal = h;
+    return SPAMM_OK;
+}
+
+void dist_free(spamm_ctx ctx)
+{
+    if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    ctx->comm_stream = nullptr;
+}
 
 // ------------------------------------------------------------------ ABI
 extern "C" spamm_status spamm_ctx_set_comm(spamm_ctx ctx, spamm_comm comm, const int32_t *row_start)

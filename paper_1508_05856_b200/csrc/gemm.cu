@@ -27,7 +27,8 @@ struct GemmArgs {
     const double *b_halo;   // remote right-operand tiles (row partition): tB = -(h+1)
     const int32_t *tA, *tB;
     const int32_t *seg_code, *seg_start, *seg_len;
-    int nseg;
+    int nseg;               // segments of this launch
+    const int32_t *seg_order;  // nullable: launch-local ticket q -> segment seg_order[q]
     double *c_pool;
     int32_t *c_coord, *c_slot;
     double *c_leaf_n2;
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
             if (lane == 0) {
                 seg = atomicAdd(g.ticket, 1);
                 if (seg >= g.nseg) seg = -1;
+                else if (g.seg_order) seg = g.seg_order[seg];
                 mbar_wait(&qempty[q], qphase ^ 1);
                 segq[q] = seg;
                 mbar_arrive(&qfull[q]);
@@ -330,11 +332,13 @@ static spamm_status gemm_dispatch(spamm_ctx ctx, int b, const GemmArgs &g)
 }
 
 spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
-                      spamm_mat C, int epi, double *trace_part)
+                      spamm_mat C, int epi, double *trace_part, const int32_t *seg_order, int64_t nseg,
+                      int ticket)
 {
+    if (nseg < 0) nseg = cw->nsegs;
     GemmArgs g{A->pool, B->pool, b_halo, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
-               (int)cw->nsegs, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
-               cw->counters + CNT_GEMM_TICKET};
+               (int)nseg, seg_order, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
+               cw->counters + CNT_GEMM_TICKET + ticket};
     if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H>(ctx, A->b, g);
     if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X>(ctx, A->b, g);
     return gemm_dispatch<EPI_STORE>(ctx, A->b, g);

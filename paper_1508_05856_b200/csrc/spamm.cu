@@ -183,6 +183,57 @@ static void selfcheck_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, co
     spamm_mat_free(m2);
 }
 
+// Row partition, world > 1: GEMM over the all-local
+// segments on the context stream || halo exchange on the communication stream,
+// then the GEMM over the segments that use remote tiles.  Each segment is owned
+// by one CTA and accumulated in ascending k, so the split changes no result.
+static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_mat m, int epi,
+                                    double *trace_part)
+{
+    if (!ctx->comm_stream) {
+        CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+        for (auto &e : ctx->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const cudaStream_t main_s = ctx->stream, comm_s = ctx->comm_stream;
+    int32_t *order = nullptr;
+    int64_t nloc = 0;
+    ST(seg_split(ctx, cw, &order, &nloc));
+    const int64_t nrem = cw->nsegs - nloc;
+    // the exchange reads the cull's records / tB: comm stream after main
+    CK(cudaEventRecord(ctx->ev[0], main_s));
+    CK(cudaStreamWaitEvent(comm_s, ctx->ev[0], 0));
+    int pg = prof_begin(ctx, SPAMM_PH_GEMM);
+    spamm_status st = gemm_run(ctx, cw, A, B, nullptr, m, epi, trace_part, order, nloc, 0);
+    prof_end(ctx, pg);
+    // halo exchange with every allocation, kernel and collective on the comm stream
+    double *halo = nullptr;
+    int64_t nhalo = 0;
+    if (!st) {
+        ctx->stream = comm_s;
+        int px = prof_begin(ctx, SPAMM_PH_OTHER);
+        st = halo_exchange(ctx, cw, B, &halo, &nhalo);
+        prof_end(ctx, px);
+        ctx->stream = main_s;
+    }
+    if (!st) {
+        CK(cudaEventRecord(ctx->ev[1], comm_s));
+        CK(cudaStreamWaitEvent(main_s, ctx->ev[1], 0));
+        int pg2 = prof_begin(ctx, SPAMM_PH_GEMM);
+        st = gemm_run(ctx, cw, A, B, halo, m, epi, trace_part, order + nloc, nrem, 1);
+        prof_end(ctx, pg2);
+        prof_gemm_work(ctx, cw->ntasks, cw->nsegs, A->b);
+    }
+    // the halo was allocated on the comm stream: free it there, after the GEMM read it
+    CK(cudaEventRecord(ctx->ev[2], main_s));
+    CK(cudaStreamWaitEvent(comm_s, ctx->ev[2], 0));
+    ctx->stream = comm_s;
+    dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
+    ctx->stream = main_s;
+    dev_free(ctx, order, sizeof(int32_t) * cw->nsegs);
+    if (!st && selfcheck_mode()) selfcheck_gemm(ctx, cw, A, B, nullptr, m, epi);
+    return st;
+}
+
 // product with a given workspace and epilogue; C allocated here
 static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
                             double *trace_part, spamm_mat *C)
@@ -195,10 +246,11 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
     if (sc) return sc;
     g_product_id++;
     if (selfcheck_mode()) selfcheck_cull(ctx, cw, A, B, tau);
-    // row partition: fetch the remote right-operand tiles the local tasks use
+    const bool overlap = A->dist && A->parts.world > 1;
     double *halo = nullptr;
     int64_t nhalo = 0;
-    if (A->dist) {
+    if (A->dist && !overlap) {
+        // world size 1: nothing is remote, the exchange is a no-op
         int px = prof_begin(ctx, SPAMM_PH_OTHER);
         sc = halo_exchange(ctx, cw, B, &halo, &nhalo);
         prof_end(ctx, px);
@@ -216,7 +268,11 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
         return st;
     }
     st = mat_reset_pattern(ctx, m);
-    if (!st) {
+    if (!st && overlap) {
+        // row partition, world > 1: the all-local segments run while the halo of remote
+        // right-operand tiles is exchanged on the communication stream; then the rest
+        st = overlapped_gemm(ctx, cw, A, B, m, epi, trace_part);
+    } else if (!st) {
         int pg = prof_begin(ctx, SPAMM_PH_GEMM);
         st = gemm_run(ctx, cw, A, B, halo, m, epi, trace_part);
         prof_end(ctx, pg);
