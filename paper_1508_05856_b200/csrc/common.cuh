@@ -236,6 +236,8 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
                       spamm_mat C, int epi, double *trace_part, const int32_t *seg_order = nullptr,
                       int64_t nseg = -1, int ticket = 0);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
+// out[0..n) = the segments of `in` (nullable => 0..n-1), longest first (a schedule only)
+spamm_status lpt_order(spamm_ctx ctx, const int32_t *seg_len, const int32_t *in, int64_t n, int32_t *out);
 // scaled / stabilised NS map in place over X: coef <- {alpha, eps, sqrt(alpha)/2}(t)
 spamm_status ns_scaled_map(spamm_ctx ctx, spamm_mat X, const double *t, double *coef);
 // append value*I blocks for absent diagonal positions at slots base..; *added = count (syncs)

@@ -104,8 +104,10 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
     uint64_t *empty = full + STAGES;
     uint64_t *qfull = empty + STAGES;
     uint64_t *qempty = qfull + QN;
-    int *segq = reinterpret_cast<int *>(qempty + QN);
-    double *red = reinterpret_cast<double *>(segq + 2 * QN);  // [2 parity][2 (ss,tr)][CW]
+    int4 *segq = reinterpret_cast<int4 *>(qempty + QN);     // {seg, len, code, -} per queue entry
+    constexpr int RS = 2 * QN;                                // epilogue reduction slots (> QN)
+    double *red = reinterpret_cast<double *>(segq + QN);      // [RS][2 (ss,tr)][CW]
+    int *rcnt = reinterpret_cast<int *>(red + RS * 2 * CW);   // [RS] warps done per slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -117,6 +119,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
             mbar_init(&qfull[q], 1);
             mbar_init(&qempty[q], CW);
         }
+        for (int r = 0; r < RS; r++) rcnt[r] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -128,22 +131,29 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
         int stage = 0, q = 0;
         uint32_t phase = 0, qphase = 0;
         for (;;) {
-            int seg = 0;
+            int seg = 0, start = 0, len = 0;
             if (lane == 0) {
                 seg = atomicAdd(g.ticket, 1);
                 if (seg >= g.nseg) seg = -1;
                 else if (g.seg_order) seg = g.seg_order[seg];
+                int code = 0;
+                if (seg >= 0) {
+                    start = g.seg_start[seg];
+                    len = g.seg_len[seg];
+                    code = g.seg_code[seg];
+                }
                 mbar_wait(&qempty[q], qphase ^ 1);
-                segq[q] = seg;
+                segq[q] = make_int4(seg, len, code, 0);
                 mbar_arrive(&qfull[q]);
             }
             seg = __shfl_sync(0xffffffffu, seg, 0);
+            start = __shfl_sync(0xffffffffu, start, 0);
+            len = __shfl_sync(0xffffffffu, len, 0);
             if (++q == QN) {
                 q = 0;
                 qphase ^= 1;
             }
             if (seg < 0) break;
-            const int start = g.seg_start[seg], len = g.seg_len[seg];
             for (int t0 = 0; t0 < len; t0 += 32) {
                 const int t = t0 + lane;
                 const int sa = t < len ? g.tA[start + t] : 0;
@@ -191,19 +201,20 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
 
     int stage = 0, q = 0;
     uint32_t phase = 0, qphase = 0;
-    int par = 0;
+    int slot = 0;
     for (;;) {
         mbar_wait(&qfull[q], qphase);
-        const int seg = segq[q];
+        const int4 e = segq[q];
         __syncwarp();
         if (lane == 0) mbar_arrive(&qempty[q]);
         if (++q == QN) {
             q = 0;
             qphase ^= 1;
         }
+        const int seg = e.x;
         if (seg < 0) break;
-        const int len = g.seg_len[seg];
-        const uint32_t code = g.seg_code[seg];
+        const int len = e.y;
+        const uint32_t code = (uint32_t)e.z;
         double acc[MF][NF][2];
 #pragma unroll
         for (int i = 0; i < MF; i++)
@@ -277,25 +288,32 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
             ss += __shfl_xor_sync(0xffffffffu, ss, o);
             tr += __shfl_xor_sync(0xffffffffu, tr, o);
         }
-        double *rp = red + par * 2 * CW;
+        // No CTA barrier: each warp deposits its partials in this segment's slot and
+        // the last warp to arrive sums the CW partials in warp order (deterministic)
+        // and writes the block's metadata; the others go on to the next segment.
+        // Warps drift apart by < QN segments (queue entries are released only when
+        // every warp has taken them), so RS = 2 QN slots are never reused early.
         if (lane == 0) {
+            double *rp = red + slot * 2 * CW;
             rp[warp] = ss;
             rp[CW + warp] = tr;
-        }
-        asm volatile("bar.sync 1, %0;\n" ::"n"(CW * 32) : "memory");
-        if (threadIdx.x == 0) {
-            double s2 = 0.0, t2 = 0.0;
+            __threadfence_block();
+            if (atomicAdd(&rcnt[slot], 1) == CW - 1) {
+                __threadfence_block();
+                double s2 = 0.0, t2 = 0.0;
 #pragma unroll
-            for (int w = 0; w < CW; w++) {
-                s2 += rp[w];
-                t2 += rp[CW + w];
+                for (int w = 0; w < CW; w++) {
+                    s2 += *(volatile double *)&rp[w];
+                    t2 += *(volatile double *)&rp[CW + w];
+                }
+                rcnt[slot] = 0;
+                g.c_leaf_n2[code] = s2;
+                g.c_coord[seg] = (int32_t)code;
+                g.c_slot[code] = seg;
+                if (EPI != EPI_STORE && diag) g.trace_part[I] = t2;
             }
-            g.c_leaf_n2[code] = s2;
-            g.c_coord[seg] = (int32_t)code;
-            g.c_slot[code] = seg;
-            if (EPI != EPI_STORE && diag) g.trace_part[I] = t2;
         }
-        par ^= 1;
+        if (++slot == RS) slot = 0;
     }
 }
 
@@ -303,8 +321,10 @@ template <int B, int CW, int WM, int WN, int STAGES, int EPI>
 static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
 {
     constexpr int NT = 32 * (CW + 1);
+    constexpr int QN = 4, RS = 2 * QN;   // as in the kernel
     const size_t smem = sizeof(double) * 2 * STAGES * B * B + 2 * STAGES * sizeof(uint64_t) +
-                        2 * 4 * sizeof(uint64_t) + 2 * 4 * sizeof(int) + 4 * CW * sizeof(double);
+                        2 * QN * sizeof(uint64_t) + QN * sizeof(int4) + RS * 2 * CW * sizeof(double) +
+                        RS * sizeof(int);
     auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI>;
     static int occ = 0;
     if (!occ) {
@@ -342,6 +362,60 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
     if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H>(ctx, A->b, g);
     if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X>(ctx, A->b, g);
     return gemm_dispatch<EPI_STORE>(ctx, A->b, g);
+}
+
+// ------------------------------------------------------- LPT segment order
+// The persistent GEMM takes segments from a ticket; running the longest first
+// bounds the tail of a launch by the shortest segments (longest-processing-time
+// first).  The order is only a schedule: every segment is owned by one CTA and
+// accumulated in ascending k whatever its position, so results do not depend on
+// it (positions inside a length bucket are taken with atomics).
+constexpr int LPT_BUCKETS = 1024;
+
+__global__ void k_lpt_hist(const int32_t *in, int64_t n, const int32_t *seg_len, int32_t *hist)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int s = in ? in[q] : (int)q;
+    const int len = seg_len[s];
+    atomicAdd(&hist[len < LPT_BUCKETS ? len : LPT_BUCKETS - 1], 1);
+}
+
+// single CTA: base[len] = number of segments longer than len (descending order)
+__global__ void __launch_bounds__(LPT_BUCKETS) k_lpt_scan(int32_t *hist)
+{
+    __shared__ V1 sw[LPT_BUCKETS / 32];
+    const int t = threadIdx.x;                 // t-th bucket from the top
+    const int bkt = LPT_BUCKETS - 1 - t;
+    V1 v{hist[bkt]};
+    V1 tot;
+    V1 ex = block_excl_scan<V1, LPT_BUCKETS>(v, &tot, sw);
+    hist[bkt] = ex.x;
+}
+
+__global__ void k_lpt_scatter(const int32_t *in, int64_t n, const int32_t *seg_len, int32_t *base, int32_t *out)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int s = in ? in[q] : (int)q;
+    const int len = seg_len[s];
+    out[atomicAdd(&base[len < LPT_BUCKETS ? len : LPT_BUCKETS - 1], 1)] = s;
+}
+
+spamm_status lpt_order(spamm_ctx ctx, const int32_t *seg_len, const int32_t *in, int64_t n, int32_t *out)
+{
+    if (n <= 0) return SPAMM_OK;
+    int32_t *hist = dalloc<int32_t>(ctx, LPT_BUCKETS);
+    if (!hist) return set_err(ctx, SPAMM_ENOMEM, "lpt histogram");
+    CK(cudaMemsetAsync(hist, 0, sizeof(int32_t) * LPT_BUCKETS, ctx->stream));
+    k_lpt_hist<<<cdiv(n, 256), 256, 0, ctx->stream>>>(in, n, seg_len, hist);
+    CKL(ctx);
+    k_lpt_scan<<<1, LPT_BUCKETS, 0, ctx->stream>>>(hist);
+    CKL(ctx);
+    k_lpt_scatter<<<cdiv(n, 256), 256, 0, ctx->stream>>>(in, n, seg_len, hist, out);
+    CKL(ctx);
+    dev_free(ctx, hist, sizeof(int32_t) * LPT_BUCKETS);
+    return SPAMM_OK;
 }
 
 // -------------------------------------------------- diagonal fix-up of H
