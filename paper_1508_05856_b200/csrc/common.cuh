@@ -184,7 +184,6 @@ spamm_status mat_new(spamm_ctx ctx, int64_t n, int b, int64_t cap, spamm_mat *ou
 spamm_status mat_reset_pattern(spamm_ctx ctx, spamm_mat m);     // slot=-1, leaf norms=0
 spamm_status pyramid_build(spamm_ctx ctx, spamm_mat m);           // levels L-1..0 from leaves
 spamm_status mat_map(spamm_ctx ctx, spamm_mat src, int op, double c, double mu, spamm_mat *out);
-spamm_status leaf_norms_from_pool(spamm_ctx ctx, spamm_mat m);  // recompute leaf norm2 from pool
 int is_device_ptr(const void *p);
 
 // dist.cu — the row-partitioned path

@@ -22,7 +22,8 @@
 #include "common.cuh"
 #include "scan.cuh"
 
-constexpr int CT = 512;  // scan tile = threads per CTA (one task per thread)
+constexpr int CT = 512;  // threads per CTA of the scan kernels
+constexpr int CI = 4;    // consecutive items per thread: a scan tile is CT*CI items
 
 struct CullArgs {
     const double *a_n2, *b_n2;   // pyramids
@@ -139,47 +140,66 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
     const double T = cull_T(g);
     const double *an = g.a_n2 + pyr_off(l + 1), *bn = g.b_n2 + pyr_off(l + 1);
     int tile;
-    while ((tile = next_tile(st.ticket, n, CT, &s_tile)) >= 0) {
-        int t = tile * CT + threadIdx.x;
-        int4 c = make_int4(0, 0, 0, 0);
-        uint32_t m = 0;
-        if (t < n) {
-            int4 r = rec[t];
-            uint32_t code = r.x;
-            int K = r.y, I = morton_i(code), J = morton_j(code);
-            const double2 *pa2 = reinterpret_cast<const double2 *>(an + 4 * (int64_t)morton(I, K));
-            const double2 *pb2 = reinterpret_cast<const double2 *>(bn + 4 * (int64_t)morton(K, J));
-            double2 a01 = __ldg(pa2), a23 = __ldg(pa2 + 1), b01 = __ldg(pb2), b23 = __ldg(pb2 + 1);
-            double pa[2][2] = {{a01.x, a01.y}, {a23.x, a23.y}};  // [di][dk]
-            double pb[2][2] = {{b01.x, b01.y}, {b23.x, b23.y}};  // [dk][dj]
+    // CI consecutive parent tasks per thread: a tile is CT*CI tasks, so the
+    // decoupled look-back walks CI times fewer predecessor tiles
+    while ((tile = next_tile(st.ticket, n, CT * CI, &s_tile)) >= 0) {
+        const int t0 = tile * (CT * CI) + threadIdx.x * CI;
+        int4 c[CI];
+        uint32_t m[CI];
+        int4 csum = make_int4(0, 0, 0, 0);
 #pragma unroll
-            for (int di = 0; di < 2; di++) {
-                if (!rows_meet(g, 2 * I + di, l + 1)) continue;
+        for (int i = 0; i < CI; i++) {
+            const int t = t0 + i;
+            c[i] = make_int4(0, 0, 0, 0);
+            m[i] = 0;
+            if (t < n) {
+                int4 r = rec[t];
+                uint32_t code = r.x;
+                int K = r.y, I = morton_i(code), J = morton_j(code);
+                const double2 *pa2 = reinterpret_cast<const double2 *>(an + 4 * (int64_t)morton(I, K));
+                const double2 *pb2 = reinterpret_cast<const double2 *>(bn + 4 * (int64_t)morton(K, J));
+                double2 a01 = __ldg(pa2), a23 = __ldg(pa2 + 1), b01 = __ldg(pb2), b23 = __ldg(pb2 + 1);
+                double pa[2][2] = {{a01.x, a01.y}, {a23.x, a23.y}};  // [di][dk]
+                double pb[2][2] = {{b01.x, b01.y}, {b23.x, b23.y}};  // [dk][dj]
+                uint32_t mm = 0;
 #pragma unroll
-                for (int dj = 0; dj < 2; dj++)
+                for (int di = 0; di < 2; di++) {
+                    if (!rows_meet(g, 2 * I + di, l + 1)) continue;
 #pragma unroll
-                    for (int dk = 0; dk < 2; dk++)
-                        if (keep(pa[di][dk], pb[dk][dj], T)) m |= 1u << (2 * ((di << 1) | dj) + dk);
+                    for (int dj = 0; dj < 2; dj++)
+#pragma unroll
+                        for (int dk = 0; dk < 2; dk++)
+                            if (keep(pa[di][dk], pb[dk][dj], T)) mm |= 1u << (2 * ((di << 1) | dj) + dk);
+                }
+                m[i] = mm;
+                c[i] = make_int4(__popc(mm & 3u), __popc((mm >> 2) & 3u), __popc((mm >> 4) & 3u),
+                                 __popc((mm >> 6) & 3u));
+                csum = vadd(csum, c[i]);
             }
-            c = make_int4(__popc(m & 3u), __popc((m >> 2) & 3u), __popc((m >> 4) & 3u),
-                          __popc((m >> 6) & 3u));
-            mask[t] = (uint8_t)m;
         }
         int4 tot;
-        int4 ex = block_excl_scan<int4, CT>(c, &tot, sw);
+        int4 ex = block_excl_scan<int4, CT>(csum, &tot, sw);
         if (threadIdx.x < 32) {
             int4 e = tile_lookback(st, tile, tot);
             if (threadIdx.x == 0) s_excl = e;
         }
         __syncthreads();
         int4 p = vadd(s_excl, ex);
-        if (t < n) pre[t] = p;
-        if (t == n - 1) {
-            int4 e = vadd(p, c);
-            pre[n] = e;
-            int total = e.x + e.y + e.z + e.w;
-            cnt[l + 1] = total;
-            if (total > g.cap) cnt[CNT_OVERFLOW] = 1;
+#pragma unroll
+        for (int i = 0; i < CI; i++) {
+            const int t = t0 + i;
+            if (t < n) {
+                pre[t] = p;
+                mask[t] = (uint8_t)m[i];
+            }
+            if (t == n - 1) {
+                int4 e = vadd(p, c[i]);
+                pre[n] = e;
+                int total = e.x + e.y + e.z + e.w;
+                cnt[l + 1] = total;
+                if (total > g.cap) cnt[CNT_OVERFLOW] = 1;
+            }
+            p = vadd(p, c[i]);
         }
         __syncthreads();
     }
@@ -265,27 +285,39 @@ __global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, in
     if (*(volatile int32_t *)&cnt[CNT_OVERFLOW]) return;
     const int n = clamp_n(cnt, L, cap);
     int tile;
-    while ((tile = next_tile(st.ticket, n, CT, &s_tile)) >= 0) {
-        int t = tile * CT + threadIdx.x;
-        int4 r = make_int4(0, 0, -1, 0);
-        if (t < n) r = rec[t];
-        V1 h{(t < n && r.z == t) ? 1 : 0};
+    while ((tile = next_tile(st.ticket, n, CT * CI, &s_tile)) >= 0) {
+        const int t0 = tile * (CT * CI) + threadIdx.x * CI;
+        int4 r[CI];
+        int hs = 0;
+#pragma unroll
+        for (int i = 0; i < CI; i++) {
+            const int t = t0 + i;
+            r[i] = make_int4(0, 0, -1, 0);
+            if (t < n) r[i] = rec[t];
+            hs += (t < n && r[i].z == t) ? 1 : 0;
+        }
         V1 tot;
-        V1 ex = block_excl_scan<V1, CT>(h, &tot, sw);
+        V1 ex = block_excl_scan<V1, CT>(V1{hs}, &tot, sw);
         if (threadIdx.x < 32) {
             int e = tile_lookback(st, tile, tot).x;
             if (threadIdx.x == 0) s_excl = e;
         }
         __syncthreads();
         int s = s_excl + ex.x;
-        if (h.x && s < cap_segs) {
-            seg_code[s] = r.x;
-            seg_start[s] = t;
-            seg_len[s] = r.w - r.z;
-        }
-        if (t == n - 1) {
-            cnt[CNT_NSEG] = s + h.x;
-            if (s + h.x > cap_segs) cnt[CNT_OVERFLOW] = 1;
+#pragma unroll
+        for (int i = 0; i < CI; i++) {
+            const int t = t0 + i;
+            const int h = (t < n && r[i].z == t) ? 1 : 0;
+            if (h && s < cap_segs) {
+                seg_code[s] = r[i].x;
+                seg_start[s] = t;
+                seg_len[s] = r[i].w - r[i].z;
+            }
+            if (t == n - 1) {
+                cnt[CNT_NSEG] = s + h;
+                if (s + h > cap_segs) cnt[CNT_OVERFLOW] = 1;
+            }
+            s += h;
         }
         __syncthreads();
     }
@@ -321,7 +353,7 @@ static spamm_status cull_alloc(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap
     cull_free(ctx, cw);
     cw->cap = cap;
     cw->cap_segs = cap_segs;
-    cw->tiles = cdiv(cap + 1, CT);
+    cw->tiles = cdiv(cap + 1, CT * CI);
     cw->rec[0] = dalloc<int4>(ctx, cap);
     cw->rec[1] = dalloc<int4>(ctx, cap);
     cw->pre = dalloc<int4>(ctx, cap + 1);

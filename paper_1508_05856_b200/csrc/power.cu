@@ -64,13 +64,22 @@ __global__ void k_row_fill(const int32_t *slot, int nb, const int32_t *rowptr, i
 // per row, RG = 256/TPR rows per CTA, b/RG CTAs per block row.  Each thread
 // accumulates its partial dot products over the row's blocks in order (U blocks
 // in flight), then the TPR threads of a row reduce with a fixed xor tree.
+// Persistent: CTAs take (block row, row group) units from a ticket, so the grid is
+// exactly the resident capacity (no partial last wave) and uneven rows balance.
 template <int B>
 __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t *rowptr,
                                               const int32_t *cols, const int32_t *slots,
-                                              const double *v, double *w)
+                                              const double *v, double *w, int32_t *ticket, int nunits)
 {
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
-    const int I = blockIdx.x / CPR, rg = blockIdx.x % CPR;
+    __shared__ int s_unit;
+    for (;;) {
+    if (threadIdx.x == 0) s_unit = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int unit = s_unit;
+    __syncthreads();
+    if (unit >= nunits) return;
+    const int I = unit / CPR, rg = unit % CPR;
     const int p0 = rowptr[I], p1 = rowptr[I + 1];
     const int r = rg * RG + threadIdx.x / TPR;
     const int e0 = r * B + (threadIdx.x % TPR) * E;   // physical offset inside a block
@@ -78,41 +87,54 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
 #pragma unroll
     for (int i = 0; i < E; i++) lc[i] = pool_col(e0 + i, B);
     double acc = 0.0;
-    constexpr int U = 4;  // blocks in flight per thread
-    for (int p = p0; p < p1; p += U) {
-        double x[U][E], vx[U][E];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (p + u < p1) {
-                const double *blk = pool + (int64_t)slots[p + u] * B * B + e0;
-                const double *vv = v + (int64_t)cols[p + u] * B;
-                if constexpr (E >= 2) {
-#pragma unroll
-                    for (int i = 0; i < E; i += 2) {
-                        double2 t = __ldg(reinterpret_cast<const double2 *>(blk + i));
-                        x[u][i] = t.x;
-                        x[u][i + 1] = t.y;
-                    }
-                } else {
-                    x[u][0] = __ldg(blk);
-                }
-#pragma unroll
-                for (int i = 0; i < E; i++) vx[u][i] = __ldg(vv + lc[i]);
-            }
+    constexpr int U = 4;      // blocks in flight per thread
+    constexpr int SPC = 512;  // block-row entries staged in shared memory per pass
+    __shared__ int s_slot[SPC], s_col[SPC];
+    for (int pc = p0; pc < p1; pc += SPC) {
+        const int pe = p1 < pc + SPC ? p1 : pc + SPC;
+        __syncthreads();
+        for (int i = threadIdx.x; i < pe - pc; i += 256) {
+            s_slot[i] = slots[pc + i];
+            s_col[i] = cols[pc + i];
         }
+        __syncthreads();
+        // one global round trip per U blocks: the slot / column indices come from smem
+        for (int p = pc; p < pe; p += U) {
+            double x[U][E], vx[U][E];
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (p + u < p1) {
-                double s = 0.0;
+            for (int u = 0; u < U; u++) {
+                if (p + u < pe) {
+                    const double *blk = pool + (int64_t)s_slot[p + u - pc] * B * B + e0;
+                    const double *vv = v + (int64_t)s_col[p + u - pc] * B;
+                    if constexpr (E >= 2) {
 #pragma unroll
-                for (int i = 0; i < E; i++) s = fma(x[u][i], vx[u][i], s);
-                acc += s;
+                        for (int i = 0; i < E; i += 2) {
+                            double2 t = __ldg(reinterpret_cast<const double2 *>(blk + i));
+                            x[u][i] = t.x;
+                            x[u][i + 1] = t.y;
+                        }
+                    } else {
+                        x[u][0] = __ldg(blk);
+                    }
+#pragma unroll
+                    for (int i = 0; i < E; i++) vx[u][i] = __ldg(vv + lc[i]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (p + u < pe) {
+                    double sdot = 0.0;
+#pragma unroll
+                    for (int i = 0; i < E; i++) sdot = fma(x[u][i], vx[u][i], sdot);
+                    acc += sdot;
+                }
             }
         }
     }
 #pragma unroll
     for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x % TPR) == 0) w[(int64_t)I * B + r] = acc;
+    }
 }
 
 // single CTA: nrm = sqrt(sum w^2) (fixed order); v = w / nrm
@@ -153,10 +175,18 @@ __global__ void k_dot(const double *a, const double *b, int64_t n, double *out)
 
 template <int B>
 static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
-                 const int32_t *slots, const double *v, double *w)
+                 const int32_t *slots, const double *v, double *w, int32_t *ticket)
 {
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
-    k_spmv<B><<<s->nb * CPR, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w);
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<B>, 256, 0);
+        if (occ < 1) occ = 1;
+    }
+    const int nunits = s->nb * CPR;
+    int grid = ctx->sm_count * occ;
+    if (grid > nunits) grid = nunits;
+    k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
     ctx->launches++;
 }
 
@@ -168,7 +198,10 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     int32_t *cnt = dalloc<int32_t>(ctx, nb), *rowptr = dalloc<int32_t>(ctx, nb + 1);
     int32_t *cols = dalloc<int32_t>(ctx, nblk), *slots = dalloc<int32_t>(ctx, nblk);
     double *v = dalloc<double>(ctx, n), *w = dalloc<double>(ctx, n), *c = dalloc<double>(ctx, 1);
-    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c) return set_err(ctx, SPAMM_ENOMEM, "power");
+    int32_t *tickets = dalloc<int32_t>(ctx, K + 1);   // one per SpMV launch
+    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets) return set_err(ctx, SPAMM_ENOMEM, "power");
+    CK(cudaMemsetAsync(tickets, 0, sizeof(int32_t) * (K + 1), ctx->stream));
+    int nmv = 0;
     cudaStream_t st = ctx->stream;
     k_row_count<<<nb, 256, 0, st>>>(s->slot, nb, cnt);
     k_row_scan<<<1, 1024, 0, st>>>(cnt, nb, rowptr);
@@ -178,10 +211,11 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     // row partition: local block rows of w = s v, then all ranks gather the full w
     // (each row is computed by one rank with the single-device kernel: bitwise G-invariant)
     auto mv = [&](const double *x, double *y) -> spamm_status {
+        int32_t *tk = tickets + nmv++;
         switch (s->b) {
-        case 16: spmv<16>(ctx, s, rowptr, cols, slots, x, y); break;
-        case 32: spmv<32>(ctx, s, rowptr, cols, slots, x, y); break;
-        default: spmv<64>(ctx, s, rowptr, cols, slots, x, y); break;
+        case 16: spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk); break;
+        case 32: spmv<32>(ctx, s, rowptr, cols, slots, x, y, tk); break;
+        default: spmv<64>(ctx, s, rowptr, cols, slots, x, y, tk); break;
         }
         return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
     };
@@ -204,5 +238,6 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     dev_free(ctx, v, sizeof(double) * n);
     dev_free(ctx, w, sizeof(double) * n);
     dev_free(ctx, c, sizeof(double));
+    dev_free(ctx, tickets, sizeof(int32_t) * (K + 1));
     return SPAMM_OK;
 }

@@ -425,51 +425,49 @@ extern "C" spamm_status spamm_build_tree_blocks(spamm_ctx ctx, int64_t n, int32_
     return st;
 }
 
-// ------------------------------------------------------------ recompute
-__global__ void k_leaf_norm2_pool(const double *pool, const int32_t *coord, int64_t nblk, int b,
-                                  double *leaf_n2)
-{
-    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (w >= nblk) return;
-    double s = warp_block_sumsq(pool + w * (int64_t)b * b, b, b, lane);
-    if (lane == 0) leaf_n2[coord[w]] = s;
-}
-
-spamm_status leaf_norms_from_pool(spamm_ctx ctx, spamm_mat m)
-{
-    if (m->nblk > 0) {
-        k_leaf_norm2_pool<<<cdiv(m->nblk * 32, 256), 256, 0, ctx->stream>>>(
-            m->pool, m->coord, m->nblk, m->b, m->norm2 + pyr_off(m->L));
-        CKL(ctx);
-    }
-    return SPAMM_OK;
-}
-
 // --------------------------------------------------------------- maps
 // op 0: y = x / c ; op 1: y = (x / c + mu delta) / (1 + mu) ; op 2: y = x * c ;
 // op 5: y = delta (identity).  Same pattern as src (plus the diagonal for 1/5).
-__global__ void k_map(const double *src, const int32_t *coord, int64_t nblk, int b, int op,
-                      double c, double mu, double *dst)
+// Vectorised map over one stored block per CTA (double2 in the pool layout) with
+// the block's squared norm fused in (thread partials in element order, then a
+// fixed warp-shuffle + warp-order tree: deterministic).  Same ops as k_map.
+__global__ void __launch_bounds__(256) k_map2(const double *src, const int32_t *coord, int b, int op, double c,
+                                              double mu, double *dst, double *leaf_n2)
 {
-    int64_t blk = blockIdx.x;
-    if (blk >= nblk) return;
-    uint32_t code = coord[blk];
-    bool diag = morton_i(code) == morton_j(code);
-    const double *s = src ? src + blk * (int64_t)b * b : nullptr;
-    double *d = dst + blk * (int64_t)b * b;
-    for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-        int r = e / b, q = pool_col(e, b);   // logical (row, column) of physical e
-        double x = s ? s[e] : 0.0;
-        double dl = (diag && r == q) ? 1.0 : 0.0;
-        double y;
+    __shared__ double red[8];
+    const int64_t blk = blockIdx.x;
+    const uint32_t code = coord[blk];
+    const bool diag = morton_i(code) == morton_j(code);
+    const int64_t base = blk * (int64_t)b * b;
+    const double2 *s2 = src ? reinterpret_cast<const double2 *>(src + base) : nullptr;
+    double2 *d2 = reinterpret_cast<double2 *>(dst + base);
+    const int half = b / 2, n2 = b * b / 2;
+    double ss = 0.0;
+    for (int p = threadIdx.x; p < n2; p += 256) {
+        const int r = p / half, ch = p % half;
+        const int q0 = (ch ^ swz(r)) << 1;            // logical column of the pair's first element
+        const double2 x = s2 ? s2[p] : make_double2(0.0, 0.0);
+        const double dl0 = (diag && r == q0) ? 1.0 : 0.0, dl1 = (diag && r == q0 + 1) ? 1.0 : 0.0;
+        double y0, y1;
         switch (op) {
-        case 0: y = x / c; break;
-        case 1: y = (x / c + mu * dl) / (1.0 + mu); break;
-        case 2: y = x * c; break;
-        default: y = dl; break;
+        case 0: y0 = x.x / c; y1 = x.y / c; break;
+        case 1: y0 = (x.x / c + mu * dl0) / (1.0 + mu); y1 = (x.y / c + mu * dl1) / (1.0 + mu); break;
+        case 2: y0 = x.x * c; y1 = x.y * c; break;
+        default: y0 = dl0; y1 = dl1; break;
         }
-        d[e] = y;
+        d2[p] = make_double2(y0, y1);
+        ss = fma(y0, y0, ss);
+        ss = fma(y1, y1, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) t += red[w];
+        leaf_n2[code] = t;
     }
 }
 
@@ -486,28 +484,23 @@ spamm_status mat_map(spamm_ctx ctx, spamm_mat src, int op, double c, double mu, 
                                cudaMemcpyDeviceToDevice, ctx->stream));
             CK(cudaMemcpyAsync(m->coord, src->coord, sizeof(int32_t) * src->nblk,
                                cudaMemcpyDeviceToDevice, ctx->stream));
-            k_map<<<(int)src->nblk, 256, 0, ctx->stream>>>(src->pool, src->coord, src->nblk, src->b,
-                                                          op, c, mu, m->pool);
+            CK(cudaMemsetAsync(m->norm2, 0, sizeof(double) * pyr_size(m->L), ctx->stream));
+            k_map2<<<(int)src->nblk, 256, 0, ctx->stream>>>(src->pool, src->coord, src->b, op, c, mu, m->pool,
+                                                           m->norm2 + pyr_off(m->L));
             CKL(ctx);
         } else {
             CK(cudaMemsetAsync(m->slot, 0xFF, sizeof(int32_t) * (size_t)src->nb * src->nb, ctx->stream));
+            CK(cudaMemsetAsync(m->norm2, 0, sizeof(double) * pyr_size(m->L), ctx->stream));
         }
         m->nblk = src->nblk;
         if (fill) {
             // absent diagonal blocks: x = 0 => op 1 gives mu/(1+mu) I, op 5 gives I
             double dv = (op == 5) ? 1.0 : (0.0 / c + mu * 1.0) / (1.0 + mu);
-            CK(cudaMemsetAsync(m->norm2, 0, sizeof(double) * pyr_size(m->L), ctx->stream));
-            st = leaf_norms_from_pool(ctx, m);
-            if (st) break;
             int64_t h = 0;
             st = diag_append(ctx, m, m->nblk, dv, &h);
             if (st) break;
             m->nblk += h;
-        } else {
-            CK(cudaMemsetAsync(m->norm2, 0, sizeof(double) * pyr_size(m->L), ctx->stream));
-            st = leaf_norms_from_pool(ctx, m);
         }
-        if (st) break;
         st = norms_finish(ctx, m);
     } while (0);
     if (st) {
