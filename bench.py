@@ -49,6 +49,12 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--map", default="plain", choices=["plain", "scaled"],
+                    help="NS map: plain 1/2(3I-X) (north_star) or the paper's scaled/stabilised h_alpha")
+    ap.add_argument("--channel", default="dual", choices=["dual", "single"],
+                    help="dual (north_star, P:383-389) or single-channel (P:398-402) iteration")
+    ap.add_argument("--tau-s-factor", type=float, default=None, help="override tau_s / tau")
+    ap.add_argument("--t-stop", type=float, default=None, help="override the convergence exit |t_k| <= t_stop")
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced"],
                     help="row partition for --gpus > 1 (balanced: on s (x) s per-row task counts)")
     ap.add_argument("--dist-world1", action="store_true",
@@ -204,8 +210,9 @@ def run_ours(args):
     cfg = si.CONFIGS[args.config]
     tau = args.tau if args.tau is not None else cfg.tau
     iters = args.iters if args.iters is not None else cfg.iters
-    tau_s = tau * cfg.tau_s_factor
-    t_stop = cfg.t_stop
+    tau_s = tau * (args.tau_s_factor if args.tau_s_factor is not None else cfg.tau_s_factor)
+    t_stop = args.t_stop if args.t_stop is not None else cfg.t_stop
+    scaled = args.map == "scaled"
     nb = cfg.n // cfg.b
 
     # ---- row partition over the ranks; fixed for the run
@@ -250,7 +257,10 @@ def run_ours(args):
 
     def step(inp, readback):
         S = build(inp)
-        r = sp.spamm_ns_sqrt(ctx, S, tau, iters, tau_s=tau_s, mu=cfg.mu, t_stop=t_stop)
+        if args.channel == "single":
+            r = sp.spamm_ns_sqrt_single(ctx, S, tau, iters, tau_s=tau_s, t_stop=t_stop, scaled=scaled)
+        else:
+            r = sp.spamm_ns_sqrt(ctx, S, tau, iters, tau_s=tau_s, mu=cfg.mu, t_stop=t_stop, scaled=scaled)
         S.free()
         flops = sum(p["flops"] for k in r["stats"] for p in k)
         tasks = sum(p["tasks"] for k in r["stats"] for p in k)
@@ -378,7 +388,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
                 "workload": workload_name(cfg, tau, iters), "n": cfg.n, "leaf": cfg.b, "tau": tau,
-                "tau_s": tau_s, "iters": iters, "t_stop": t_stop,
+                "tau_s": tau_s, "iters": iters, "t_stop": t_stop, "map": args.map, "channel": args.channel,
                 "parallelism": (f"row-partitioned over {ws} GPUs ({args.partition} split), NCCL halo "
                                 "exchange + norm all-gather") if comm is not None else "single",
                 "l2": f"inputs larger than L2 (s ~ {blocks_mb:.0f} MB of blocks, iterates > 126 MB)",

@@ -185,6 +185,12 @@ spamm_status spamm_get_blocks(spamm_ctx ctx, spamm_mat m, int64_t nreq, const in
  * Errors: ESHAPE (n or b differ), EINVAL (tau < 0 or not finite). */
 spamm_status spamm_multiply(spamm_ctx ctx, spamm_mat A, spamm_mat B, double tau, spamm_mat *C,
                             spamm_stats *stats /* nullable, host */);
+/* C = A^T (x)_tau B: the SpAMM product of the transposed left operand (node (I,K) of
+ * A^T is node (K,I) of A; ||a^T|| = ||a||, so A's norms serve as they are).  Needed by
+ * the single-channel iteration.  Errors as
+ * spamm_multiply, plus EINVAL on a row-partitioned context (A^T's rows are not local). */
+spamm_status spamm_multiply_t(spamm_ctx ctx, spamm_mat A, spamm_mat B, double tau, spamm_mat *C,
+                              spamm_stats *stats /* nullable, host */);
 /* Leaf triples (i,k,j) of the last product on ctx, grouped by output block (i,j)
  * in Morton order, k ascending; ikj is HOST [3*cap]; *n = total count. */
 spamm_status spamm_export_tasks(spamm_ctx ctx, int32_t *ikj, int64_t cap, int64_t *n);
@@ -206,6 +212,20 @@ spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, 
 spamm_status spamm_ns_step_map(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
                                int32_t map, spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
                                double *t_k, spamm_stats stats[3], double *alpha_eps);
+/* Single-channel square-root iteration (Eq. single; the sensitive product
+ * rightmost), one step from (Z_k, H_k = h[X_k]) with s' = s/c:
+ *   Z_{k+1} = Z_k (x)_tau H_k,  W = s' (x)_tau_s Z_{k+1},  H_{k+1} = h[Z_{k+1}^T (x)_tau W],
+ * t_next = (n - tr X_{k+1})/n; map as in spamm_ns_step_map.  W_out nullable.
+ * stats[3] = (Z H, s' Z, Z^T W).  Not available on a row-partitioned context. */
+spamm_status spamm_ns_step_single(spamm_ctx ctx, spamm_mat S1, spamm_mat Z, spamm_mat H, double tau,
+                                  double tau_s, int32_t map, spamm_mat *Z_next, spamm_mat *H_next,
+                                  spamm_mat *W_out, double *t_next, spamm_stats stats[3],
+                                  double *alpha_eps);
+/* Full single-channel run: c (power iteration or opts->scale), Z_0 = I, X_0 = s/c,
+ * iters steps (opts: tau_s, map, t_stop, histories as spamm_ns_sqrt; mu must be 0),
+ * outputs Z * c^{-1/2} -> s^{-1/2} and Y = W c^{1/2} -> s^{1/2}. */
+spamm_status spamm_ns_sqrt_single(spamm_ctx ctx, spamm_mat s, double tau, int32_t iters, spamm_mat *Y,
+                                  spamm_mat *Z, const spamm_ns_opts *opts);
 /* Scale estimate c ~ ||s||_2: K power steps from 1/sqrt(n) * ones, Rayleigh quotient. */
 spamm_status spamm_power_scale(spamm_ctx ctx, spamm_mat s, int32_t K, double *c);
 /* Y0 = s/c (mu = 0) or (s/c + mu I)/(1+mu). */

@@ -62,6 +62,10 @@ def lib():
             "or_block_coords": (i64, [vp, vp, vp, i64]),
             "or_multiply": (vp, [vp, vp, dbl, vp, i64, P(i64)]),
             "or_copy": (vp, [vp]),
+            "or_transpose": (vp, [vp]),
+            "or_multiply_t": (vp, [vp, vp, dbl, vp, i64, P(i64)]),
+            "or_ns_sqrt_single": (i32, [vp, dbl, dbl, i32, dbl, i32, dbl, i32, P(vp), P(vp), vp, vp,
+                                        P(dbl), P(C.c_int)]),
             "or_identity": (vp, [i32, i32]),
             "or_scale": (vp, [vp, dbl, i32]),
             "or_trace": (dbl, [vp]),
@@ -171,17 +175,18 @@ class OMat:
         return OMat(lib().or_copy(self.h))
 
 
-def multiply(A: OMat, B: OMat, tau: float, want_tasks: bool = False):
-    """C = A (x)_tau B (Eq. newspamm).  Returns C or (C, tasks[ntasks,3] = (i,k,j)
-    sorted lexicographically)."""
+def multiply(A: OMat, B: OMat, tau: float, want_tasks: bool = False, trans_a: bool = False):
+    """C = A (x)_tau B (Eq. newspamm), or A^T (x)_tau B with trans_a.  Returns C or
+    (C, tasks[ntasks,3] = (i,k,j) sorted lexicographically)."""
     n = C.c_int64(0)
+    fn = lib().or_multiply_t if trans_a else lib().or_multiply
     if not want_tasks:
-        h = lib().or_multiply(A.h, B.h, float(tau), None, 0, C.byref(n))
+        h = fn(A.h, B.h, float(tau), None, 0, C.byref(n))
         return OMat(h)
     cap = 1 << 16
     while True:
         buf = np.empty(3 * cap, dtype=np.int32)
-        h = lib().or_multiply(A.h, B.h, float(tau), _ptr(buf), cap, C.byref(n))
+        h = fn(A.h, B.h, float(tau), _ptr(buf), cap, C.byref(n))
         if n.value <= cap:
             t = buf[: 3 * n.value].reshape(-1, 3)
             t = t[np.lexsort((t[:, 1], t[:, 2], t[:, 0]))]   # sort by (i, j, k)
@@ -242,3 +247,25 @@ def alpha(t: float) -> float:
 def eps(t: float) -> float:
     """Stabilisation sigmoid eps(t) of P:446-448."""
     return lib().or_eps(float(t))
+
+
+def transpose(A: OMat) -> OMat:
+    """A^T with the node norms carried over (||a^T|| = ||a||)."""
+    return OMat(lib().or_transpose(A.h))
+
+
+def ns_sqrt_single(s: OMat, tau: float, iters: int, tau_s: float | None = None, scale: float = 0.0,
+                   power_iters: int = 100, t_stop: float = 0.0, scaled: bool = False):
+    """Single-channel run: Z <- Z (x) h[X], W = s (x)_tau_s Z, X <- Z^T (x) W.
+    Returns dict(Y = W sqrt(c), Z, t, counts[k] = (ZH, sZ, Z^T W), c, rc, iters)."""
+    tau_s = tau if tau_s is None else tau_s
+    yo, zo = C.c_void_p(), C.c_void_p()
+    t = np.zeros(iters)
+    counts = np.zeros(3 * iters, dtype=np.int64)
+    c = C.c_double(0)
+    done = C.c_int(0)
+    rc = lib().or_ns_sqrt_single(s.h, tau, tau_s, iters, scale, power_iters, t_stop, int(scaled), C.byref(yo),
+                                 C.byref(zo), _ptr(t), _ptr(counts), C.byref(c), C.byref(done))
+    k = done.value if rc == 0 else done.value + 1
+    return dict(Y=OMat(yo.value), Z=OMat(zo.value), t=t[:k], counts=counts.reshape(iters, 3)[:k],
+                c=c.value, rc=rc, iters=k)

@@ -405,6 +405,45 @@ static onode *copy_node(const onode *p, int lev, int L, int b)
     return q;
 }
 
+/* Transpose: children 01 <-> 10, leaves transposed; every node keeps its norm
+ * (the Frobenius norm is transpose-invariant: ||a^T|| = ||a||, so a^T's
+ * decorations are a's, bitwise). */
+static onode *transpose_node(const onode *p, int lev, int L, int b)
+{
+    if (!p) return NULL;
+    if (lev == L) {
+        onode *q = new_leaf(b);
+        for (int r = 0; r < b; r++)
+            for (int c = 0; c < b; c++) q->blk[(size_t)c * b + r] = p->blk[(size_t)r * b + c];
+        q->norm = p->norm;
+        return q;
+    }
+    onode *q = new_interior();
+    q->ch[0] = transpose_node(p->ch[0], lev + 1, L, b);
+    q->ch[1] = transpose_node(p->ch[2], lev + 1, L, b);
+    q->ch[2] = transpose_node(p->ch[1], lev + 1, L, b);
+    q->ch[3] = transpose_node(p->ch[3], lev + 1, L, b);
+    q->norm = p->norm;
+    return q;
+}
+
+omat *or_transpose(const omat *m)
+{
+    omat *c = (omat *)calloc(1, sizeof(omat));
+    *c = *m;
+    c->root = transpose_node(m->root, 0, m->L, m->b);
+    return c;
+}
+
+/* A^T (x)_tau B: the SpAMM product (Eq. newspamm) of the transposed quadtree. */
+omat *or_multiply_t(const omat *A, const omat *B, double tau, int32_t *tasks, int64_t cap, int64_t *ntasks)
+{
+    omat *At = or_transpose(A);
+    omat *C = or_multiply(At, B, tau, tasks, cap, ntasks);
+    or_free(At);
+    return C;
+}
+
 omat *or_copy(const omat *m)
 {
     omat *c = (omat *)calloc(1, sizeof(omat));
@@ -620,4 +659,52 @@ int or_num_threads(void)
 #else
     return 1;
 #endif
+}
+
+/* ------------------------------------------------- single channel
+ * z_k <- z_{k-1} . h[x_{k-1}],  x_k <- z_k^T . s . z_k, with SpAMM products and the
+ * sensitive product rightmost:
+ *   Z_{k+1} = Z_k (x)_tau H_k,  W = s (x)_tau_s Z_{k+1},  X_{k+1} = Z_{k+1}^T (x)_tau W,
+ * t_k = (n - tr X_k)/n, H_k = h(X_k) (map 0: 1/2 (3I - X); map 1: scaled/stabilised).
+ * Start Z_0 = I, X_0 = s/c (= Z_0^T s Z_0; reading L11 analogue: s/c is exact here).
+ * Output Z -> (s/c)^{-1/2} / sqrt(c) = s^{-1/2};  Y = W * sqrt(c) -> s^{1/2}.
+ * counts [3*iters]: tasks of (Z H, s Z, Z^T W). */
+int or_ns_sqrt_single(const omat *s, double tau, double tau_s, int iters, double scale, int power_iters,
+                      double t_stop, int map, omat **Yout, omat **Zout, double *t_hist, int64_t *counts,
+                      double *c_used, int *iters_done)
+{
+    double c = scale > 0.0 ? scale : or_power_scale(s, power_iters);
+    if (c_used) *c_used = c;
+    omat *S1 = or_ns_y0(s, c, 0.0);
+    omat *Z = or_identity(s->n, s->b);
+    omat *X = or_copy(S1);
+    omat *W = or_copy(S1);
+    int rc = 0;
+    if (iters_done) *iters_done = 0;
+    for (int k = 0; k < iters; k++) {
+        double tr = or_trace(X);
+        double t = ((double)X->n - tr) / (double)X->n;
+        if (t_hist) t_hist[k] = t;
+        omat *H = map ? map_mat(X, 6, or_alpha(t), or_eps(t)) : map_mat(X, 4, 0.0, 0.0);
+        int64_t c0 = 0, c1 = 0, c2 = 0;
+        omat *Zn = or_multiply(Z, H, tau, NULL, 0, &c0);
+        omat *Wn = or_multiply(S1, Zn, tau_s, NULL, 0, &c1);
+        omat *Xn = or_multiply_t(Zn, Wn, tau, NULL, 0, &c2);
+        if (counts) { counts[3 * k] = c0; counts[3 * k + 1] = c1; counts[3 * k + 2] = c2; }
+        or_free(H);
+        if (!isfinite(t) || !isfinite(or_norm(Zn)) || !isfinite(or_norm(Xn))) {
+            or_free(Zn); or_free(Wn); or_free(Xn);
+            rc = -1;
+            break;
+        }
+        or_free(Z); or_free(W); or_free(X);
+        Z = Zn; W = Wn; X = Xn;
+        if (iters_done) *iters_done = k + 1;
+        if (t_stop > 0.0 && fabs(t) <= t_stop) break;
+    }
+    double f = sqrt(c);
+    *Yout = map_mat(W, 2, f, 0.0);
+    *Zout = map_mat(Z, 0, f, 0.0);
+    or_free(Z); or_free(W); or_free(X); or_free(S1);
+    return rc;
 }

@@ -26,7 +26,7 @@ __all__ = [
     "spamm_ctx_create", "spamm_ctx_destroy", "spamm_last_error", "spamm_kernel_launches",
     "spamm_build_tree", "spamm_build_tree_blocks", "spamm_mat_free", "spamm_mat_info",
     "spamm_norm", "spamm_to_dense", "spamm_level_norms2", "spamm_get_blocks",
-    "spamm_multiply", "spamm_export_tasks", "spamm_ns_step", "spamm_ns_step_map", "spamm_power_scale",
+    "spamm_multiply", "spamm_multiply_t", "spamm_ns_step_single", "spamm_ns_sqrt_single", "spamm_export_tasks", "spamm_ns_step", "spamm_ns_step_map", "spamm_power_scale",
     "spamm_ns_y0", "spamm_identity", "spamm_ns_sqrt", "spamm_scale",
     "spamm_export_blocks", "spamm_profile_enable", "spamm_profile_read", "spamm_peak_dmma",
     "Comm", "spamm_comm_nccl_unique_id", "spamm_comm_nccl_create", "spamm_comm_local_group",
@@ -106,6 +106,9 @@ def load():
         "spamm_get_blocks": (i32, [vp, vp, i64, vp, vp, vp, vp]),
         "spamm_multiply": (i32, [vp, vp, vp, dbl, P(vp), P(spamm_stats)]),
         "spamm_export_tasks": (i32, [vp, vp, i64, P(i64)]),
+        "spamm_multiply_t": (i32, [vp, vp, vp, dbl, P(vp), P(spamm_stats)]),
+        "spamm_ns_step_single": (i32, [vp, vp, vp, vp, dbl, dbl, i32, P(vp), P(vp), P(vp), P(dbl), vp, vp]),
+        "spamm_ns_sqrt_single": (i32, [vp, vp, dbl, i32, P(vp), P(vp), P(spamm_ns_opts)]),
         "spamm_ns_step": (i32, [vp, vp, vp, dbl, dbl, P(vp), P(vp), P(vp), P(dbl), vp]),
         "spamm_ns_step_map": (i32, [vp, vp, vp, dbl, dbl, i32, P(vp), P(vp), P(vp), P(dbl), vp, vp]),
         "spamm_power_scale": (i32, [vp, vp, i32, P(dbl)]),
@@ -418,6 +421,49 @@ def spamm_multiply(ctx: Ctx, A: Mat, B: Mat, tau: float, want_stats: bool = Fals
     ctx.check(load().spamm_multiply(ctx.h, A.h, B.h, float(tau), C.byref(h), C.byref(st)))
     m = Mat(ctx, h)
     return (m, st.as_dict()) if want_stats else m
+
+
+def spamm_multiply_t(ctx: Ctx, A: Mat, B: Mat, tau: float, want_stats: bool = False):
+    """C = A^T (x)_tau B."""
+    h = C.c_void_p()
+    st = spamm_stats()
+    ctx.check(load().spamm_multiply_t(ctx.h, A.h, B.h, float(tau), C.byref(h), C.byref(st)))
+    m = Mat(ctx, h)
+    return (m, st.as_dict()) if want_stats else m
+
+
+def spamm_ns_step_single(ctx: Ctx, S1: Mat, Z: Mat, H: Mat, tau: float, tau_s: float | None = None,
+                         scaled: bool = False, want_w: bool = False):
+    """One single-channel step; returns (Z', H', t', stats[3], (alpha, eps) [, W])."""
+    tau_s = tau if tau_s is None else tau_s
+    zn, hn, wn = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    t = C.c_double()
+    ae = (C.c_double * 2)()
+    sts = (spamm_stats * 3)()
+    ctx.check(load().spamm_ns_step_single(ctx.h, S1.h, Z.h, H.h, float(tau), float(tau_s), int(scaled),
+                                          C.byref(zn), C.byref(hn), C.byref(wn) if want_w else None,
+                                          C.byref(t), sts, ae))
+    out = (Mat(ctx, zn), Mat(ctx, hn), t.value, [s.as_dict() for s in sts], (ae[0], ae[1]))
+    return out + (Mat(ctx, wn),) if want_w else out
+
+
+def spamm_ns_sqrt_single(ctx: Ctx, s: Mat, tau: float, iters: int, tau_s: float | None = None,
+                         scale: float = 0.0, power_iters: int = 100, t_stop: float = 0.0,
+                         scaled: bool = False):
+    """Full single-channel run: returns dict(Y, Z, t, stats, c, iters)."""
+    t = np.zeros(iters)
+    sts = (spamm_stats * (3 * iters))()
+    c = C.c_double()
+    done = C.c_int32(0)
+    o = spamm_ns_opts(-1.0 if tau_s is None else float(tau_s), 0.0, float(scale), int(power_iters),
+                      t.ctypes.data, C.cast(sts, C.c_void_p), C.cast(C.pointer(c), C.c_void_p), float(t_stop),
+                      C.cast(C.pointer(done), C.c_void_p), int(scaled))
+    yo, zo = C.c_void_p(), C.c_void_p()
+    ctx.check(load().spamm_ns_sqrt_single(ctx.h, s.h, float(tau), int(iters), C.byref(yo), C.byref(zo),
+                                          C.byref(o)))
+    k = done.value
+    stats = [[sts[3 * j + p].as_dict() for p in range(3)] for j in range(k)]
+    return dict(Y=Mat(ctx, yo), Z=Mat(ctx, zo), t=t[:k], stats=stats, c=c.value, iters=k)
 
 
 def spamm_export_tasks(ctx: Ctx) -> np.ndarray:

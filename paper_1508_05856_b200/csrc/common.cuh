@@ -223,7 +223,8 @@ struct Cull {
 };
 // Enqueue the query, synchronise once to read the counts, and grow + re-run
 // on capacity overflow.
-spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1);
+spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
+                      int transA = 0);
 void cull_free(spamm_ctx ctx, Cull *cw);
 spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj_host, int64_t cap, int64_t *n);
 
@@ -233,7 +234,7 @@ enum { EPI_STORE = 0, EPI_NS_H = 1, EPI_NS_X = 2 };
 // ticket = which of the GEMM ticket counters (zeroed by the cull) the launch uses
 spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
                       spamm_mat C, int epi, double *trace_part, const int32_t *seg_order = nullptr,
-                      int64_t nseg = -1, int ticket = 0);
+                      int64_t nseg = -1, int ticket = 0, int transA = 0);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
 // out[0..n) = the segments of `in` (nullable => 0..n-1), longest first (a schedule only)
 spamm_status lpt_order(spamm_ctx ctx, const int32_t *seg_len, const int32_t *in, int64_t n, int32_t *out);

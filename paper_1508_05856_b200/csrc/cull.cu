@@ -31,7 +31,15 @@ struct CullArgs {
     double tau;
     int64_t cap;
     int L, r0, r1;               // leaf level; output block rows [r0, r1) (row partition, §8(e))
+    int transA;                  // 1: the left operand is A^T (single channel, §8(f) f2):
+                                 //    node (I,K) of A^T is node (K,I) of A, norms shared
 };
+
+// Morton code of node (I, K) of the left operand in A's own pyramid / slot map
+__device__ __forceinline__ uint32_t a_code(const CullArgs &g, int I, int K)
+{
+    return g.transA ? morton(K, I) : morton(I, K);
+}
 
 // level-`lev` row index I covers leaf rows [I << (L-lev), (I+1) << (L-lev)); keep the
 // sub-volume only if that range meets the local output rows
@@ -79,7 +87,7 @@ __global__ void __launch_bounds__(1024) k_cull_init(CullArgs g, int l0, int4 *re
             uint32_t code = idx / S;
             int K = idx % S;
             int I = morton_i(code), J = morton_j(code);
-            f[e] = rows_meet(g, I, l0) && keep(an[morton(I, K)], bn[morton(K, J)], T);
+            f[e] = rows_meet(g, I, l0) && keep(an[a_code(g, I, K)], bn[morton(K, J)], T);
         }
         mycount += f[e];
     }
@@ -156,10 +164,15 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
                 int4 r = rec[t];
                 uint32_t code = r.x;
                 int K = r.y, I = morton_i(code), J = morton_j(code);
-                const double2 *pa2 = reinterpret_cast<const double2 *>(an + 4 * (int64_t)morton(I, K));
+                const double2 *pa2 = reinterpret_cast<const double2 *>(an + 4 * (int64_t)a_code(g, I, K));
                 const double2 *pb2 = reinterpret_cast<const double2 *>(bn + 4 * (int64_t)morton(K, J));
                 double2 a01 = __ldg(pa2), a23 = __ldg(pa2 + 1), b01 = __ldg(pb2), b23 = __ldg(pb2 + 1);
-                double pa[2][2] = {{a01.x, a01.y}, {a23.x, a23.y}};  // [di][dk]
+                // [di][dk]; for A^T the stored child (dk, di) of node (K, I)
+                double pa[2][2] = {{a01.x, a01.y}, {a23.x, a23.y}};
+                if (g.transA) {
+                    pa[0][1] = a23.x;
+                    pa[1][0] = a01.y;
+                }
                 double pb[2][2] = {{b01.x, b01.y}, {b23.x, b23.y}};  // [dk][dj]
                 uint32_t mm = 0;
 #pragma unroll
@@ -245,7 +258,7 @@ __global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const i
                             rec_out[pos] = make_int4((int)ccode, ck, gs, ge);
                             if (FINAL) {
                                 int i = 2 * I + (q >> 1), j = 2 * J + (q & 1);
-                                tA[pos] = g.a_slot[morton(i, ck)];
+                                tA[pos] = g.a_slot[a_code(g, i, ck)];
                                 tB[pos] = g.b_slot[morton(ck, j)];
                                 tK[pos] = ck;
                             }
@@ -268,7 +281,7 @@ __global__ void k_cull_leaf_direct(CullArgs g, int l, const int4 *rec, int32_t *
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         int4 r = rec[t];
         int i = morton_i(r.x), j = morton_j(r.x), k = r.y;
-        tA[t] = g.a_slot[morton(i, k)];
+        tA[t] = g.a_slot[a_code(g, i, k)];
         tB[t] = g.b_slot[morton(k, j)];
         tK[t] = k;
     }
@@ -380,14 +393,14 @@ static spamm_status cull_alloc(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap
 
 // Enqueue the whole query (no host sync).
 static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0,
-                                 int r1)
+                                 int r1, int transA)
 {
     const int L = A->L;
     const int l0 = L < 4 ? L : 4;
     cw->L = L;
     cw->l0 = l0;
     cw->b = A->b;
-    CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap, L, r0, r1};
+    CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap, L, r0, r1, transA};
     cudaStream_t s = ctx->stream;
     CK(cudaMemsetAsync(cw->counters, 0, sizeof(int32_t) * 64, s));
     CK(cudaMemsetAsync(cw->tile_flag, 0, sizeof(int32_t) * (SPAMM_MAX_L + 2) * cw->tiles, s));
@@ -428,7 +441,7 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     return SPAMM_OK;
 }
 
-spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1)
+spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1, int transA)
 {
     int64_t nb = A->nb;
     int64_t want = cw->hint > 0 ? cw->hint : (int64_t)1 << 16;
@@ -437,7 +450,7 @@ spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double 
         ST(cull_alloc(ctx, cw, cap, nb * nb));
     }
     for (int attempt = 0; attempt < 8; attempt++) {
-        ST(cull_enqueue(ctx, cw, A, B, tau, r0, r1));
+        ST(cull_enqueue(ctx, cw, A, B, tau, r0, r1, transA));
         CK(cudaMemcpyAsync(cw->hcnt, cw->counters, sizeof(int32_t) * 64, cudaMemcpyDeviceToHost,
                            ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));

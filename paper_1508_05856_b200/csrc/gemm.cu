@@ -90,7 +90,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 //     issue DMMAs into register accumulators, release the stage; at the end
 //     of a segment run the fused epilogue.  The producer runs ahead across
 //     segment boundaries, so the next segment's tiles load during an epilogue.
-template <int B, int CW, int WM, int WN, int STAGES, int EPI>
+// TA = 1: the left operand is A^T (single channel, §8(f) f2): the A tile is read
+// with the column pattern of the B fragments (A^T[m][k] = A[k][m]).
+template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
 __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
 {
     static_assert(WM * WN == CW, "warp grid");
@@ -184,12 +186,19 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
     const int g8 = lane >> 2, t4 = lane & 3;
     const int m0 = (warp / WN) * TM, n0 = (warp % WN) * TN;
     // per-thread fragment offsets (doubles) inside a tile; see pool_at / swz
-    int aoff[MF][2];
+    int aoff[MF][TA ? 4 : 2];
 #pragma unroll
     for (int mf = 0; mf < MF; mf++) {
-        const int r = m0 + 8 * mf + g8;
+        if constexpr (TA) {
+            const int col = m0 + 8 * mf + g8;   // A^T row = A column
 #pragma unroll
-        for (int h = 0; h < 2; h++) aoff[mf][h] = r * B + (((2 * t4 + h) ^ swz(r)) << 1);
+            for (int s = 0; s < 4; s++)
+                aoff[mf][s] = (4 * t4 + s) * B + ((((col >> 1) ^ ((t4 << 1) | (s & 1)))) << 1) + (col & 1);
+        } else {
+            const int r = m0 + 8 * mf + g8;
+#pragma unroll
+            for (int h = 0; h < 2; h++) aoff[mf][h] = r * B + (((2 * t4 + h) ^ swz(r)) << 1);
+        }
     }
     int boff[NF][4];
 #pragma unroll
@@ -231,9 +240,14 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
                 double a[MF][4], bf[NF][4];
 #pragma unroll
                 for (int mf = 0; mf < MF; mf++) {
-                    const double2 v0 = *reinterpret_cast<const double2 *>(As + aoff[mf][0] + 16 * kc);
-                    const double2 v1 = *reinterpret_cast<const double2 *>(As + aoff[mf][1] + 16 * kc);
-                    a[mf][0] = v0.x; a[mf][1] = v0.y; a[mf][2] = v1.x; a[mf][3] = v1.y;
+                    if constexpr (TA) {
+#pragma unroll
+                        for (int s = 0; s < 4; s++) a[mf][s] = As[aoff[mf][s] + 16 * kc * B];
+                    } else {
+                        const double2 v0 = *reinterpret_cast<const double2 *>(As + aoff[mf][0] + 16 * kc);
+                        const double2 v1 = *reinterpret_cast<const double2 *>(As + aoff[mf][1] + 16 * kc);
+                        a[mf][0] = v0.x; a[mf][1] = v0.y; a[mf][2] = v1.x; a[mf][3] = v1.y;
+                    }
                 }
 #pragma unroll
                 for (int nf = 0; nf < NF; nf++)
@@ -317,7 +331,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
     }
 }
 
-template <int B, int CW, int WM, int WN, int STAGES, int EPI>
+template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
 static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
 {
     constexpr int NT = 32 * (CW + 1);
@@ -325,7 +339,7 @@ static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
     const size_t smem = sizeof(double) * 2 * STAGES * B * B + 2 * STAGES * sizeof(uint64_t) +
                         2 * QN * sizeof(uint64_t) + QN * sizeof(int4) + RS * 2 * CW * sizeof(double) +
                         RS * sizeof(int);
-    auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI>;
+    auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI, TA>;
     static int occ = 0;
     if (!occ) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -340,28 +354,33 @@ static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
     return SPAMM_OK;
 }
 
-template <int EPI>
+template <int EPI, int TA>
 static spamm_status gemm_dispatch(spamm_ctx ctx, int b, const GemmArgs &g)
 {
     switch (b) {
-    case 64: return launch_gemm<64, 8, 2, 4, 3, EPI>(ctx, g);
-    case 32: return launch_gemm<32, 4, 2, 2, 4, EPI>(ctx, g);
-    case 16: return launch_gemm<16, 1, 1, 1, 4, EPI>(ctx, g);
+    case 64: return launch_gemm<64, 8, 2, 4, 3, EPI, TA>(ctx, g);
+    case 32: return launch_gemm<32, 4, 2, 2, 4, EPI, TA>(ctx, g);
+    case 16: return launch_gemm<16, 1, 1, 1, 4, EPI, TA>(ctx, g);
     default: return set_err(ctx, SPAMM_EINVAL, "b=%d", b);
     }
 }
 
 spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
                       spamm_mat C, int epi, double *trace_part, const int32_t *seg_order, int64_t nseg,
-                      int ticket)
+                      int ticket, int transA)
 {
     if (nseg < 0) nseg = cw->nsegs;
     GemmArgs g{A->pool, B->pool, b_halo, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
                (int)nseg, seg_order, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
                cw->counters + CNT_GEMM_TICKET + ticket};
-    if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H>(ctx, A->b, g);
-    if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X>(ctx, A->b, g);
-    return gemm_dispatch<EPI_STORE>(ctx, A->b, g);
+    if (transA) {
+        if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 1>(ctx, A->b, g);
+        if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 1>(ctx, A->b, g);
+        return gemm_dispatch<EPI_STORE, 1>(ctx, A->b, g);
+    }
+    if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 0>(ctx, A->b, g);
+    if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 0>(ctx, A->b, g);
+    return gemm_dispatch<EPI_STORE, 0>(ctx, A->b, g);
 }
 
 // ------------------------------------------------------- LPT segment order

@@ -149,13 +149,13 @@ static void *snapshot(spamm_ctx ctx, const void *src, int64_t bytes)
 
 static int64_t g_product_id = 0;
 
-static void selfcheck_cull(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau)
+static void selfcheck_cull(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int transA)
 {
     const int64_t nt = cw->ntasks, ns = cw->nsegs;
     void *tA = snapshot(ctx, cw->tA, 4 * nt), *tB = snapshot(ctx, cw->tB, 4 * nt);
     void *sc = snapshot(ctx, cw->seg_code, 4 * ns), *ss = snapshot(ctx, cw->seg_start, 4 * ns),
          *sl = snapshot(ctx, cw->seg_len, 4 * ns);
-    cull_run(ctx, cw, A, B, tau, A->r0, A->r1);
+    cull_run(ctx, cw, A, B, tau, A->r0, A->r1, transA);
     long long f[5], m[5];
     m[0] = cw->ntasks == nt && cw->nsegs == ns ? 0 : -1;
     if (!m[0]) {
@@ -175,7 +175,7 @@ static void selfcheck_cull(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, do
 }
 
 static void selfcheck_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *halo, spamm_mat C,
-                           int epi)
+                           int epi, int transA = 0)
 {
     spamm_mat m2 = nullptr;
     if (mat_new(ctx, A->n, A->b, cw->nsegs + A->nb, &m2)) return;
@@ -183,7 +183,7 @@ static void selfcheck_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, co
     double *tr = dalloc<double>(ctx, A->nb);
     cudaMemsetAsync(tr, 0, sizeof(double) * A->nb, ctx->stream);
     cudaMemsetAsync(cw->counters + CNT_GEMM_TICKET, 0, sizeof(int32_t), ctx->stream);
-    gemm_run(ctx, cw, A, B, halo, m2, epi, tr);
+    gemm_run(ctx, cw, A, B, halo, m2, epi, tr, nullptr, -1, 0, transA);
     const int64_t b2 = (int64_t)A->b * A->b;
     long long f0, f1;
     long long m0 = cmp_words(ctx, C->pool, m2->pool, 8 * b2 * cw->nsegs, &f0);
@@ -256,16 +256,18 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
 
 // product with a given workspace and epilogue; C allocated here
 static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
-                            double *trace_part, spamm_mat *C)
+                            double *trace_part, spamm_mat *C, int transA = 0)
 {
+    if (transA && A->dist)
+        return set_err(ctx, SPAMM_EINVAL, "A^T (x) B is not available on a row-partitioned context");
     if (A->dist != B->dist || A->r0 != B->r0 || A->r1 != B->r1)
         return set_err(ctx, SPAMM_ESHAPE, "operands have different row partitions");
     int pc = prof_begin(ctx, SPAMM_PH_CULL);
-    spamm_status sc = cull_run(ctx, cw, A, B, tau, A->r0, A->r1);
+    spamm_status sc = cull_run(ctx, cw, A, B, tau, A->r0, A->r1, transA);
     prof_end(ctx, pc);
     if (sc) return sc;
     g_product_id++;
-    if (selfcheck_mode()) selfcheck_cull(ctx, cw, A, B, tau);
+    if (selfcheck_mode()) selfcheck_cull(ctx, cw, A, B, tau, transA);
     const bool overlap = A->dist && A->parts.world > 1;
     double *halo = nullptr;
     int64_t nhalo = 0;
@@ -296,11 +298,11 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
         int32_t *order = lpt_mode() ? dalloc<int32_t>(ctx, cw->nsegs) : nullptr;
         if (order) st = lpt_order(ctx, cw->seg_len, nullptr, cw->nsegs, order);
         int pg = prof_begin(ctx, SPAMM_PH_GEMM);
-        if (!st) st = gemm_run(ctx, cw, A, B, halo, m, epi, trace_part, order, cw->nsegs, 0);
+        if (!st) st = gemm_run(ctx, cw, A, B, halo, m, epi, trace_part, order, cw->nsegs, 0, transA);
         prof_end(ctx, pg);
         dev_free(ctx, order, sizeof(int32_t) * cw->nsegs);
         prof_gemm_work(ctx, cw->ntasks, cw->nsegs, A->b);
-        if (!st && selfcheck_mode()) selfcheck_gemm(ctx, cw, A, B, halo, m, epi);
+        if (!st && selfcheck_mode()) selfcheck_gemm(ctx, cw, A, B, halo, m, epi, transA);
     }
     dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
     if (!st) {
@@ -325,6 +327,16 @@ extern "C" spamm_status spamm_multiply(spamm_ctx ctx, spamm_mat A, spamm_mat B, 
     ST(check_pair(ctx, A, B, tau));
     if (!C) return set_err(ctx, SPAMM_EINVAL, "NULL output");
     ST(product(ctx, ctx->cw[0], A, B, tau, EPI_STORE, nullptr, C));
+    if (stats) *stats = ctx->cw[0]->stats;
+    return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_multiply_t(spamm_ctx ctx, spamm_mat A, spamm_mat B, double tau, spamm_mat *C,
+                                         spamm_stats *stats)
+{
+    ST(check_pair(ctx, A, B, tau));
+    if (!C) return set_err(ctx, SPAMM_EINVAL, "NULL output");
+    ST(product(ctx, ctx->cw[0], A, B, tau, EPI_STORE, nullptr, C, 1));
     if (stats) *stats = ctx->cw[0]->stats;
     return SPAMM_OK;
 }
@@ -475,6 +487,196 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
             spamm_mat_free(Zf);
         }
     }
+    if (st) {
+        ctx->err = err;
+        return st;
+    }
+    return st2;
+}
+
+// ------------------------------------------------------------ single channel
+// PAPER.md Eq. single, sensitive product rightmost:
+//   Z_{k+1} = Z_k (x)_tau H_k,  W_{k+1} = s' (x)_tau_s Z_{k+1},
+//   H_{k+1} = h[Z_{k+1}^T (x)_tau W_{k+1}]  (X never stored for the plain map),
+// s' = s/c, Z_0 = I, X_0 = s' (t_0, H_0 = h[X_0] by maps), outputs Z -> s^{-1/2},
+// Y = W sqrt(c) -> s^{1/2}.  Not available on a row-partitioned context (Z^T).
+
+// t = (n - tr m)/n from the stored diagonal blocks (fixed order per block, then
+// the fixed-order trace_finish)
+__global__ void k_diag_trace(const double *pool, const int32_t *slot, int nb, int b, double *part)
+{
+    const int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (i >= nb) return;
+    const int s = slot[morton(i, i)];
+    double t = 0.0;
+    if (s >= 0)
+        for (int r = lane; r < b; r += 32) t += pool[(int64_t)s * b * b + pool_at(r, r, b)];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) part[i] = t;
+}
+
+static spamm_status mat_trace_err(spamm_ctx ctx, spamm_mat m, double *t_dev)
+{
+    double *part = dalloc<double>(ctx, m->nb);
+    if (!part) return set_err(ctx, SPAMM_ENOMEM, "trace");
+    k_diag_trace<<<cdiv(m->nb, 8), 256, 0, ctx->stream>>>(m->pool, m->slot, m->nb, m->b, part);
+    CKL(ctx);
+    spamm_status st = trace_finish(ctx, part, m->nb, m->n, t_dev);
+    dev_free(ctx, part, sizeof(double) * m->nb);
+    return st;
+}
+
+// H = h[X] of a stored X by maps (the initial H_0 = h[s']): t from the trace first
+static spamm_status h_of(spamm_ctx ctx, spamm_mat X, int map, spamm_mat *H)
+{
+    ST(mat_trace_err(ctx, X, ctx->dscratch));
+    if (!map) return mat_map(ctx, X, 4, 0.0, 0.0, H);
+    spamm_mat C;
+    ST(mat_map(ctx, X, 7, 0.0, 0.0, &C));
+    spamm_status st = ns_scaled_map(ctx, C, ctx->dscratch, ctx->dscratch + 8);
+    if (!st) st = norms_finish(ctx, C);
+    if (st) {
+        spamm_mat_free(C);
+        return st;
+    }
+    *H = C;
+    return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_ns_step_single(spamm_ctx ctx, spamm_mat S1, spamm_mat Z, spamm_mat H, double tau,
+                                             double tau_s, int32_t map, spamm_mat *Z_next, spamm_mat *H_next,
+                                             spamm_mat *W_out, double *t_next, spamm_stats stats[3],
+                                             double *alpha_eps)
+{
+    ST(check_pair(ctx, Z, H, tau));
+    ST(check_pair(ctx, S1, Z, tau));
+    if (!(tau_s >= 0.0) || !std::isfinite(tau_s)) return set_err(ctx, SPAMM_EINVAL, "tau_s must be >= 0");
+    if (map != 0 && map != 1) return set_err(ctx, SPAMM_EINVAL, "map must be 0 or 1");
+    if (!Z_next || !H_next) return set_err(ctx, SPAMM_EINVAL, "NULL output");
+    if (Z->dist) return set_err(ctx, SPAMM_EINVAL, "single channel needs Z^T: not on a row-partitioned context");
+    const int nb = Z->nb;
+    double *trace_part = dalloc<double>(ctx, nb);
+    if (!trace_part) return set_err(ctx, SPAMM_ENOMEM, "trace partials");
+    CK(cudaMemsetAsync(trace_part, 0, sizeof(double) * nb, ctx->stream));
+    spamm_mat Zn = nullptr, W = nullptr, Hn = nullptr;
+    spamm_status st = product(ctx, ctx->cw[0], Z, H, tau, EPI_STORE, nullptr, &Zn);
+    if (!st && stats) stats[0] = ctx->cw[0]->stats;
+    if (!st) st = product(ctx, ctx->cw[1], S1, Zn, tau_s, EPI_STORE, nullptr, &W);
+    if (!st && stats) stats[1] = ctx->cw[1]->stats;
+    if (!st) st = product(ctx, ctx->cw[2], Zn, W, tau, map ? EPI_NS_X : EPI_NS_H, trace_part, &Hn, 1);
+    if (!st && stats) stats[2] = ctx->cw[2]->stats;
+    if (!st) st = trace_finish(ctx, trace_part, nb, Z->n, ctx->dscratch);
+    if (!st && map) st = ns_scaled_map(ctx, Hn, ctx->dscratch, ctx->dscratch + 8);
+    if (!st && map) st = norms_finish(ctx, Hn);
+    double hv[3] = {0, 0, 0}, ae[2] = {1.0, 0.0};
+    if (!st) {
+        if (map) cudaMemcpyAsync(ae, ctx->dscratch + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&hv[0], ctx->dscratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&hv[1], Zn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&hv[2], Hn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) st = check_cuda(ctx, e, "ns single step");
+    }
+    dev_free(ctx, trace_part, sizeof(double) * nb);
+    if (st) {
+        spamm_mat_free(Zn);
+        spamm_mat_free(W);
+        spamm_mat_free(Hn);
+        return st;
+    }
+    if (t_next) *t_next = hv[0];
+    if (alpha_eps) {
+        alpha_eps[0] = ae[0];
+        alpha_eps[1] = ae[1];
+    }
+    *Z_next = Zn;
+    *H_next = Hn;
+    if (W_out) *W_out = W;
+    else spamm_mat_free(W);
+    if (!std::isfinite(hv[0]) || !std::isfinite(hv[1]) || !std::isfinite(hv[2]))
+        return set_err(ctx, SPAMM_ENOTFINITE, "non-finite trace error or root norm");
+    return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_ns_sqrt_single(spamm_ctx ctx, spamm_mat s, double tau, int32_t iters,
+                                             spamm_mat *Yout, spamm_mat *Zout, const spamm_ns_opts *opts)
+{
+    if (!ctx || !s || !Yout || !Zout) return set_err(ctx, SPAMM_EINVAL, "NULL argument");
+    if (iters < 1) return set_err(ctx, SPAMM_EINVAL, "iters must be >= 1");
+    if (!(tau >= 0.0) || !std::isfinite(tau)) return set_err(ctx, SPAMM_EINVAL, "tau must be finite and >= 0");
+    if (s->dist) return set_err(ctx, SPAMM_EINVAL, "single channel needs Z^T: not on a row-partitioned context");
+    spamm_ns_opts o{};
+    o.tau_s = -1.0;
+    o.power_iters = 100;
+    if (opts) o = *opts;
+    if (o.power_iters <= 0) o.power_iters = 100;
+    if (o.mu != 0.0) return set_err(ctx, SPAMM_EINVAL, "mu is not supported by the single channel");
+    const double tau_s = o.tau_s < 0.0 ? tau : o.tau_s;
+    int ps = prof_begin(ctx, SPAMM_PH_SETUP);
+    double root = 0.0;
+    ST(spamm_norm(ctx, s, &root));
+    if (!(root > 0.0)) return set_err(ctx, SPAMM_EINVAL, "s is zero");
+    double c = o.scale;
+    if (!(c > 0.0)) ST(power_scale(ctx, s, o.power_iters, &c));
+    if (o.c_out) *o.c_out = c;
+    if (o.iters_done) *o.iters_done = 0;
+    spamm_mat S1 = nullptr, Z = nullptr, H = nullptr, W = nullptr;
+    ST(spamm_ns_y0(ctx, s, c, 0.0, &S1));                 // s' = s/c = X_0
+    spamm_status st = spamm_identity(ctx, s->n, s->b, &Z);
+    if (!st) st = h_of(ctx, S1, o.map, &H);                // H_0 = h[X_0], t_0 -> dscratch
+    double t = 0.0;
+    if (!st) {
+        CK(cudaMemcpyAsync(&t, ctx->dscratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    if (!st) st = mat_map(ctx, S1, 2, 1.0, 0.0, &W);       // W_0 = s' (replaced by the first step)
+    prof_end(ctx, ps);
+    int pl = prof_begin(ctx, SPAMM_PH_LOOP);
+    for (int k = 0; k < iters && !st; k++) {
+        if (o.t_history) o.t_history[k] = t;
+        spamm_mat Zn = nullptr, Hn = nullptr, Wn = nullptr;
+        double tn = 0.0;
+        spamm_stats sts[3];
+        st = spamm_ns_step_single(ctx, S1, Z, H, tau, tau_s, o.map, &Zn, &Hn, &Wn, &tn, sts, nullptr);
+        if (o.per_product && st == SPAMM_OK) memcpy(o.per_product + 3 * k, sts, sizeof(sts));
+        if (st) {
+            spamm_mat_free(Zn);
+            spamm_mat_free(Hn);
+            spamm_mat_free(Wn);
+            break;
+        }
+        spamm_mat_free(Z);
+        spamm_mat_free(H);
+        spamm_mat_free(W);
+        Z = Zn;
+        H = Hn;
+        W = Wn;
+        if (o.iters_done) *o.iters_done = k + 1;
+        const double tk = t;
+        t = tn;
+        if (o.t_stop > 0.0 && std::fabs(tk) <= o.t_stop) break;
+    }
+    prof_end(ctx, pl);
+    std::string err = ctx->err;
+    spamm_status st2 = SPAMM_OK;
+    if (Z && W) {
+        const double f = std::sqrt(c);
+        spamm_mat Yf = nullptr, Zf = nullptr;
+        st2 = mat_map(ctx, W, 2, f, 0.0, &Yf);
+        if (!st2) st2 = mat_map(ctx, Z, 0, f, 0.0, &Zf);
+        if (!st2) {
+            *Yout = Yf;
+            *Zout = Zf;
+        } else {
+            spamm_mat_free(Yf);
+            spamm_mat_free(Zf);
+        }
+    }
+    spamm_mat_free(S1);
+    spamm_mat_free(Z);
+    spamm_mat_free(H);
+    spamm_mat_free(W);
     if (st) {
         ctx->err = err;
         return st;

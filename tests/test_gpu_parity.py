@@ -333,3 +333,44 @@ def test_ns_scaled_free_run_and_t_stop(ctx, cfg):
     np.testing.assert_allclose(r["t"], ro["t"], rtol=0, atol=1e-12)
     counts = np.array([[p["tasks"] for p in k] for k in r["stats"]])
     assert np.array_equal(counts, ro["counts"])
+
+
+# ------------------------------------------- single channel (§8(f) f2)
+@pytest.mark.parametrize("n,b", [(128, 16), (1024, 32), (2048, 64)])
+@pytest.mark.parametrize("tau", [0.0, 1e-6])
+def test_multiply_transposed(ctx, n, b, tau):
+    """A^T (x)_tau B: task set (modulo the window) and values vs the oracle's transposed tree."""
+    a = decaying(n, 20.0 / n, n + 7 * b)
+    c = decaying(n, 30.0 / n, n + 9 * b)
+    a[:b, 2 * b:3 * b] = 0.0
+    A, Ao = build_pair(ctx, "dense", a, b, n)
+    B, Bo = build_pair(ctx, "dense", c, b, n)
+    Cg, st = sp().spamm_multiply_t(ctx, A, B, tau, want_stats=True)
+    tg = {tuple(x) for x in sp().spamm_export_tasks(ctx)}
+    Co, to = O.multiply(Ao, Bo, tau, want_tasks=True, trans_a=True)
+    so = {tuple(x) for x in to}
+    assert len(tg) == st["tasks"]
+    diff = tg ^ so
+    assert diff <= window_set(O.transpose(Ao), Bo, tau)
+    if not diff:
+        assert rel(gpu_to_oracle(ctx, Cg).to_dense(), Co.to_dense()) <= 1e-12
+    if tau == 0.0:
+        assert rel(sp().spamm_to_dense(ctx, Cg).cpu().numpy(), a.T @ c) <= 1e-13
+
+
+@pytest.mark.parametrize("cfg,scaled", [("C1", False), ("C2", False), ("C2", True)])
+def test_ns_single_channel_free_run(ctx, cfg, scaled):
+    """Single channel full run vs the oracle: Y, Z <= 1e-10, t_k, task counts."""
+    c = si.CONFIGS[cfg]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    cs = O.power_scale(So)
+    tau_s = 0.01 * c.tau
+    r = sp().spamm_ns_sqrt_single(ctx, S, c.tau, c.iters, tau_s=tau_s, scale=cs, scaled=scaled, t_stop=1e-9)
+    ro = O.ns_sqrt_single(So, c.tau, c.iters, tau_s=tau_s, scale=cs, scaled=scaled, t_stop=1e-9)
+    assert r["iters"] == ro["iters"]
+    np.testing.assert_allclose(r["t"], ro["t"], rtol=0, atol=1e-12)
+    counts = np.array([[p["tasks"] for p in k] for k in r["stats"]])
+    assert np.array_equal(counts, ro["counts"])
+    assert rel(gpu_to_oracle(ctx, r["Y"]).to_dense(), ro["Y"].to_dense()) <= 1e-10
+    assert rel(gpu_to_oracle(ctx, r["Z"]).to_dense(), ro["Z"].to_dense()) <= 1e-10

@@ -433,3 +433,65 @@ def test_t_stop_prefix():
     assert 0 < k < cfg.iters
     assert np.array_equal(stop["t"], full["t"][:k])
     assert abs(stop["t"][-1]) <= 1e-6 and np.all(np.abs(full["t"][:k - 1]) > 1e-6)
+
+
+# ------------------------------------------- single channel (§8(f) f2)
+def test_transpose_and_multiply_t():
+    """A^T (x)_tau B: tau = 0 equals numpy A.T @ B; the task set is the brute-force leaf
+    test on the transposed norms ||A_ki|| ||B_kj|| >= tau ||A|| ||B||; the
+    transpose is an involution that carries the norms over."""
+    n, b = 256, 16
+    r = _rng(11)
+    i = np.arange(n)
+    a = np.exp(-0.05 * np.abs(i[:, None] - i[None, :])) * r.standard_normal((n, n))
+    c = np.exp(-0.03 * np.abs(i[:, None] - i[None, :])) * r.standard_normal((n, n))
+    a[:b, 3 * b:4 * b] = 0.0
+    A, B = O.OMat.from_dense(a, b), O.OMat.from_dense(c, b)
+    At = O.transpose(A)
+    assert np.array_equal(At.to_dense(), a.T)
+    assert np.array_equal(O.transpose(At).to_dense(), a)
+    assert At.norm() == A.norm()
+    C0 = O.multiply(A, B, 0.0, trans_a=True)
+    assert np.linalg.norm(C0.to_dense() - a.T @ c) <= 1e-13 * np.linalg.norm(a.T @ c)
+    for tau in (1e-4, 1e-2):
+        Ct, tasks = O.multiply(A, B, tau, want_tasks=True, trans_a=True)
+        na, nb_ = A.leaf_norms(), B.leaf_norms()          # na[k, i] = ||A_ki||
+        thr = tau * A.norm() * B.norm()
+        prod = na.T[:, :, None] * nb_[None, :, :]          # [i, k, j]
+        brute = {tuple(x) for x in np.argwhere((na.T[:, :, None] > 0) & (nb_[None] > 0) & (prod >= thr))}
+        got = {tuple(x) for x in tasks}
+        amb = {tuple(x) for x in np.argwhere(np.abs(prod - thr) <= 1e-12 * thr)}
+        assert (got ^ brute) <= amb
+
+
+def test_single_channel_tau0_matches_eig_and_dual():
+    """P:398-402 at tau = 0: Z -> s^{-1/2}, Y = s Z -> s^{1/2}; the single and dual
+    channels are the same iteration in exact arithmetic (z_k commutes with s)."""
+    n, b = 128, 16
+    g = _rng(4).standard_normal((n, n)) * np.exp(-0.05 * np.abs(np.subtract.outer(np.arange(n), np.arange(n))))
+    s = g @ g.T / n + 0.5 * np.eye(n)
+    S = O.OMat.from_dense(s, b)
+    r1 = O.ns_sqrt_single(S, 0.0, 40)
+    r2 = O.ns_sqrt(S, 0.0, 40)
+    for M, p in ((r1["Y"], 0.5), (r1["Z"], -0.5)):
+        ref = _eig_pow(s, p)
+        assert np.linalg.norm(M.to_dense() - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert np.linalg.norm(r1["Z"].to_dense() - r2["Z"].to_dense()) <= 1e-12 * np.linalg.norm(r2["Z"].to_dense())
+    assert abs(r1["t"][-1]) < 1e-14
+
+
+def test_single_channel_diagonal_scalar_map():
+    """Diagonal s: the single channel decouples into z' = z h(x), x' = z'^2 lambda/c
+    (P:398-402 with commuting scalars); at tau = 0 the iterates match to 1 ulp-level."""
+    n, b = 64, 16
+    lam = np.linspace(0.1, 1.0, n)
+    S = O.OMat.from_dense(np.diag(lam), b)
+    r = O.ns_sqrt_single(S, 0.0, 12, scale=1.0)
+    z, x = np.ones(n), lam.copy()
+    for k in range(12):
+        assert r["t"][k] == pytest.approx((n - x.sum()) / n, abs=1e-15)
+        h = 0.5 * (3.0 - x)
+        z = z * h
+        x = z * (lam * z)
+    np.testing.assert_allclose(np.diag(r["Z"].to_dense()), z, rtol=1e-15)
+    assert r["counts"].shape == (12, 3)
