@@ -195,6 +195,12 @@ spamm_status spamm_multiply_t(spamm_ctx ctx, spamm_mat A, spamm_mat B, double ta
  * in Morton order, k ascending; ikj is HOST [3*cap]; *n = total count. */
 spamm_status spamm_export_tasks(spamm_ctx ctx, int32_t *ikj, int64_t cap, int64_t *n);
 
+/* Product-volume instrumentation (the lensing of P:804-823):
+ * histogram of d = max(|i-j|, |i-k|, |j-k|) over the last product's surviving leaf
+ * triples (i,k,j); hist: HOST [nbins] int64, d >= nbins-1 counted in the last bin.
+ * Exact integer counts.  Synchronises. */
+spamm_status spamm_task_distance_hist(spamm_ctx ctx, int64_t *hist, int32_t nbins);
+
 /* -------------------------------------------------------- Newton-Schulz */
 /* One dual step (north_star form): X = Z (x)_tau Y; t = (n - tr X)/n;
  * H = 1/2 (3I - X) (fused in the X epilogue, X is never stored);

@@ -26,7 +26,7 @@ __all__ = [
     "spamm_ctx_create", "spamm_ctx_destroy", "spamm_last_error", "spamm_kernel_launches",
     "spamm_build_tree", "spamm_build_tree_blocks", "spamm_mat_free", "spamm_mat_info",
     "spamm_norm", "spamm_to_dense", "spamm_level_norms2", "spamm_get_blocks",
-    "spamm_multiply", "spamm_multiply_t", "spamm_ns_step_single", "spamm_ns_sqrt_single", "spamm_export_tasks", "spamm_ns_step", "spamm_ns_step_map", "spamm_power_scale",
+    "spamm_multiply", "spamm_multiply_t", "spamm_task_distance_hist", "spamm_ns_step_single", "spamm_ns_sqrt_single", "spamm_export_tasks", "spamm_ns_step", "spamm_ns_step_map", "spamm_power_scale",
     "spamm_ns_y0", "spamm_identity", "spamm_ns_sqrt", "spamm_scale",
     "spamm_export_blocks", "spamm_profile_enable", "spamm_profile_read", "spamm_peak_dmma",
     "Comm", "spamm_comm_nccl_unique_id", "spamm_comm_nccl_create", "spamm_comm_local_group",
@@ -107,6 +107,7 @@ def load():
         "spamm_multiply": (i32, [vp, vp, vp, dbl, P(vp), P(spamm_stats)]),
         "spamm_export_tasks": (i32, [vp, vp, i64, P(i64)]),
         "spamm_multiply_t": (i32, [vp, vp, vp, dbl, P(vp), P(spamm_stats)]),
+        "spamm_task_distance_hist": (i32, [vp, vp, i32]),
         "spamm_ns_step_single": (i32, [vp, vp, vp, vp, dbl, dbl, i32, P(vp), P(vp), P(vp), P(dbl), vp, vp]),
         "spamm_ns_sqrt_single": (i32, [vp, vp, dbl, i32, P(vp), P(vp), P(spamm_ns_opts)]),
         "spamm_ns_step": (i32, [vp, vp, vp, dbl, dbl, P(vp), P(vp), P(vp), P(dbl), vp]),
@@ -464,6 +465,13 @@ def spamm_ns_sqrt_single(ctx: Ctx, s: Mat, tau: float, iters: int, tau_s: float 
     k = done.value
     stats = [[sts[3 * j + p].as_dict() for p in range(3)] for j in range(k)]
     return dict(Y=Mat(ctx, yo), Z=Mat(ctx, zo), t=t[:k], stats=stats, c=c.value, iters=k)
+
+
+def spamm_task_distance_hist(ctx: Ctx, nbins: int) -> np.ndarray:
+    """Histogram of max(|i-j|, |i-k|, |j-k|) over the last product's leaf triples."""
+    out = np.zeros(nbins, dtype=np.int64)
+    ctx.check(load().spamm_task_distance_hist(ctx.h, _ptr(out), int(nbins)))
+    return out
 
 
 def spamm_export_tasks(ctx: Ctx) -> np.ndarray:

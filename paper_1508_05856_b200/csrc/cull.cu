@@ -19,6 +19,8 @@
 //   k_cull_segments compaction of segment heads -> {code, start, len}.
 // Counts live in device memory; kernels are persistent / grid-stride, so the
 // whole query is enqueued with no host round trip.
+#include <algorithm>
+
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -530,4 +532,38 @@ extern "C" spamm_status spamm_row_task_counts(spamm_ctx ctx, spamm_mat A, spamm_
     if (cw->hcnt) cudaFreeHost(cw->hcnt);
     delete cw;
     return st;
+}
+
+// ------------------------------------------------ lensing instrumentation (f4)
+// Histogram of the diagonal-plane distance d = max(|i-j|, |i-k|, |j-k|) of the
+// last product's surviving leaf triples (the product-volume "lensing" of P:804-823,
+// S:484): integer atomics, so the counts are exact and deterministic.
+__global__ void k_task_dist_hist(const int4 *rec, int64_t n, int nbins, unsigned long long *hist)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 r = rec[t];
+        const int i = morton_i((uint32_t)r.x), j = morton_j((uint32_t)r.x), k = r.y;
+        int d = abs(i - j);
+        d = max(d, abs(i - k));
+        d = max(d, abs(j - k));
+        atomicAdd(&hist[d < nbins ? d : nbins - 1], 1ull);
+    }
+}
+
+extern "C" spamm_status spamm_task_distance_hist(spamm_ctx ctx, int64_t *hist, int32_t nbins)
+{
+    if (!ctx || !hist || nbins < 1) return set_err(ctx, SPAMM_EINVAL, "bad argument");
+    for (int b = 0; b < nbins; b++) hist[b] = 0;
+    Cull *cw = ctx->last;
+    if (!cw || cw->ntasks == 0) return SPAMM_OK;
+    unsigned long long *d = dalloc<unsigned long long>(ctx, nbins);
+    if (!d) return set_err(ctx, SPAMM_ENOMEM, "histogram");
+    CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * nbins, ctx->stream));
+    const int grid = (int)std::min<int64_t>(cdiv(cw->ntasks, 256), 8 * ctx->sm_count);
+    k_task_dist_hist<<<grid, 256, 0, ctx->stream>>>(cw->rec[cw->final_buf], cw->ntasks, nbins, d);
+    CKL(ctx);
+    CK(cudaMemcpyAsync(hist, d, sizeof(int64_t) * nbins, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    dev_free(ctx, d, sizeof(unsigned long long) * nbins);
+    return SPAMM_OK;
 }

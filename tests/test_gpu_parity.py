@@ -374,3 +374,18 @@ def test_ns_single_channel_free_run(ctx, cfg, scaled):
     assert np.array_equal(counts, ro["counts"])
     assert rel(gpu_to_oracle(ctx, r["Y"]).to_dense(), ro["Y"].to_dense()) <= 1e-10
     assert rel(gpu_to_oracle(ctx, r["Z"]).to_dense(), ro["Z"].to_dense()) <= 1e-10
+
+
+def test_task_distance_histogram(ctx):
+    """Lensing instrumentation (§8(f) f4): the histogram of max(|i-j|,|i-k|,|j-k|) over the
+    surviving triples equals the one computed from the oracle's task list (exact ints)."""
+    c = si.CONFIGS["C2"]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    sp().spamm_multiply(ctx, S, S, c.tau)
+    h = sp().spamm_task_distance_hist(ctx, 200)
+    _, to = O.multiply(So, So, c.tau, want_tasks=True)
+    d = np.max(np.abs(np.stack([to[:, 0] - to[:, 2], to[:, 0] - to[:, 1], to[:, 2] - to[:, 1]])), axis=0)
+    ref = np.bincount(np.minimum(d, 199), minlength=200)
+    assert np.array_equal(h, ref)
+    assert h.sum() == len(to)
