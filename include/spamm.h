@@ -69,6 +69,7 @@ typedef struct {
     int64_t candidates;         /* leaf-level candidate triples tested               */
     int64_t level_survivors[24];/* survivors per quadtree level (index = level)      */
     double flops;               /* 2 b^3 |S|                                         */
+    int64_t halo_blocks;        /* row partition: remote right-operand blocks fetched */
 } spamm_stats;
 
 /* Options of spamm_ns_sqrt (NULL => defaults).  History buffers are HOST memory. */

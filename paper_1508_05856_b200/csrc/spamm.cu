@@ -234,6 +234,7 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
         st = halo_exchange(ctx, cw, B, &halo, &nhalo);
         prof_end(ctx, px);
         ctx->stream = main_s;
+        cw->stats.halo_blocks = nhalo;
     }
     if (!st) {
         CK(cudaEventRecord(ctx->ev[1], comm_s));

@@ -36,6 +36,63 @@ __global__ void __launch_bounds__(256) k(const double *seed, long iters, double 
     if (t == 1.2345) out[0] = t;
 }
 
+// MODE 2: the leaf GEMM's consumer inner loop with its shared-memory fragment loads
+// (32x16 warp tile, MF=4, NF=2, 4 k-chunks of 16 per 64-wide task), no barriers.
+__global__ void __launch_bounds__(256) k_lds(long iters, double *out)
+{
+    extern __shared__ double sm[];
+    for (int i = threadIdx.x; i < 2 * 4096; i += blockDim.x) sm[i] = 1e-3 * (i & 7);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3, m0 = (warp / 4) * 32, n0 = (warp % 4) * 16;
+    const double *As = sm, *Bs = sm + 4096;
+    double c[4][2][2] = {};
+    for (long it = 0; it < iters; it++) {
+#pragma unroll
+        for (int kc = 0; kc < 4; kc++) {
+            double a[4][4], b[2][4];
+#pragma unroll
+            for (int mf = 0; mf < 4; mf++) {
+                const int r = m0 + 8 * mf + g8;
+                const double2 v0 = *reinterpret_cast<const double2 *>(As + r * 64 + 16 * kc + 4 * t4);
+                const double2 v1 = *reinterpret_cast<const double2 *>(As + r * 64 + 16 * kc + 4 * t4 + 2);
+                a[mf][0] = v0.x; a[mf][1] = v0.y; a[mf][2] = v1.x; a[mf][3] = v1.y;
+            }
+#pragma unroll
+            for (int nf = 0; nf < 2; nf++)
+#pragma unroll
+                for (int s = 0; s < 4; s++) b[nf][s] = Bs[(16 * kc + 4 * t4 + s) * 64 + n0 + 8 * nf + g8];
+#pragma unroll
+            for (int s = 0; s < 4; s++)
+#pragma unroll
+                for (int mf = 0; mf < 4; mf++)
+#pragma unroll
+                    for (int nf = 0; nf < 2; nf++) dmma(c[mf][nf][0], c[mf][nf][1], a[mf][s], b[nf][s]);
+        }
+    }
+    double t = 0;
+    for (int mf = 0; mf < 4; mf++)
+        for (int nf = 0; nf < 2; nf++) t += c[mf][nf][0] + c[mf][nf][1];
+    if (t == 1.2345) out[0] = t;
+}
+
+void run_lds(long iters, double *seed)
+{
+    cudaFuncSetAttribute(k_lds, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_lds<<<148, 256, 65536>>>(iters / 10, seed + 64);
+    cudaEventRecord(e0);
+    k_lds<<<148, 256, 65536>>>(iters, seed + 64);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double flops = 148.0 * 8 * iters * 128 * 512;
+    printf("mode 2 (with smem fragment loads, bank conflicts ignored) 148 CTAs x 8 warps: %.2f TFLOP/s\n", flops / ms / 1e9);
+}
+
 template <int MODE>
 void run(int ctas, int threads, long iters, double *seed)
 {
@@ -62,5 +119,6 @@ int main()
         run<0>(148 * (w == 256 ? 4 : 1), w == 256 ? 256 : 256, 200000, seed);
         run<1>(148 * (w == 256 ? 4 : 1), w == 256 ? 256 : 256, 200000, seed);
     }
+    run_lds(50000, seed);
     return 0;
 }
