@@ -345,10 +345,65 @@ def run_ours(args):
         except (OSError, ValueError):
             pass
 
-    # ---- e2e through the C ABI with HOST buffers
+    # ---- e2e through the C ABI with HOST buffers: every step copies its input from
+    # pinned host memory (H2D) and its result Y, Z back to pinned host memory (D2H).
+    # The copies run on two copy streams, pipelined with the neighbouring steps' compute
+    # (double-buffered result buffers), as a serving pipeline would; all of them are
+    # inside the timed region.
     e2e = None
     if not args.no_e2e:
-        step(h_in, True)  # allocate pinned result buffers
+        h2d, copy = torch.cuda.Stream(dev), torch.cuda.Stream(dev)   # separate copy engines / queues
+        dbuf, hbuf, done = [{}, {}], [{}, {}], [None, None]
+
+        def bufs(i, key, nblk):
+            d = dbuf[i].get(key)
+            if d is None or d[0].shape[0] < nblk:
+                cap = int(nblk * 1.25) + 16
+                dbuf[i][key] = (torch.empty(cap, dtype=torch.int32, device=dev),
+                                torch.empty(cap, dtype=torch.int32, device=dev),
+                                torch.empty((cap, cfg.b, cfg.b), dtype=torch.float64, device=dev))
+                hbuf[i][key] = (torch.empty(cap, dtype=torch.int32).pin_memory(),
+                                torch.empty(cap, dtype=torch.int32).pin_memory(),
+                                torch.empty((cap, cfg.b, cfg.b), dtype=torch.float64).pin_memory())
+            return dbuf[i][key], hbuf[i][key]
+
+        def e2e_step(i):
+            with torch.cuda.stream(h2d):
+                d = tuple(h.to(dev, non_blocking=True) for h in h_in)
+            stream.wait_stream(h2d)
+            for x in d:
+                x.record_stream(stream)
+            S = build(d)
+            if args.channel == "single":
+                r = sp.spamm_ns_sqrt_single(ctx, S, tau, iters, tau_s=tau_s, t_stop=t_stop, scaled=scaled)
+            else:
+                r = sp.spamm_ns_sqrt(ctx, S, tau, iters, tau_s=tau_s, mu=cfg.mu, t_stop=t_stop, scaled=scaled)
+            S.free()
+            slot = i % 2
+            if done[slot] is not None:
+                stream.wait_event(done[slot])        # that slot's previous D2H has finished
+            nbytes = 0
+            pairs = []
+            for key in ("Y", "Z"):
+                nblk = r[key].nblocks
+                db, hb = bufs(slot, key, nblk)
+                sp.spamm_export_blocks(ctx, r[key], db)
+                pairs.append((db, hb, nblk))
+                nbytes += nblk * (8 + 8 * cfg.b * cfg.b)
+            r["Y"].free()
+            r["Z"].free()
+            copy.wait_stream(stream)
+            with torch.cuda.stream(copy):
+                for db, hb, nblk in pairs:
+                    for dt_, ht_ in zip(db, hb):
+                        ht_[:nblk].copy_(dt_[:nblk], non_blocking=True)
+            done[slot] = copy.record_event()
+            flops = sum(p["flops"] for k in r["stats"] for p in k)
+            return flops, nbytes
+
+        for i in range(2):                            # allocate the buffers (untimed)
+            e2e_step(i)
+        torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
         e2 = torch.cuda.Event(enable_timing=True)
@@ -356,9 +411,10 @@ def run_ours(args):
         e2.record(stream)
         ef = 0.0
         d2h = 0
-        for _ in range(args.steps):
-            f, _, d2h, _ = step(h_in, True)
+        for i in range(args.steps):
+            f, d2h = e2e_step(i)
             ef += f
+        stream.wait_stream(copy)
         e3.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -366,7 +422,8 @@ def run_ours(args):
         e2e = {"value": D.sum_over_ranks(ef, dev) / (ems * 1e-3) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": int(D.sum_over_ranks(in_bytes, dev)),
                "d2h_bytes_per_step": int(D.sum_over_ranks(d2h, dev)),
-               "ms_per_step": ems / args.steps}
+               "ms_per_step": ems / args.steps,
+               "pipelining": "H2D / D2H on copy streams overlapped with the neighbouring steps' compute"}
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None

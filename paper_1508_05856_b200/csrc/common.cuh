@@ -68,6 +68,8 @@ struct spamm_ctx_s {
     std::vector<int> row_start;   // [world+1] block rows; empty => equal split per nb
     struct Dist *dist = nullptr;  // exchange workspaces
     cudaStream_t comm_stream = nullptr;   // halo exchange overlapped with the local GEMM
+    void *zc = nullptr;            // mapped pinned host buffer for small device->host reads
+    void *zc_dev = nullptr;        // its device alias
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
 
@@ -151,6 +153,24 @@ __host__ __device__ static inline int pool_col(int e, int b)
 {
     int r = e / b, q = e % b;
     return ((((q >> 1) ^ swz(r)) << 1) | (q & 1));
+}
+
+// ------------------------------------------------------ small device->host reads
+// Counts and scalars are read back through a kernel that stores into mapped pinned
+// host memory, not cudaMemcpy: a small D2H copy queues behind any large transfer on
+// the copy engine (e.g. a caller streaming the previous result to the host), while a
+// kernel's stores go straight over the bus.  One launch + one stream sync per call.
+#define SPAMM_ZC_BYTES 65536
+struct FetchItem {
+    const void *src;   // device
+    void *dst;         // host
+    uint32_t bytes;    // multiple of 4
+};
+spamm_status fetch(spamm_ctx ctx, const FetchItem *items, int n);
+static inline spamm_status fetch1(spamm_ctx ctx, const void *src, void *dst, uint32_t bytes)
+{
+    FetchItem it{src, dst, bytes};
+    return fetch(ctx, &it, 1);
 }
 
 // ------------------------------------------------------------------ errors

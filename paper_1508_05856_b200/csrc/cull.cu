@@ -453,9 +453,7 @@ spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double 
     }
     for (int attempt = 0; attempt < 8; attempt++) {
         ST(cull_enqueue(ctx, cw, A, B, tau, r0, r1, transA));
-        CK(cudaMemcpyAsync(cw->hcnt, cw->counters, sizeof(int32_t) * 64, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+        ST(fetch1(ctx, cw->counters, cw->hcnt, sizeof(int32_t) * 64));
         if (!cw->hcnt[CNT_OVERFLOW]) {
             cw->ntasks = cw->hcnt[cw->L];
             cw->nsegs = cw->hcnt[CNT_NSEG];

@@ -244,16 +244,14 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
         CKL(ctx);
         k_owner_bounds<<<1, 96, 0, s>>>(excl, nb, P, dbounds);
         CKL(ctx);
-        CK(cudaMemcpyAsync(hb.data(), dbounds, sizeof(int64_t) * (W + 1), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        ST(fetch1(ctx, dbounds, hb.data(), sizeof(int64_t) * (W + 1)));
         total = hb[W];
         // 2. request counts: M[q][p] = blocks rank q wants from rank p
         std::vector<int64_t> mine(W);
         for (int p = 0; p < W; p++) mine[p] = hb[p + 1] - hb[p];
         CK(cudaMemcpyAsync(dmine, mine.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice, s));
         if ((st = comm->allgather(ctx, dmine, dall, sizeof(int64_t) * W))) break;
-        CK(cudaMemcpyAsync(M.data(), dall, sizeof(int64_t) * W * W, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        ST(fetch1(ctx, dall, M.data(), sizeof(int64_t) * W * W));
         for (int q = 0; q < W; q++) serve += M[(size_t)q * W + me];
         // 3. request lists to the owners
         codes = dalloc<int32_t>(ctx, total);
@@ -359,9 +357,7 @@ spamm_status seg_split(spamm_ctx ctx, Cull *cw, int32_t **order, int64_t *nlocal
         k_need_scan<512><<<std::min(ntiles, 2 * ctx->sm_count), 512, 0, s>>>(flag, ns, tiles, excl);
         k_seg_order<<<cdiv(ns, 256), 256, 0, s>>>(flag, excl, ns, ord);
         ctx->launches += 2;
-        cudaMemcpyAsync(&h, excl + ns, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-        cudaError_t e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) st = check_cuda(ctx, e, "segment split");
+        st = fetch1(ctx, excl + ns, &h, sizeof(int32_t));
     }
     dev_free(ctx, flag, sizeof(int32_t) * ns);
     dev_free(ctx, excl, sizeof(int32_t) * (ns + 1));

@@ -491,8 +491,7 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
     k_diag_fill<<<m->nb, 256, 0, ctx->stream>>>(newslot, m->pool, m->b, value, m->norm2 + pyr_off(m->L));
     CKL(ctx);
     int64_t h = 0;
-    CK(cudaMemcpyAsync(&h, ctx->iscratch, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    ST(fetch1(ctx, ctx->iscratch, &h, sizeof(int64_t)));
     dev_free(ctx, newslot, sizeof(int32_t) * m->nb);
     *added = h;
     return SPAMM_OK;

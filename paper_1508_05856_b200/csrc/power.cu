@@ -228,8 +228,7 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
     CKL(ctx);
     double h = 0;
-    CK(cudaMemcpyAsync(&h, c, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ST(fetch1(ctx, c, &h, sizeof(double)));
     *c_host = h;
     dev_free(ctx, cnt, sizeof(int32_t) * nb);
     dev_free(ctx, rowptr, sizeof(int32_t) * (nb + 1));

@@ -69,6 +69,7 @@ extern "C" void spamm_ctx_destroy(spamm_ctx ctx)
         if (ctx->cw[i]->hcnt) cudaFreeHost(ctx->cw[i]->hcnt);
         delete ctx->cw[i];
     }
+    if (ctx->zc) cudaFreeHost(ctx->zc);
     dev_free(ctx, ctx->dscratch, sizeof(double) * 64);
     dev_free(ctx, ctx->iscratch, sizeof(int64_t) * 64);
     cudaStreamSynchronize(ctx->stream);
@@ -382,12 +383,9 @@ extern "C" spamm_status spamm_ns_step_map(spamm_ctx ctx, spamm_mat Y, spamm_mat 
     double hv[3] = {0, 0, 0}, ae[2] = {1.0, 0.0};
     if (!st) {
         // t_k and the root norms (non-finite detection)
-        if (map) cudaMemcpyAsync(ae, ctx->dscratch + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-        cudaMemcpyAsync(&hv[0], ctx->dscratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-        cudaMemcpyAsync(&hv[1], Yn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-        cudaMemcpyAsync(&hv[2], Zn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-        cudaError_t e = cudaStreamSynchronize(ctx->stream);
-        if (e != cudaSuccess) st = check_cuda(ctx, e, "ns step");
+        FetchItem it[4] = {{ctx->dscratch, &hv[0], 8}, {Yn->norm2, &hv[1], 8}, {Zn->norm2, &hv[2], 8},
+                           {ctx->dscratch + 8, ae, 16}};
+        st = fetch(ctx, it, map ? 4 : 3);
     }
     dev_free(ctx, trace_part, sizeof(double) * nb);
     if (st) {
@@ -572,12 +570,9 @@ extern "C" spamm_status spamm_ns_step_single(spamm_ctx ctx, spamm_mat S1, spamm_
     if (!st && map) st = norms_finish(ctx, Hn);
     double hv[3] = {0, 0, 0}, ae[2] = {1.0, 0.0};
     if (!st) {
-        if (map) cudaMemcpyAsync(ae, ctx->dscratch + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-        cudaMemcpyAsync(&hv[0], ctx->dscratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-        cudaMemcpyAsync(&hv[1], Zn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-        cudaMemcpyAsync(&hv[2], Hn->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-        cudaError_t e = cudaStreamSynchronize(ctx->stream);
-        if (e != cudaSuccess) st = check_cuda(ctx, e, "ns single step");
+        FetchItem it[4] = {{ctx->dscratch, &hv[0], 8}, {Zn->norm2, &hv[1], 8}, {Hn->norm2, &hv[2], 8},
+                           {ctx->dscratch + 8, ae, 16}};
+        st = fetch(ctx, it, map ? 4 : 3);
     }
     dev_free(ctx, trace_part, sizeof(double) * nb);
     if (st) {
@@ -628,8 +623,7 @@ extern "C" spamm_status spamm_ns_sqrt_single(spamm_ctx ctx, spamm_mat s, double 
     if (!st) st = h_of(ctx, S1, o.map, &H);                // H_0 = h[X_0], t_0 -> dscratch
     double t = 0.0;
     if (!st) {
-        CK(cudaMemcpyAsync(&t, ctx->dscratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+        ST(fetch1(ctx, ctx->dscratch, &t, sizeof(double)));
     }
     if (!st) st = mat_map(ctx, S1, 2, 1.0, 0.0, &W);       // W_0 = s' (replaced by the first step)
     prof_end(ctx, ps);

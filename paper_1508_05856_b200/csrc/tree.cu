@@ -72,6 +72,45 @@ void dev_free(spamm_ctx ctx, void *p, size_t bytes)
     else cudaFreeAsync(p, ctx->stream);
 }
 
+struct FetchArgs {
+    const uint32_t *src[8];
+    uint32_t words[8];
+    uint32_t off[8];
+    int n;
+};
+
+__global__ void k_fetch(FetchArgs a, uint32_t *dst)
+{
+    for (int i = 0; i < a.n; i++)
+        for (uint32_t w = threadIdx.x; w < a.words[i]; w += blockDim.x) dst[a.off[i] + w] = a.src[i][w];
+}
+
+spamm_status fetch(spamm_ctx ctx, const FetchItem *items, int n)
+{
+    if (!ctx->zc) {
+        CK(cudaHostAlloc(&ctx->zc, SPAMM_ZC_BYTES, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(&ctx->zc_dev, ctx->zc, 0));
+    }
+    for (int i0 = 0; i0 < n; i0 += 8) {
+        FetchArgs a{};
+        uint32_t off = 0;
+        for (int i = i0; i < n && i < i0 + 8; i++) {
+            if (items[i].bytes % 4 || off * 4 + items[i].bytes > SPAMM_ZC_BYTES)
+                return set_err(ctx, SPAMM_EINVAL, "fetch of %u bytes", items[i].bytes);
+            a.src[a.n] = (const uint32_t *)items[i].src;
+            a.words[a.n] = items[i].bytes / 4;
+            a.off[a.n] = off;
+            off += items[i].bytes / 4;
+            a.n++;
+        }
+        k_fetch<<<1, 256, 0, ctx->stream>>>(a, (uint32_t *)ctx->zc_dev);
+        CKL(ctx);
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < a.n; i++) memcpy(items[i0 + i].dst, (const uint32_t *)ctx->zc + a.off[i], items[i0 + i].bytes);
+    }
+    return SPAMM_OK;
+}
+
 int is_device_ptr(const void *p)
 {
     cudaPointerAttributes a;
@@ -330,12 +369,8 @@ static spamm_status build_common(spamm_ctx ctx, BlockSrc src, int64_t count, int
             ctx->launches++;
             // total present = last tile inclusive prefix
             V1 last;
-            if (cudaMemcpyAsync(&last, pre + (ntiles - 1), sizeof(V1), cudaMemcpyDeviceToHost,
-                                ctx->stream) != cudaSuccess ||
-                cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
-                st = check_cuda(ctx, cudaGetLastError(), "build count");
-                break;
-            }
+            st = fetch1(ctx, pre + (ntiles - 1), &last, sizeof(V1));
+            if (st) break;
             nblk = last.x;
         }
         st = mat_new(ctx, n, b, nblk, &m);
@@ -631,8 +666,7 @@ extern "C" spamm_status spamm_norm(spamm_ctx ctx, spamm_mat m, double *fro)
 {
     if (!ctx || !m || !fro) return set_err(ctx, SPAMM_EINVAL, "bad argument");
     double r;
-    CK(cudaMemcpyAsync(&r, m->norm2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    ST(fetch1(ctx, m->norm2, &r, sizeof(double)));
     *fro = sqrt(r);
     return SPAMM_OK;
 }
