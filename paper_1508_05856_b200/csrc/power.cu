@@ -3,8 +3,11 @@
 // v0 = 1/sqrt(n) * ones, then the Rayleigh quotient c = v^T s v.
 // Block-CSR SpMV (one CTA per block row, blocks in ascending column order,
 // warp-per-row dot products with fixed-order shuffle reductions: deterministic).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "scan.cuh"
+#include "tma.cuh"
 
 // per block row: count of present blocks
 __global__ void k_row_count(const int32_t *slot, int nb, int32_t *cnt)
@@ -137,6 +140,132 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
     }
 }
 
+// ------------------------------------------------- TMA-staged SpMV (b = 64)
+// One persistent CTA per SM streams whole 32 KiB blocks into a 6-stage shared
+// memory ring with TMA bulk copies (thread 0 issues, mbarrier transaction counts
+// signal arrival), so ~192 KiB per SM are in flight without holding them in
+// registers.  Work units are quarters of block rows (a quarter of the row's blocks,
+// ascending), taken from a ticket; a thread owns one 16-byte chunk of 8 rows of
+// each block (consecutive lanes read consecutive chunks: conflict-free) and keeps
+// 8 row accumulators across the unit's blocks.  Each unit writes its 64 partial row
+// sums; k_spmv_fix adds the 4 quarters in a fixed order (deterministic).
+constexpr int SPT_STAGES = 6, SPT_Q = 4, SPT_B = 64;
+
+struct SpmvTmaArgs {
+    const double *pool;
+    const int32_t *rowptr, *cols, *slots;
+    const double *v;
+    double *part;       // [nb * SPT_Q * 64]
+    int32_t *ticket;
+    int nunits;         // nb * SPT_Q
+};
+
+__global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
+{
+    constexpr int TILE = SPT_B * SPT_B;
+    extern __shared__ __align__(1024) double sm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + SPT_STAGES * TILE);
+    int4 *meta = reinterpret_cast<int4 *>(full + SPT_STAGES);   // {unit, column block, last, -}
+    __shared__ int s_total;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // issuer state (thread 0); the unit's slot / column indices are fetched in one
+    // batch of independent loads (UCH at a time), not one dependent load per issue
+    constexpr int UCH = 32;
+    int issued = 0, unit = -1, p = 0, pend = 0, ubase = 0;
+    int us[UCH], uc[UCH];
+    bool done = false;
+    if (tid == 0) {
+        for (int st = 0; st < SPT_STAGES; st++) mbar_init(&full[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        s_total = -1;
+    }
+    __syncthreads();
+    double acc[8];
+#pragma unroll
+    for (int m = 0; m < 8; m++) acc[m] = 0.0;
+    // logical column pairs of this thread's chunk in rows warp + 8m (pool swizzle)
+    int lc[8];
+#pragma unroll
+    for (int m = 0; m < 8; m++) lc[m] = (lane ^ swz(warp + 8 * m)) << 1;
+    for (int j = 0;; j++) {
+        if (tid == 0) {
+            // keep the ring full: blocks j .. j + STAGES - 1 in flight
+            while (!done && issued < j + SPT_STAGES) {
+                if (p == pend) {
+                    unit = atomicAdd(g.ticket, 1);
+                    if (unit >= g.nunits) {
+                        done = true;
+                        s_total = issued;
+                        break;
+                    }
+                    const int I = unit / SPT_Q, q = unit % SPT_Q;
+                    const int p0 = g.rowptr[I], len = g.rowptr[I + 1] - p0;
+                    p = p0 + (q * len) / SPT_Q;
+                    pend = p0 + ((q + 1) * len) / SPT_Q;
+                    ubase = p - UCH;   // forces a fetch below
+                    continue;
+                }
+                if (p - ubase >= UCH) {
+                    ubase = p;
+#pragma unroll
+                    for (int i = 0; i < UCH; i++) {
+                        us[i] = p + i < pend ? __ldg(g.slots + p + i) : 0;
+                        uc[i] = p + i < pend ? __ldg(g.cols + p + i) : 0;
+                    }
+                }
+                const int st = issued % SPT_STAGES;
+                meta[st] = make_int4(unit, uc[p - ubase], p + 1 == pend, 0);
+                mbar_expect_tx(&full[st], TILE * 8);
+                bulk_g2s(sm + st * TILE, g.pool + (int64_t)us[p - ubase] * TILE, TILE * 8, &full[st]);
+                issued++;
+                p++;
+            }
+        }
+        __syncthreads();
+        if (s_total >= 0 && j >= s_total) break;
+        const int st = j % SPT_STAGES;
+        mbar_wait(&full[st], (j / SPT_STAGES) & 1);
+        const int4 mt = meta[st];
+        const double2 *x2 = reinterpret_cast<const double2 *>(sm + st * TILE);
+        const double *vv = g.v + (int64_t)mt.y * SPT_B;
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            const double2 x = x2[tid + 256 * m];
+            const double2 w = *reinterpret_cast<const double2 *>(vv + lc[m]);
+            acc[m] = fma(x.x, w.x, acc[m]);
+            acc[m] = fma(x.y, w.y, acc[m]);
+        }
+        if (mt.z) {
+            // last block of the unit: 8 rows per warp, fixed xor tree per row
+#pragma unroll
+            for (int m = 0; m < 8; m++) {
+                double t = acc[m];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (lane == 0) g.part[(int64_t)mt.x * SPT_B + warp + 8 * m] = t;
+                acc[m] = 0.0;
+            }
+        }
+        __syncthreads();   // stage st may be refilled from the next iteration on
+    }
+}
+
+// w[I*64 + r] = (P0 + P1) + (P2 + P3), P_q = quarter q's partial (0 if the quarter is empty)
+__global__ void k_spmv_fix(const int32_t *rowptr, const double *part, int nb, double *w)
+{
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= (int64_t)nb * SPT_B) return;
+    const int I = (int)(e / SPT_B), r = (int)(e % SPT_B);
+    const int p0 = rowptr[I], len = rowptr[I + 1] - p0;
+    double P[SPT_Q];
+#pragma unroll
+    for (int q = 0; q < SPT_Q; q++) {
+        const bool any = ((q + 1) * len) / SPT_Q > (q * len) / SPT_Q;
+        P[q] = any ? part[((int64_t)I * SPT_Q + q) * SPT_B + r] : 0.0;
+    }
+    w[e] = (P[0] + P[1]) + (P[2] + P[3]);
+}
+
 // single CTA: nrm = sqrt(sum w^2) (fixed order); v = w / nrm
 __global__ void k_normalize(const double *w, int64_t n, double *v)
 {
@@ -173,6 +302,23 @@ __global__ void k_dot(const double *a, const double *b, int64_t n, double *out)
     if (threadIdx.x == 0) *out = sh[0];
 }
 
+static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
+                             const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part)
+{
+    const size_t smem = sizeof(double) * SPT_STAGES * SPT_B * SPT_B + SPT_STAGES * (sizeof(uint64_t) + sizeof(int4));
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
+    k_spmv_tma<<<ctx->sm_count, 256, smem, ctx->stream>>>(g);
+    CKL(ctx);
+    k_spmv_fix<<<cdiv((int64_t)s->nb * SPT_B, 256), 256, 0, ctx->stream>>>(rowptr, part, s->nb, w);
+    CKL(ctx);
+    return SPAMM_OK;
+}
+
 template <int B>
 static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
                  const int32_t *slots, const double *v, double *w, int32_t *ticket)
@@ -190,6 +336,17 @@ static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_
     ctx->launches++;
 }
 
+// SPAMM_SPMV_TMA=0 selects the register-streaming SpMV for b = 64 as well
+static bool spmv_tma_mode()
+{
+    static int m = -1;
+    if (m < 0) {
+        const char *e = getenv("SPAMM_SPMV_TMA");
+        m = (e && *e == '0') ? 0 : 1;
+    }
+    return m == 1;
+}
+
 spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
 {
     const int nb = s->nb;
@@ -199,7 +356,10 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     int32_t *cols = dalloc<int32_t>(ctx, nblk), *slots = dalloc<int32_t>(ctx, nblk);
     double *v = dalloc<double>(ctx, n), *w = dalloc<double>(ctx, n), *c = dalloc<double>(ctx, 1);
     int32_t *tickets = dalloc<int32_t>(ctx, K + 1);   // one per SpMV launch
-    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets) return set_err(ctx, SPAMM_ENOMEM, "power");
+    const bool tma = s->b == 64 && spmv_tma_mode();
+    double *part = tma ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * SPT_B) : nullptr;
+    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets || (tma && !part))
+        return set_err(ctx, SPAMM_ENOMEM, "power");
     CK(cudaMemsetAsync(tickets, 0, sizeof(int32_t) * (K + 1), ctx->stream));
     int nmv = 0;
     cudaStream_t st = ctx->stream;
@@ -212,6 +372,10 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     // (each row is computed by one rank with the single-device kernel: bitwise G-invariant)
     auto mv = [&](const double *x, double *y) -> spamm_status {
         int32_t *tk = tickets + nmv++;
+        if (tma) {
+            ST(spmv_tma(ctx, s, rowptr, cols, slots, x, y, tk, part));
+            return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
+        }
         switch (s->b) {
         case 16: spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk); break;
         case 32: spmv<32>(ctx, s, rowptr, cols, slots, x, y, tk); break;
@@ -238,5 +402,6 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     dev_free(ctx, w, sizeof(double) * n);
     dev_free(ctx, c, sizeof(double));
     dev_free(ctx, tickets, sizeof(int32_t) * (K + 1));
+    dev_free(ctx, part, sizeof(double) * (int64_t)nb * SPT_Q * SPT_B);
     return SPAMM_OK;
 }
