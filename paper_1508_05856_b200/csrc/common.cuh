@@ -14,6 +14,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -197,6 +198,19 @@ spamm_status check_cuda(spamm_ctx ctx, cudaError_t e, const char *what);
     } while (0)
 
 static inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// Per-device, thread-safe one-time kernel configuration (function attributes are
+// per device; contexts may be driven from several host threads).  f() is
+// idempotent, so two threads racing on the first call both running it is harmless.
+template <typename F>
+static inline cudaError_t once_per_device(std::atomic<uint64_t> &done, int device, F &&f)
+{
+    const uint64_t bit = 1ull << (device & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    cudaError_t e = f();
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
 
 // ------------------------------------------------------------ internal API
 // tree.cu

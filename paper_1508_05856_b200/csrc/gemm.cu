@@ -304,13 +304,17 @@ static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
                         2 * QN * sizeof(uint64_t) + QN * sizeof(int4) + RS * 2 * CW * sizeof(double) +
                         RS * sizeof(int);
     auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI, TA>;
-    static int occ = 0;
-    if (!occ) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
-        if (occ < 1) occ = 1;
-    }
+    static std::atomic<uint64_t> configured{0};
+    static std::atomic<int> occ_cache{0};
+    CK(once_per_device(configured, ctx->device, [&]() {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int o = 0;
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, NT, smem);
+        if (e == cudaSuccess) occ_cache.store(o < 1 ? 1 : o);
+        return e;
+    }));
     if (g.nseg == 0) return SPAMM_OK;
+    const int occ = occ_cache.load();
     int grid = ctx->sm_count * occ;
     if (grid > g.nseg) grid = g.nseg;
     kern<<<grid, NT, smem, ctx->stream>>>(g);

@@ -306,11 +306,10 @@ static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, 
                              const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part)
 {
     const size_t smem = sizeof(double) * SPT_STAGES * SPT_B * SPT_B + SPT_STAGES * (sizeof(uint64_t) + sizeof(int4));
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(k_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    static std::atomic<uint64_t> configured{0};
+    CK(once_per_device(configured, ctx->device, [&]() {
+        return cudaFuncSetAttribute(k_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }));
     SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
     k_spmv_tma<<<ctx->sm_count, 256, smem, ctx->stream>>>(g);
     CKL(ctx);
@@ -324,10 +323,12 @@ static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_
                  const int32_t *slots, const double *v, double *w, int32_t *ticket)
 {
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
-    static int occ = 0;
+    static std::atomic<int> occ_cache{0};
+    int occ = occ_cache.load();
     if (!occ) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<B>, 256, 0);
         if (occ < 1) occ = 1;
+        occ_cache.store(occ);
     }
     const int nunits = s->nb * CPR;
     int grid = ctx->sm_count * occ;
@@ -339,12 +340,12 @@ static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_
 // SPAMM_SPMV_TMA=0 selects the register-streaming SpMV for b = 64 as well
 static bool spmv_tma_mode()
 {
-    static int m = -1;
-    if (m < 0) {
+    // function-local static: initialised once, thread-safely (C++11)
+    static const bool m = [] {
         const char *e = getenv("SPAMM_SPMV_TMA");
-        m = (e && *e == '0') ? 0 : 1;
-    }
-    return m == 1;
+        return !(e && *e == '0');
+    }();
+    return m;
 }
 
 spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)

@@ -96,11 +96,10 @@ static spamm_status check_pair(spamm_ctx ctx, spamm_mat A, spamm_mat B, double t
 // +0.5 % step time on C3 from its three extra launches per product, so off by default)
 static int lpt_mode()
 {
-    static int m = -1;
-    if (m < 0) {
+    static const int m = [] {   // initialised once, thread-safely (C++11)
         const char *e = getenv("SPAMM_LPT");
-        m = (e && *e == '1') ? 1 : 0;
-    }
+        return (e && *e == '1') ? 1 : 0;
+    }();
     return m;
 }
 
@@ -110,11 +109,10 @@ static int lpt_mode()
 // construction); mismatches are reported on stderr.
 static int selfcheck_mode()
 {
-    static int m = -1;
-    if (m < 0) {
+    static const int m = [] {   // initialised once, thread-safely (C++11)
         const char *e = getenv("SPAMM_SELFCHECK");
-        m = (e && *e == '1') ? 1 : 0;
-    }
+        return (e && *e == '1') ? 1 : 0;
+    }();
     return m;
 }
 

@@ -42,11 +42,10 @@ spamm_status check_cuda(spamm_ctx ctx, cudaError_t e, const char *what)
 // -1 ints) so a read of memory no kernel wrote shows up as NaN / a bad slot.
 static int poison_mode()
 {
-    static int m = -1;
-    if (m < 0) {
+    static const int m = [] {   // initialised once, thread-safely (C++11)
         const char *e = getenv("SPAMM_POISON");
-        m = (e && *e == '1') ? 1 : 0;
-    }
+        return (e && *e == '1') ? 1 : 0;
+    }();
     return m;
 }
 
