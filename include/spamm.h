@@ -233,6 +233,19 @@ spamm_status spamm_ns_step_single(spamm_ctx ctx, spamm_mat S1, spamm_mat Z, spam
  * outputs Z * c^{-1/2} -> s^{-1/2} and Y = W c^{1/2} -> s^{1/2}. */
 spamm_status spamm_ns_sqrt_single(spamm_ctx ctx, spamm_mat s, double tau, int32_t iters, spamm_mat *Y,
                                   spamm_mat *Z, const spamm_ns_opts *opts);
+/* Regularised product representation of the inverse factor (Eq. product_rep,
+ * P:748-776; reading L21): slices of shifted,
+ * preconditioned residuals, each "effective by one order":
+ *   c = ||s||_2 (power iteration, or scale > 0), S_i = s/c + mu_i I,
+ *   R_0 = S_0, R_i = F^T (x)_tau1 (S_i (x)_tau1 F) for i >= 1,
+ *   Z_i = R_i^{-1/2} by the dual iteration (tau = tau_s = tau0, up to iters steps,
+ *   t_stop as in spamm_ns_opts), F = Z_0, F <- F (x)_tau1 Z_i;
+ *   *G = F / sqrt(c), so that G^T (s + c mu_{m} I) G ~ I.
+ * mu: HOST [nslices], relative shifts, decreasing.  c_out, slice_iters ([nslices]) nullable.
+ * Single device only (EINVAL on a row-partitioned context). */
+spamm_status spamm_regularized_factor(spamm_ctx ctx, spamm_mat s, double tau0, double tau1, const double *mu,
+                                      int32_t nslices, int32_t iters, double t_stop, double scale, spamm_mat *G,
+                                      double *c_out, int32_t *slice_iters);
 /* Scale estimate c ~ ||s||_2: K power steps from 1/sqrt(n) * ones, Rayleigh quotient. */
 spamm_status spamm_power_scale(spamm_ctx ctx, spamm_mat s, int32_t K, double *c);
 /* Y0 = s/c (mu = 0) or (s/c + mu I)/(1+mu). */

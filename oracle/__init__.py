@@ -63,6 +63,7 @@ def lib():
             "or_multiply": (vp, [vp, vp, dbl, vp, i64, P(i64)]),
             "or_copy": (vp, [vp]),
             "or_transpose": (vp, [vp]),
+            "or_regularized_factor": (i32, [vp, dbl, dbl, vp, i32, i32, dbl, dbl, i32, P(vp), P(dbl), vp]),
             "or_multiply_t": (vp, [vp, vp, dbl, vp, i64, P(i64)]),
             "or_ns_sqrt_single": (i32, [vp, dbl, dbl, i32, dbl, i32, dbl, i32, P(vp), P(vp), vp, vp,
                                         P(dbl), P(C.c_int)]),
@@ -269,3 +270,16 @@ def ns_sqrt_single(s: OMat, tau: float, iters: int, tau_s: float | None = None, 
     k = done.value if rc == 0 else done.value + 1
     return dict(Y=OMat(yo.value), Z=OMat(zo.value), t=t[:k], counts=counts.reshape(iters, 3)[:k],
                 c=c.value, rc=rc, iters=k)
+
+
+def regularized_factor(s: OMat, tau0: float, tau1: float, mus, iters: int, t_stop: float = 0.0,
+                       scale: float = 0.0, power_iters: int = 100):
+    """Regularised product representation: returns dict(G, c, slice_iters, rc) with
+    G^T (s + c mu_m I) G ~ I."""
+    mu = np.ascontiguousarray(mus, dtype=np.float64)
+    g = C.c_void_p()
+    c = C.c_double(0)
+    its = np.zeros(len(mu), dtype=np.int64)
+    rc = lib().or_regularized_factor(s.h, tau0, tau1, _ptr(mu), len(mu), iters, t_stop, scale, power_iters,
+                                     C.byref(g), C.byref(c), _ptr(its))
+    return dict(G=OMat(g.value), c=c.value, slice_iters=its, rc=rc)

@@ -456,6 +456,7 @@ omat *or_copy(const omat *m)
  * op 2: y = x * c  ;  op 3: y = x / c  (same as 0; kept for clarity)
  * op 4: H = 1/2 (3 delta - x)  written as 1.5*delta - 0.5*x (exactly equal, the
  *       1/2 scale is exact).  Diagonal blocks absent from x become 1.5 I.
+ * op 8: y = x / c + mu delta   (shifted normalised s, regularised slices)
  * op 6: scaled + stabilised map with alpha = c, eps = mu:
  *       x~ = (1 - 2 eps) x + eps delta   ([0,1] -> [eps, 1-eps], "prior to the logistic")
  *       H  = h_alpha[x~] = sqrt(alpha)/2 (3 delta - alpha x~). */
@@ -463,7 +464,7 @@ static onode *map_rec(const onode *p, int lev, int L, int b, int I, int J, int o
                       double c, double mu)
 {
     int diag = (I == J);
-    int fill = (op == 1 || op == 4 || op == 5 || op == 6);   /* ops that create absent diagonal blocks */
+    int fill = (op == 1 || op == 4 || op == 5 || op == 6 || op == 8);   /* ops that create absent diagonal blocks */
     if (!p && !(diag && fill)) return NULL;
     if (!p && lev < L && diag && fill) {
         onode *q = new_interior();
@@ -489,6 +490,7 @@ static onode *map_rec(const onode *p, int lev, int L, int b, int I, int J, int o
                     y = (sqrt(c) / 2.0) * (3.0 * d - c * xt);
                     break;
                 }
+                case 8: y = x / c + mu * d; break;
                 default: y = 1.5 * d - 0.5 * x; break;
                 }
                 q->blk[(size_t)r * b + s] = y;
@@ -706,5 +708,53 @@ int or_ns_sqrt_single(const omat *s, double tau, double tau_s, int iters, double
     *Yout = map_mat(W, 2, f, 0.0);
     *Zout = map_mat(Z, 0, f, 0.0);
     or_free(Z); or_free(W); or_free(X); or_free(S1);
+    return rc;
+}
+
+/* ------------------------------------------ regularised product representation
+ * Eq. product_rep (reading L21): slices of shifted, preconditioned
+ * residuals, each solved by the dual iteration at the slice precision tau0, chained
+ * by products at tau1:
+ *   c = ||s||_2 ;  S_i = s/c + mu_i I  (mu_0 > mu_1 > ... , relative shifts)
+ *   R_0 = S_0,  R_i = F^T (x)_tau1 (S_i (x)_tau1 F)  (i >= 1)
+ *   Z_i = R_i^{-1/2} (dual NS, tau = tau_s = tau0, own scale by power iteration)
+ *   F = Z_0,  F <- F (x)_tau1 Z_i
+ * Output G = F / sqrt(c): G^T (s + c mu_m I) G ~ I (an inverse factor). */
+int or_regularized_factor(const omat *s, double tau0, double tau1, const double *mu, int nslices, int iters,
+                          double t_stop, double scale, int power_iters, omat **Gout, double *c_used,
+                          int64_t *slice_iters)
+{
+    double c = scale > 0.0 ? scale : or_power_scale(s, power_iters);
+    if (c_used) *c_used = c;
+    omat *F = NULL;
+    int rc = 0;
+    for (int i = 0; i < nslices && !rc; i++) {
+        omat *Si = map_mat(s, 8, c, mu[i]);
+        omat *R;
+        if (!F) {
+            R = Si;
+        } else {
+            omat *W = or_multiply(Si, F, tau1, NULL, 0, NULL);
+            R = or_multiply_t(F, W, tau1, NULL, 0, NULL);
+            or_free(W);
+            or_free(Si);
+        }
+        omat *Y, *Z;
+        int done = 0;
+        rc = or_ns_sqrt(R, tau0, tau0, iters, 0.0, power_iters, 0.0, t_stop, 0, &Y, &Z, NULL, NULL, NULL, &done);
+        if (slice_iters) slice_iters[i] = done;
+        or_free(R);
+        or_free(Y);
+        if (!F) {
+            F = Z;
+        } else {
+            omat *Fn = or_multiply(F, Z, tau1, NULL, 0, NULL);
+            or_free(F);
+            or_free(Z);
+            F = Fn;
+        }
+    }
+    *Gout = map_mat(F, 0, sqrt(c), 0.0);
+    or_free(F);
     return rc;
 }

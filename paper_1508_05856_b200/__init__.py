@@ -26,7 +26,7 @@ __all__ = [
     "spamm_ctx_create", "spamm_ctx_destroy", "spamm_last_error", "spamm_kernel_launches",
     "spamm_build_tree", "spamm_build_tree_blocks", "spamm_mat_free", "spamm_mat_info",
     "spamm_norm", "spamm_to_dense", "spamm_level_norms2", "spamm_get_blocks",
-    "spamm_multiply", "spamm_multiply_t", "spamm_task_distance_hist", "spamm_ns_step_single", "spamm_ns_sqrt_single", "spamm_export_tasks", "spamm_ns_step", "spamm_ns_step_map", "spamm_power_scale",
+    "spamm_multiply", "spamm_multiply_t", "spamm_task_distance_hist", "spamm_regularized_factor", "spamm_ns_step_single", "spamm_ns_sqrt_single", "spamm_export_tasks", "spamm_ns_step", "spamm_ns_step_map", "spamm_power_scale",
     "spamm_ns_y0", "spamm_identity", "spamm_ns_sqrt", "spamm_scale",
     "spamm_export_blocks", "spamm_profile_enable", "spamm_profile_read", "spamm_peak_dmma",
     "Comm", "spamm_comm_nccl_unique_id", "spamm_comm_nccl_create", "spamm_comm_local_group",
@@ -109,6 +109,7 @@ def load():
         "spamm_export_tasks": (i32, [vp, vp, i64, P(i64)]),
         "spamm_multiply_t": (i32, [vp, vp, vp, dbl, P(vp), P(spamm_stats)]),
         "spamm_task_distance_hist": (i32, [vp, vp, i32]),
+        "spamm_regularized_factor": (i32, [vp, vp, dbl, dbl, vp, i32, i32, dbl, dbl, P(vp), P(dbl), vp]),
         "spamm_ns_step_single": (i32, [vp, vp, vp, vp, dbl, dbl, i32, P(vp), P(vp), P(vp), P(dbl), vp, vp]),
         "spamm_ns_sqrt_single": (i32, [vp, vp, dbl, i32, P(vp), P(vp), P(spamm_ns_opts)]),
         "spamm_ns_step": (i32, [vp, vp, vp, dbl, dbl, P(vp), P(vp), P(vp), P(dbl), vp]),
@@ -473,6 +474,19 @@ def spamm_task_distance_hist(ctx: Ctx, nbins: int) -> np.ndarray:
     out = np.zeros(nbins, dtype=np.int64)
     ctx.check(load().spamm_task_distance_hist(ctx.h, _ptr(out), int(nbins)))
     return out
+
+
+def spamm_regularized_factor(ctx: Ctx, s: Mat, tau0: float, tau1: float, mus, iters: int,
+                             t_stop: float = 0.0, scale: float = 0.0):
+    """Regularised product representation: dict(G, c, slice_iters) with
+    G^T (s + c mu_m I) G ~ I."""
+    mu = np.ascontiguousarray(mus, dtype=np.float64)
+    g = C.c_void_p()
+    c = C.c_double()
+    its = np.zeros(len(mu), dtype=np.int32)
+    ctx.check(load().spamm_regularized_factor(ctx.h, s.h, float(tau0), float(tau1), _ptr(mu), len(mu), int(iters),
+                                              float(t_stop), float(scale), C.byref(g), C.byref(c), _ptr(its)))
+    return dict(G=Mat(ctx, g), c=c.value, slice_iters=its)
 
 
 def spamm_export_tasks(ctx: Ctx) -> np.ndarray:

@@ -676,3 +676,66 @@ extern "C" spamm_status spamm_ns_sqrt_single(spamm_ctx ctx, spamm_mat s, double 
     }
     return st2;
 }
+
+// ------------------------------------- regularised product representation
+// Eq. product_rep (reading L21), SURVEY.md §8(f) f3:
+//   c = ||s||_2, S_i = s/c + mu_i I, R_0 = S_0, R_i = F^T (x)_tau1 (S_i (x)_tau1 F),
+//   Z_i = R_i^{-1/2} (dual iteration at tau = tau_s = tau0), F = Z_0, F <- F (x)_tau1 Z_i;
+//   G = F / sqrt(c) with G^T (s + c mu_m I) G ~ I.  Single device (uses F^T).
+extern "C" spamm_status spamm_regularized_factor(spamm_ctx ctx, spamm_mat s, double tau0, double tau1,
+                                                 const double *mu, int32_t nslices, int32_t iters, double t_stop,
+                                                 double scale, spamm_mat *G, double *c_out, int32_t *slice_iters)
+{
+    if (!ctx || !s || !mu || !G || nslices < 1 || iters < 1) return set_err(ctx, SPAMM_EINVAL, "bad argument");
+    if (!(tau0 >= 0.0) || !(tau1 >= 0.0)) return set_err(ctx, SPAMM_EINVAL, "tau must be >= 0");
+    if (s->dist) return set_err(ctx, SPAMM_EINVAL, "regularised slices need F^T: not on a row-partitioned context");
+    double c = scale;
+    if (!(c > 0.0)) ST(power_scale(ctx, s, 100, &c));
+    if (c_out) *c_out = c;
+    spamm_mat F = nullptr;
+    spamm_status st = SPAMM_OK;
+    for (int i = 0; i < nslices && !st; i++) {
+        spamm_mat Si = nullptr, R = nullptr;
+        st = mat_map(ctx, s, 8, c, mu[i], &Si);
+        if (st) break;
+        if (!F) {
+            R = Si;
+        } else {
+            spamm_mat W = nullptr;
+            st = product(ctx, ctx->cw[0], Si, F, tau1, EPI_STORE, nullptr, &W);
+            if (!st) st = product(ctx, ctx->cw[1], F, W, tau1, EPI_STORE, nullptr, &R, 1);
+            spamm_mat_free(W);
+            spamm_mat_free(Si);
+            if (st) break;
+        }
+        spamm_ns_opts o{};
+        o.tau_s = tau0;
+        o.power_iters = 100;
+        o.t_stop = t_stop;
+        int32_t done = 0;
+        o.iters_done = &done;
+        spamm_mat Y = nullptr, Z = nullptr;
+        st = spamm_ns_sqrt(ctx, R, tau0, iters, &Y, &Z, &o);
+        if (slice_iters) slice_iters[i] = done;
+        spamm_mat_free(R);
+        spamm_mat_free(Y);
+        if (st) {
+            spamm_mat_free(Z);
+            break;
+        }
+        if (!F) {
+            F = Z;
+        } else {
+            spamm_mat Fn = nullptr;
+            st = product(ctx, ctx->cw[2], F, Z, tau1, EPI_STORE, nullptr, &Fn);
+            spamm_mat_free(Z);
+            if (!st) {
+                spamm_mat_free(F);
+                F = Fn;
+            }
+        }
+    }
+    if (!st) st = mat_map(ctx, F, 0, std::sqrt(c), 0.0, G);
+    spamm_mat_free(F);
+    return st;
+}

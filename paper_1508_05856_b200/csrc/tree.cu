@@ -462,7 +462,8 @@ extern "C" spamm_status spamm_build_tree_blocks(spamm_ctx ctx, int64_t n, int32_
 // --------------------------------------------------------------- maps
 // op 0: y = x / c ; op 1: y = (x / c + mu delta) / (1 + mu) ; op 2: y = x * c ;
 // op 4: y = 1.5 delta - 0.5 x (= 1/2 (3I - X)) ; op 5: y = delta (identity) ;
-// op 7: y = x (copy).  Same pattern as src, plus the diagonal for ops 1, 4, 5, 7
+// op 7: y = x (copy) ; op 8: y = x / c + mu delta (shifted normalised s, regularised
+// slices).  Same pattern as src, plus the diagonal for ops 1, 4, 5, 7, 8
 // (op 7 adds absent diagonal blocks as zeros, for the scaled map that follows).
 // Vectorised map over one stored block per CTA (double2 in the pool layout) with
 // the block's squared norm fused in (thread partials in element order, then a
@@ -491,6 +492,7 @@ __global__ void __launch_bounds__(256) k_map2(const double *src, const int32_t *
         case 2: y0 = x.x * c; y1 = x.y * c; break;
         case 4: y0 = 1.5 * dl0 - 0.5 * x.x; y1 = 1.5 * dl1 - 0.5 * x.y; break;
         case 7: y0 = x.x; y1 = x.y; break;
+        case 8: y0 = x.x / c + mu * dl0; y1 = x.y / c + mu * dl1; break;
         default: y0 = dl0; y1 = dl1; break;
         }
         d2[p] = make_double2(y0, y1);
@@ -511,7 +513,7 @@ __global__ void __launch_bounds__(256) k_map2(const double *src, const int32_t *
 
 spamm_status mat_map(spamm_ctx ctx, spamm_mat src, int op, double c, double mu, spamm_mat *out)
 {
-    bool fill = (op == 1 || op == 4 || op == 5 || op == 7);
+    bool fill = (op == 1 || op == 4 || op == 5 || op == 7 || op == 8);
     int64_t cap = src->nblk + (fill ? src->nb : 0);
     spamm_mat m;
     ST(mat_new(ctx, src->n, src->b, cap, &m));
@@ -533,7 +535,8 @@ spamm_status mat_map(spamm_ctx ctx, spamm_mat src, int op, double c, double mu, 
         m->nblk = src->nblk;
         if (fill) {
             // absent diagonal blocks: x = 0 => op 1 gives mu/(1+mu) I, op 4 1.5 I, op 5 I, op 7 0
-            double dv = (op == 5) ? 1.0 : (op == 4) ? 1.5 : (op == 7) ? 0.0 : (0.0 / c + mu * 1.0) / (1.0 + mu);
+            double dv = (op == 5) ? 1.0 : (op == 4) ? 1.5 : (op == 7) ? 0.0 : (op == 8) ? mu
+                      : (0.0 / c + mu * 1.0) / (1.0 + mu);
             int64_t h = 0;
             st = diag_append(ctx, m, m->nblk, dv, &h);
             if (st) break;

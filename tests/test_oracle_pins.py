@@ -495,3 +495,46 @@ def test_single_channel_diagonal_scalar_map():
         x = z * (lam * z)
     np.testing.assert_allclose(np.diag(r["Z"].to_dense()), z, rtol=1e-15)
     assert r["counts"].shape == (12, 3)
+
+
+# ------------------------------------- regularised product representation (§8(f) f3)
+def _ill_conditioned(n, kappa, seed):
+    g = _rng(seed).standard_normal((n, n)) * np.exp(-0.05 * np.abs(np.subtract.outer(np.arange(n), np.arange(n))))
+    _, V = np.linalg.eigh(g @ g.T)
+    w = np.geomspace(1.0 / kappa, 1.0, n)
+    s = (V * w) @ V.T
+    return 0.5 * (s + s.T)
+
+
+def test_regularized_factor_tau0_inverse_factor():
+    """P:748-776 at tau0 = tau1 = 0: G^T (s + c mu_m I) G = I; one slice is the inverse square
+    root (s + c mu_0 I)^{-1/2} of the shifted matrix (the 'MAYEBOO' preconditioner)."""
+    n, b = 128, 16
+    s = _ill_conditioned(n, 1e6, 21)
+    S = O.OMat.from_dense(s, b)
+    mus = [1e-1, 1e-2, 1e-3]
+    r = O.regularized_factor(S, 0.0, 0.0, mus, 60, t_stop=1e-13)
+    G, c = r["G"].to_dense(), r["c"]
+    sm = s + c * mus[-1] * np.eye(n)
+    assert np.linalg.norm(G.T @ sm @ G - np.eye(n)) / np.sqrt(n) <= 1e-11
+    r1 = O.regularized_factor(S, 0.0, 0.0, mus[:1], 60, t_stop=1e-13)
+    ref = _eig_pow(s + r1["c"] * mus[0] * np.eye(n), -0.5)
+    assert np.linalg.norm(r1["G"].to_dense() - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+def test_regularized_slices_effective_by_one_order():
+    """Each residual R_i = F^T (s/c + mu_i I) F is 'effective by one order': its
+    condition number is ~ mu_{i-1}/mu_i = 10, whatever kappa(s) (here 1e6), so every slice
+    solves a well-conditioned problem; checked at tau = 0 with the exact eigenvalues."""
+    n, b = 128, 16
+    s = _ill_conditioned(n, 1e6, 22)
+    S = O.OMat.from_dense(s, b)
+    c = O.power_scale(S)
+    mus = [1e-1, 1e-2, 1e-3, 1e-4]
+    for i in range(1, len(mus)):
+        F = O.regularized_factor(S, 0.0, 0.0, mus[:i], 60, t_stop=1e-13, scale=c)["G"].to_dense() * np.sqrt(c)
+        R = F.T @ (s / c + mus[i] * np.eye(n)) @ F
+        w = np.linalg.eigvalsh(0.5 * (R + R.T))
+        assert w.max() / w.min() <= 1.05 * mus[i - 1] / mus[i]
+    ws = np.linalg.eigvalsh(s / c + mus[-1] * np.eye(n))
+    assert ws.max() / ws.min() > 5e3           # the unsliced problem is far worse conditioned
