@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
     __shared__ int4 s_excl;
     // after a capacity overflow the truncated level's group indices point past the
     // arrays: skip the rest of the query (the host grows the workspace and re-runs)
-    if (*(volatile int32_t *)&cnt[CNT_OVERFLOW]) return;
+    if (__ldcg(&cnt[CNT_OVERFLOW])) return;   // written by an earlier launch: a plain L2 load
     const int n = clamp_n(cnt, l, g.cap);
     const double T = cull_T(g);
     const double *an = g.a_n2 + pyr_off(l + 1), *bn = g.b_n2 + pyr_off(l + 1);
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, in
 {
     __shared__ V1 sw[CT / 32];
     __shared__ int s_tile, s_excl;
-    if (*(volatile int32_t *)&cnt[CNT_OVERFLOW]) return;
+    if (__ldcg(&cnt[CNT_OVERFLOW])) return;   // written by an earlier launch: a plain L2 load
     const int n = clamp_n(cnt, L, cap);
     int tile;
     while ((tile = next_tile(st.ticket, n, CT * CI, &s_tile)) >= 0) {
