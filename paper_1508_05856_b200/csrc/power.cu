@@ -149,23 +149,33 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
 // each block (consecutive lanes read consecutive chunks: conflict-free) and keeps
 // 8 row accumulators across the unit's blocks.  Each unit writes its 64 partial row
 // sums; k_spmv_fix adds the 4 quarters in a fixed order (deterministic).
-constexpr int SPT_STAGES = 6, SPT_Q = 4, SPT_B = 64;
+constexpr int SPT_Q = 4;                       // work unit = a quarter of a block row
+// stages of the ring per leaf size: 6 x 32 KiB (b=64), 16 x 8 KiB (b=32), 32 x 2 KiB (b=16)
+template <int B> struct SptCfg {
+    static constexpr int STAGES = B == 64 ? 6 : B == 32 ? 16 : 32;
+    static constexpr int LPR = B / 2;           // lanes (double2 chunks) per block row
+    static constexpr int N2 = B * B / 2;        // double2 per block
+    static constexpr int M = (N2 + 255) / 256;  // double2 per thread per block (256 threads)
+    static constexpr int RPW = 32 / LPR;        // block rows per warp per m
+};
 
 struct SpmvTmaArgs {
     const double *pool;
     const int32_t *rowptr, *cols, *slots;
     const double *v;
-    double *part;       // [nb * SPT_Q * 64]
+    double *part;       // [nb * SPT_Q * b]
     int32_t *ticket;
     int nunits;         // nb * SPT_Q
 };
 
+template <int B>
 __global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
 {
-    constexpr int TILE = SPT_B * SPT_B;
+    using Cf = SptCfg<B>;
+    constexpr int TILE = B * B, STAGES = Cf::STAGES, LPR = Cf::LPR, M = Cf::M, RPW = Cf::RPW, N2 = Cf::N2;
     extern __shared__ __align__(1024) double sm[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(sm + SPT_STAGES * TILE);
-    int4 *meta = reinterpret_cast<int4 *>(full + SPT_STAGES);   // {unit, column block, last, -}
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + STAGES * TILE);
+    int4 *meta = reinterpret_cast<int4 *>(full + STAGES);   // {unit, column block, last, -}
     __shared__ int s_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // issuer state (thread 0); the unit's slot / column indices are fetched in one
@@ -175,22 +185,25 @@ __global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
     int us[UCH], uc[UCH];
     bool done = false;
     if (tid == 0) {
-        for (int st = 0; st < SPT_STAGES; st++) mbar_init(&full[st], 1);
+        for (int st = 0; st < STAGES; st++) mbar_init(&full[st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         s_total = -1;
     }
     __syncthreads();
-    double acc[8];
+    // thread tid owns double2 chunk q = tid + 256 m of each block: block row
+    // q / LPR, chunk q % LPR (consecutive lanes, consecutive 16 B: conflict-free)
+    double acc[M];
+    int lc[M];
 #pragma unroll
-    for (int m = 0; m < 8; m++) acc[m] = 0.0;
-    // logical column pairs of this thread's chunk in rows warp + 8m (pool swizzle)
-    int lc[8];
-#pragma unroll
-    for (int m = 0; m < 8; m++) lc[m] = (lane ^ swz(warp + 8 * m)) << 1;
+    for (int m = 0; m < M; m++) {
+        const int q = tid + 256 * m, r = q / LPR;
+        acc[m] = 0.0;
+        lc[m] = ((q % LPR) ^ swz(r)) << 1;   // logical column pair (pool swizzle)
+    }
     for (int j = 0;; j++) {
         if (tid == 0) {
             // keep the ring full: blocks j .. j + STAGES - 1 in flight
-            while (!done && issued < j + SPT_STAGES) {
+            while (!done && issued < j + STAGES) {
                 if (p == pend) {
                     unit = atomicAdd(g.ticket, 1);
                     if (unit >= g.nunits) {
@@ -213,7 +226,7 @@ __global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
                         uc[i] = p + i < pend ? __ldg(g.cols + p + i) : 0;
                     }
                 }
-                const int st = issued % SPT_STAGES;
+                const int st = issued % STAGES;
                 meta[st] = make_int4(unit, uc[p - ubase], p + 1 == pend, 0);
                 mbar_expect_tx(&full[st], TILE * 8);
                 bulk_g2s(sm + st * TILE, g.pool + (int64_t)us[p - ubase] * TILE, TILE * 8, &full[st]);
@@ -223,26 +236,29 @@ __global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
         }
         __syncthreads();
         if (s_total >= 0 && j >= s_total) break;
-        const int st = j % SPT_STAGES;
-        mbar_wait(&full[st], (j / SPT_STAGES) & 1);
+        const int st = j % STAGES;
+        mbar_wait(&full[st], (j / STAGES) & 1);
         const int4 mt = meta[st];
         const double2 *x2 = reinterpret_cast<const double2 *>(sm + st * TILE);
-        const double *vv = g.v + (int64_t)mt.y * SPT_B;
+        const double *vv = g.v + (int64_t)mt.y * B;
 #pragma unroll
-        for (int m = 0; m < 8; m++) {
+        for (int m = 0; m < M; m++) {
+            if (tid + 256 * m >= N2) break;      // b = 16: warps 4..7 idle (warp-uniform)
             const double2 x = x2[tid + 256 * m];
             const double2 w = *reinterpret_cast<const double2 *>(vv + lc[m]);
             acc[m] = fma(x.x, w.x, acc[m]);
             acc[m] = fma(x.y, w.y, acc[m]);
         }
         if (mt.z) {
-            // last block of the unit: 8 rows per warp, fixed xor tree per row
+            // last block of the unit: each block row's LPR lanes reduce with a fixed xor tree
 #pragma unroll
-            for (int m = 0; m < 8; m++) {
+            for (int m = 0; m < M; m++) {
+                if (tid + 256 * m >= N2) break;
                 double t = acc[m];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                if (lane == 0) g.part[(int64_t)mt.x * SPT_B + warp + 8 * m] = t;
+                for (int o = LPR / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (lane % LPR == 0)
+                    g.part[(int64_t)mt.x * B + (warp * RPW + lane / LPR) + (256 / LPR) * m] = t;
                 acc[m] = 0.0;
             }
         }
@@ -250,18 +266,18 @@ __global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
     }
 }
 
-// w[I*64 + r] = (P0 + P1) + (P2 + P3), P_q = quarter q's partial (0 if the quarter is empty)
-__global__ void k_spmv_fix(const int32_t *rowptr, const double *part, int nb, double *w)
+// w[I*b + r] = (P0 + P1) + (P2 + P3), P_q = quarter q's partial (0 if the quarter is empty)
+__global__ void k_spmv_fix(const int32_t *rowptr, const double *part, int nb, int b, double *w)
 {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= (int64_t)nb * SPT_B) return;
-    const int I = (int)(e / SPT_B), r = (int)(e % SPT_B);
+    if (e >= (int64_t)nb * b) return;
+    const int I = (int)(e / b), r = (int)(e % b);
     const int p0 = rowptr[I], len = rowptr[I + 1] - p0;
     double P[SPT_Q];
 #pragma unroll
     for (int q = 0; q < SPT_Q; q++) {
         const bool any = ((q + 1) * len) / SPT_Q > (q * len) / SPT_Q;
-        P[q] = any ? part[((int64_t)I * SPT_Q + q) * SPT_B + r] : 0.0;
+        P[q] = any ? part[((int64_t)I * SPT_Q + q) * b + r] : 0.0;
     }
     w[e] = (P[0] + P[1]) + (P[2] + P[3]);
 }
@@ -302,18 +318,20 @@ __global__ void k_dot(const double *a, const double *b, int64_t n, double *out)
     if (threadIdx.x == 0) *out = sh[0];
 }
 
+template <int B>
 static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
                              const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part)
 {
-    const size_t smem = sizeof(double) * SPT_STAGES * SPT_B * SPT_B + SPT_STAGES * (sizeof(uint64_t) + sizeof(int4));
+    constexpr int STAGES = SptCfg<B>::STAGES;
+    const size_t smem = sizeof(double) * STAGES * B * B + STAGES * (sizeof(uint64_t) + sizeof(int4));
     static std::atomic<uint64_t> configured{0};
     CK(once_per_device(configured, ctx->device, [&]() {
-        return cudaFuncSetAttribute(k_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return cudaFuncSetAttribute(k_spmv_tma<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }));
     SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
-    k_spmv_tma<<<ctx->sm_count, 256, smem, ctx->stream>>>(g);
+    k_spmv_tma<B><<<ctx->sm_count, 256, smem, ctx->stream>>>(g);
     CKL(ctx);
-    k_spmv_fix<<<cdiv((int64_t)s->nb * SPT_B, 256), 256, 0, ctx->stream>>>(rowptr, part, s->nb, w);
+    k_spmv_fix<<<cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream>>>(rowptr, part, s->nb, B, w);
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -337,7 +355,7 @@ static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_
     ctx->launches++;
 }
 
-// SPAMM_SPMV_TMA=0 selects the register-streaming SpMV for b = 64 as well
+// SPAMM_SPMV_TMA=0 selects the register-streaming SpMV (k_spmv) instead
 static bool spmv_tma_mode()
 {
     // function-local static: initialised once, thread-safely (C++11)
@@ -357,8 +375,10 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     int32_t *cols = dalloc<int32_t>(ctx, nblk), *slots = dalloc<int32_t>(ctx, nblk);
     double *v = dalloc<double>(ctx, n), *w = dalloc<double>(ctx, n), *c = dalloc<double>(ctx, 1);
     int32_t *tickets = dalloc<int32_t>(ctx, K + 1);   // one per SpMV launch
-    const bool tma = s->b == 64 && spmv_tma_mode();
-    double *part = tma ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * SPT_B) : nullptr;
+    // TMA staging pays for 32 KiB blocks; for b = 16 / 32 the per-block barrier of the
+    // ring dominates (C2 setup 4.3 -> 8.4 ms measured), so those keep the register kernel
+    const bool tma = spmv_tma_mode() && s->b == 64;
+    double *part = tma ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * s->b) : nullptr;
     if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets || (tma && !part))
         return set_err(ctx, SPAMM_ENOMEM, "power");
     CK(cudaMemsetAsync(tickets, 0, sizeof(int32_t) * (K + 1), ctx->stream));
@@ -374,7 +394,11 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     auto mv = [&](const double *x, double *y) -> spamm_status {
         int32_t *tk = tickets + nmv++;
         if (tma) {
-            ST(spmv_tma(ctx, s, rowptr, cols, slots, x, y, tk, part));
+            switch (s->b) {
+            case 16: ST(spmv_tma<16>(ctx, s, rowptr, cols, slots, x, y, tk, part)); break;
+            case 32: ST(spmv_tma<32>(ctx, s, rowptr, cols, slots, x, y, tk, part)); break;
+            default: ST(spmv_tma<64>(ctx, s, rowptr, cols, slots, x, y, tk, part)); break;
+            }
             return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
         }
         switch (s->b) {
@@ -403,6 +427,6 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     dev_free(ctx, w, sizeof(double) * n);
     dev_free(ctx, c, sizeof(double));
     dev_free(ctx, tickets, sizeof(int32_t) * (K + 1));
-    dev_free(ctx, part, sizeof(double) * (int64_t)nb * SPT_Q * SPT_B);
+    dev_free(ctx, part, sizeof(double) * (int64_t)nb * SPT_Q * s->b);
     return SPAMM_OK;
 }
