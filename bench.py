@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3", choices=sorted(si.CONFIGS))
+    # C5 is the configuration BASELINE.json partitions across 1/2/4/8 GPUs (BJ:11) and
+    # it fits one B200; C3 (BJ:9) is the other throughput config (--config C3)
+    ap.add_argument("--config", default="C5", choices=sorted(si.CONFIGS))
     ap.add_argument("--tau", type=float, default=None, help="override tau (C4 sweep)")
     ap.add_argument("--iters", type=int, default=None, help="override NS iterations")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
