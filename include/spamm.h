@@ -70,6 +70,8 @@ typedef struct {
     int64_t level_survivors[24];/* survivors per quadtree level (index = level)      */
     double flops;               /* 2 b^3 |S|                                         */
     int64_t halo_blocks;        /* row partition: remote right-operand blocks fetched */
+    int64_t local_segments;     /* row partition: segments needing no remote block (run
+                                   while the halo is exchanged)                        */
 } spamm_stats;
 
 /* Options of spamm_ns_sqrt (NULL => defaults).  History buffers are HOST memory. */

@@ -234,6 +234,7 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
         prof_end(ctx, px);
         ctx->stream = main_s;
         cw->stats.halo_blocks = nhalo;
+        cw->stats.local_segments = nloc;
     }
     if (!st) {
         CK(cudaEventRecord(ctx->ev[1], comm_s));

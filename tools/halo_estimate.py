@@ -35,7 +35,8 @@ def fn(rank, comm):
     S = sp.spamm_build_tree_blocks(ctx, cfg.n, b, *payload)
     r = sp.spamm_ns_sqrt(ctx, S, cfg.tau, a.iters, tau_s=cfg.tau * cfg.tau_s_factor, mu=cfg.mu,
                          t_stop=cfg.t_stop)
-    out = np.array([[[p["tasks"], p["halo_blocks"]] for p in k] for k in r["stats"]])
+    out = np.array([[[p["tasks"], p["halo_blocks"], p["local_segments"], p["segments"]] for p in k]
+                     for k in r["stats"]])
     for m in (S, r["Y"], r["Z"]):
         m.free()
     ctx.close()
@@ -44,6 +45,7 @@ def fn(rank, comm):
 
 res = np.stack(D.run_rank_threads(G, fn))          # [G, k, 3, 2]
 tasks, halo = res[..., 0].astype(float), res[..., 1].astype(float)
+loc_frac = res[..., 2].sum() / max(res[..., 3].sum(), 1)
 flop_task, byte_blk = 2.0 * b ** 3, 8.0 * b * b
 t_gemm = tasks * flop_task / (a.gemm_tflops * 1e12)       # per rank, per product
 t_halo = halo * byte_blk / (a.nvlink_gbs * 1e9)
@@ -58,6 +60,7 @@ tot_gemm = t_gemm.sum(axis=(1, 2)).max()
 tot_serial = (t_gemm + t_halo).sum(axis=(1, 2)).max()
 tot_overlap = np.maximum(t_gemm, t_halo).sum(axis=(1, 2)).max()
 one = tasks.sum() * flop_task / (a.gemm_tflops * 1e12)
+print(f"all-local segments (run while the halo is exchanged): {100 * loc_frac:.1f} % of all segments")
 print(f"run GEMM time 1 GPU {one * 1e3:.1f} ms; G={G}: max-rank GEMM {tot_gemm * 1e3:.1f} ms, "
       f"+ exchange serial {tot_serial * 1e3:.1f} ms, overlapped {tot_overlap * 1e3:.1f} ms -> "
       f"efficiency {one / G / tot_serial:.2f} (serial) .. {one / G / tot_overlap:.2f} (perfect overlap)")
