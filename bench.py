@@ -57,6 +57,8 @@ def parse():
                     help="dual (north_star, P:383-389) or single-channel (P:398-402) iteration")
     ap.add_argument("--tau-s-factor", type=float, default=None, help="override tau_s / tau")
     ap.add_argument("--t-stop", type=float, default=None, help="override the convergence exit |t_k| <= t_stop")
+    ap.add_argument("--allocator", default="torch", choices=["torch", "cuda"],
+                    help="device memory: PyTorch's caching allocator (callbacks) or cudaMallocAsync")
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced"],
                     help="row partition for --gpus > 1 (balanced: on s (x) s per-row task counts)")
     ap.add_argument("--dist-world1", action="store_true",
@@ -235,7 +237,7 @@ def run_ours(args):
             row_start = D.equal_partition(nb, ws)
         rows = (row_start[rank], row_start[rank + 1])
     kind, payload = si.make_input(cfg, rows=rows if comm is not None else None)
-    ctx = sp.spamm_ctx_create(local)
+    ctx = sp.spamm_ctx_create(local, torch_allocator=args.allocator == "torch")
     if comm is not None:
         sp.spamm_ctx_set_comm(ctx, comm, row_start)
     stream = ctx.stream

@@ -45,6 +45,16 @@ extern "C" spamm_status spamm_ctx_create(int device, void *cuda_stream, const sp
     if (allocator && allocator->alloc && allocator->free) {
         ctx->alloc = *allocator;
         ctx->has_alloc = true;
+    } else {
+        // stream-ordered allocator: keep freed memory in the pool across synchronisations
+        // (the default release threshold of 0 returns it to the driver at every sync, and
+        // the next cudaMallocAsync pays for a fresh mapping: C3 ran 8x slower that way)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
     }
     ctx->dscratch = dalloc<double>(ctx, 64);
     ctx->iscratch = dalloc<int64_t>(ctx, 64);
