@@ -253,6 +253,7 @@ struct Cull {
     int L = 0, l0 = 0, b = 0;
     int64_t ntasks = 0, nsegs = 0;  // host copies after cull_sync
     int64_t hint = 0;             // capacity hint for the next use
+    double alpha = 1.0;           // EPI_STORE output scale of the next GEMM (fused unscale)
     spamm_stats stats{};
 };
 // Enqueue the query, synchronise once to read the counts, and grow + re-run

@@ -35,6 +35,7 @@ struct GemmArgs {
     double *c_leaf_n2;
     double *trace_part;
     int32_t *ticket;   // dynamic segment scheduler (zeroed before the launch)
+    double alpha;      // EPI_STORE: C = alpha (A (x) B) (the final unscale of the NS run, fused)
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b)
@@ -247,6 +248,10 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
             for (int nf = 0; nf < NF; nf++) {
                 const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
                 double y0 = acc[mf][nf][0], y1 = acc[mf][nf][1];
+                if (EPI == EPI_STORE) {
+                    y0 *= g.alpha;   // alpha = 1 (exact) except for the fused final unscale
+                    y1 *= g.alpha;
+                }
                 if (EPI != EPI_STORE) {
                     if (diag && r == c) tr += y0;
                     if (diag && r == c + 1) tr += y1;
@@ -340,7 +345,7 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
     if (nseg < 0) nseg = cw->nsegs;
     GemmArgs g{A->pool, B->pool, b_halo, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
                (int)nseg, seg_order, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
-               cw->counters + CNT_GEMM_TICKET + ticket};
+               cw->counters + CNT_GEMM_TICKET + ticket, cw->alpha};
     if (transA) {
         if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 1>(ctx, A->b, g);
         if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 1>(ctx, A->b, g);

@@ -267,8 +267,9 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
 
 // product with a given workspace and epilogue; C allocated here
 static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
-                            double *trace_part, spamm_mat *C, int transA = 0)
+                            double *trace_part, spamm_mat *C, int transA = 0, double alpha = 1.0)
 {
+    cw->alpha = alpha;
     if (transA && A->dist)
         return set_err(ctx, SPAMM_EINVAL, "A^T (x) B is not available on a row-partitioned context");
     if (A->dist != B->dist || A->r0 != B->r0 || A->r1 != B->r1)
@@ -362,9 +363,20 @@ extern "C" spamm_status spamm_export_tasks(spamm_ctx ctx, int32_t *ikj, int64_t 
     return cull_export(ctx, ctx->last, ikj, cap, n);
 }
 
-extern "C" spamm_status spamm_ns_step_map(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
-                                          int32_t map, spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
-                                          double *t_k, spamm_stats stats[3], double *alpha_eps)
+// The final unscale of spamm_ns_sqrt (Y * f, Z / f, f = sqrt(c (1+mu))) is fused into the
+// Y' and Z' GEMM epilogues of the last step (saving a read + write pass over both results).
+// The last step is known before those GEMMs run: k = iters - 1, or |t_k| <= t_stop with t_k
+// from the X product of the same step.
+struct FinalScale {
+    bool force;      // last iteration by count
+    double t_stop;   // > 0: also last when |t_k| <= t_stop
+    double f;
+    bool applied;    // out: Y', Z' were written unscaled
+};
+
+static spamm_status ns_step_impl(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s, int32_t map,
+                                 spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out, double *t_k,
+                                 spamm_stats stats[3], double *alpha_eps, FinalScale *fs)
 {
     if (map != 0 && map != 1) return set_err(ctx, SPAMM_EINVAL, "map must be 0 or 1");
     ST(check_pair(ctx, Z, Y, tau));
@@ -384,10 +396,24 @@ extern "C" spamm_status spamm_ns_step_map(spamm_ctx ctx, spamm_mat Y, spamm_mat 
     if (!st && map) st = ns_scaled_map(ctx, H, ctx->dscratch, ctx->dscratch + 8);
     if (!st && map) st = norms_finish(ctx, H);
     if (!st && stats) stats[0] = ctx->cw[0]->stats;
+    double ay = 1.0, az = 1.0;
+    if (!st && fs) {
+        bool last = fs->force;
+        if (!last && fs->t_stop > 0.0) {
+            double tt = 0.0;
+            st = fetch1(ctx, ctx->dscratch, &tt, sizeof(double));
+            last = !st && std::fabs(tt) <= fs->t_stop;
+        }
+        if (last) {
+            ay = fs->f;
+            az = 1.0 / fs->f;
+            fs->applied = true;
+        }
+    }
     // Y' = Y (x)_tau_s H ; Z' = H (x)_tau Z
-    if (!st) st = product(ctx, ctx->cw[1], Y, H, tau_s, EPI_STORE, nullptr, &Yn);
+    if (!st) st = product(ctx, ctx->cw[1], Y, H, tau_s, EPI_STORE, nullptr, &Yn, 0, ay);
     if (!st && stats) stats[1] = ctx->cw[1]->stats;
-    if (!st) st = product(ctx, ctx->cw[2], H, Z, tau, EPI_STORE, nullptr, &Zn);
+    if (!st) st = product(ctx, ctx->cw[2], H, Z, tau, EPI_STORE, nullptr, &Zn, 0, az);
     if (!st && stats) stats[2] = ctx->cw[2]->stats;
     double hv[3] = {0, 0, 0}, ae[2] = {1.0, 0.0};
     if (!st) {
@@ -415,6 +441,13 @@ extern "C" spamm_status spamm_ns_step_map(spamm_ctx ctx, spamm_mat Y, spamm_mat 
     if (!std::isfinite(hv[0]) || !std::isfinite(hv[1]) || !std::isfinite(hv[2]))
         return set_err(ctx, SPAMM_ENOTFINITE, "non-finite trace error or root norm");
     return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_ns_step_map(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
+                                          int32_t map, spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out,
+                                          double *t_k, spamm_stats stats[3], double *alpha_eps)
+{
+    return ns_step_impl(ctx, Y, Z, tau, tau_s, map, Y_next, Z_next, H_out, t_k, stats, alpha_eps, nullptr);
 }
 
 extern "C" spamm_status spamm_ns_step(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s,
@@ -457,11 +490,14 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
     spamm_status st = spamm_identity(ctx, s->n, s->b, &Z);
     prof_end(ctx, ps);
     int pl = prof_begin(ctx, SPAMM_PH_LOOP);
+    const double f = std::sqrt(c * (1.0 + mu));
+    bool unscaled = false;   // Y, Z already hold the outputs (final unscale fused)
     for (int k = 0; k < iters && !st; k++) {
         spamm_mat Yn = nullptr, Zn = nullptr;
         double t = 0.0;
         spamm_stats sts[3];
-        st = spamm_ns_step_map(ctx, Y, Z, tau, tau_s, o.map, &Yn, &Zn, nullptr, &t, sts, nullptr);
+        FinalScale fs{k == iters - 1, o.t_stop, f, false};
+        st = ns_step_impl(ctx, Y, Z, tau, tau_s, o.map, &Yn, &Zn, nullptr, &t, sts, nullptr, &fs);
         if (o.t_history && (st == SPAMM_OK || st == SPAMM_ENOTFINITE)) o.t_history[k] = t;
         if (o.per_product && st == SPAMM_OK) memcpy(o.per_product + 3 * k, sts, sizeof(sts));
         if (st) {
@@ -473,15 +509,18 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
         spamm_mat_free(Z);
         Y = Yn;
         Z = Zn;
+        unscaled = fs.applied;
         if (o.iters_done) *o.iters_done = k + 1;
-        if (o.t_stop > 0.0 && std::fabs(t) <= o.t_stop) break;
+        if (unscaled) break;   // the last step (by count or by |t_k| <= t_stop)
     }
     prof_end(ctx, pl);
     std::string err = ctx->err;
     spamm_status st2 = SPAMM_OK;
-    if (Y && Z) {
+    if (Y && Z && unscaled) {
+        *Yout = Y;
+        *Zout = Z;
+    } else if (Y && Z) {
         // unscale: Y * sqrt(c(1+mu)) -> (s + c mu I)^{1/2}, Z / sqrt(c(1+mu)) -> (s + c mu I)^{-1/2}
-        double f = std::sqrt(c * (1.0 + mu));
         spamm_mat Yf = nullptr, Zf = nullptr;
         st2 = mat_map(ctx, Y, 2, f, 0.0, &Yf);
         if (!st2) st2 = mat_map(ctx, Z, 0, f, 0.0, &Zf);
