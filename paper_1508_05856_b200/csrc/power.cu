@@ -298,6 +298,40 @@ __global__ void k_normalize(const double *w, int64_t n, double *v)
     for (int64_t i = threadIdx.x; i < n; i += 1024) v[i] = w[i] / nrm;
 }
 
+// Large n: the normalisation in two launches over NRM_CTAS contiguous chunks
+// (partials in chunk order, then every CTA sums the partials in the same order,
+// so all agree bitwise on the norm) instead of one CTA streaming all of w.
+constexpr int NRM_CTAS = 128;
+__global__ void __launch_bounds__(256) k_sumsq_part(const double *w, int64_t n, double *part)
+{
+    __shared__ double sh[256];
+    const int64_t chunk = (n + NRM_CTAS - 1) / NRM_CTAS, i0 = blockIdx.x * chunk;
+    const int64_t i1 = i0 + chunk < n ? i0 + chunk : n;
+    double s = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += 256) s = fma(w[i], w[i], s);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int k = 128; k > 0; k >>= 1) {
+        if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) k_scale_by_norm(const double *w, int64_t n, const double *part, double *v)
+{
+    __shared__ double nrm;
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int c = 0; c < NRM_CTAS; c++) t += part[c];
+        nrm = sqrt(t);
+    }
+    __syncthreads();
+    const int64_t chunk = (n + NRM_CTAS - 1) / NRM_CTAS, i0 = blockIdx.x * chunk;
+    const int64_t i1 = i0 + chunk < n ? i0 + chunk : n;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += 256) v[i] = w[i] / nrm;
+}
+
 __global__ void k_fill(double *v, int64_t n, double val)
 {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -373,7 +407,8 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     int64_t nblk = s->nblk > 0 ? s->nblk : 1;
     int32_t *cnt = dalloc<int32_t>(ctx, nb), *rowptr = dalloc<int32_t>(ctx, nb + 1);
     int32_t *cols = dalloc<int32_t>(ctx, nblk), *slots = dalloc<int32_t>(ctx, nblk);
-    double *v = dalloc<double>(ctx, n), *w = dalloc<double>(ctx, n), *c = dalloc<double>(ctx, 1);
+    double *v = dalloc<double>(ctx, n), *w = dalloc<double>(ctx, n);
+    double *c = dalloc<double>(ctx, 1 + NRM_CTAS);   // [0] = c, [1..] normalisation partials
     int32_t *tickets = dalloc<int32_t>(ctx, K + 1);   // one per SpMV launch
     // TMA staging pays for 32 KiB blocks; for b = 16 / 32 the per-block barrier of the
     // ring dominates (C2 setup 4.3 -> 8.4 ms measured), so those keep the register kernel
@@ -410,7 +445,13 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     };
     for (int it = 0; it < K; it++) {
         ST(mv(v, w));
-        k_normalize<<<1, 1024, 0, st>>>(w, n, v);
+        if (n >= (1 << 16)) {
+            k_sumsq_part<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1);
+            k_scale_by_norm<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1, v);
+            ctx->launches++;
+        } else {
+            k_normalize<<<1, 1024, 0, st>>>(w, n, v);
+        }
         ctx->launches++;
     }
     ST(mv(v, w));
@@ -425,7 +466,7 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     dev_free(ctx, slots, sizeof(int32_t) * nblk);
     dev_free(ctx, v, sizeof(double) * n);
     dev_free(ctx, w, sizeof(double) * n);
-    dev_free(ctx, c, sizeof(double));
+    dev_free(ctx, c, sizeof(double) * (1 + NRM_CTAS));
     dev_free(ctx, tickets, sizeof(int32_t) * (K + 1));
     dev_free(ctx, part, sizeof(double) * (int64_t)nb * SPT_Q * s->b);
     return SPAMM_OK;

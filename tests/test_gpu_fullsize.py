@@ -78,3 +78,18 @@ def test_lockstep_step_full_size(cfg_name, k_in):
         err, present = sampled_rel(ctx, G, Go.block, n, b, coords, rng)
         assert present == min(1500, len(coords[0]))
         assert err <= 1e-12, (cfg_name, err)
+
+
+@pytest.mark.parametrize("cfg_name", ["C3", "C5"])
+def test_power_scale_full_size(cfg_name):
+    """c ~ ||s||_2 (reading L12) at full size: the TMA-staged SpMV and the two-launch
+    normalisation (n >= 65536) agree with the oracle's power iteration to 1e-12."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cfg = si.CONFIGS[cfg_name]
+    _, (bi, bj, blocks) = si.make_input(cfg)
+    ctx = sp().spamm_ctx_create(0)
+    S = sp().spamm_build_tree_blocks(ctx, cfg.n, cfg.b, bi, bj, blocks)
+    c = sp().spamm_power_scale(ctx, S, 100)
+    So = O.OMat.from_blocks(cfg.n, cfg.b, bi, bj, blocks)
+    assert c == pytest.approx(O.power_scale(So, 100), rel=1e-12)
