@@ -409,3 +409,21 @@ def test_regularized_factor_parity(ctx):
     # an approximate inverse factor: the paper's slices carry "a numerical resolution of
     # approximately one digit"; here ~2e-3 per unit of the spectrum
     assert np.linalg.norm(G.T @ sm @ G - np.eye(c.n)) / math.sqrt(c.n) <= 1e-2
+
+
+def test_ns_nonfinite_reported(ctx):
+    """a run that diverges (scale far below ||s||_2, so the NS map leaves its
+    basin: x(3-x)^2/4 explodes for x > 5) returns SPAMM_ENOTFINITE; the oracle reports the
+    failure too."""
+    c = si.CONFIGS["C1"]
+    s = si.kms(c.n, c.rho)
+    S, So = build_pair(ctx, "dense", s, c.b, c.n)
+    bad = O.power_scale(So) / 8.0
+    with pytest.raises(sp().SpammError) as e:
+        sp().spamm_ns_sqrt(ctx, S, c.tau, 25, scale=bad)
+    assert e.value.code == 6
+    ro = O.ns_sqrt(So, c.tau, 25, scale=bad)
+    assert ro["rc"] != 0        # non-finite t_k or root norm (S:226)
+    # the context stays usable after the failure
+    r = sp().spamm_ns_sqrt(ctx, S, c.tau, 5, scale=O.power_scale(So))
+    assert np.all(np.isfinite(r["t"]))
