@@ -19,6 +19,9 @@
 //      permuted inside each 16-wide k chunk as k = 4t + s (same permutation on
 //      B's rows, so the product is unchanged);
 //   B: lane (g,t) reads B[4t+s][g] (LDS.64).
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "scan.cuh"
 #include "tma.cuh"
@@ -218,6 +221,16 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
                 for (int nf = 0; nf < NF; nf++)
 #pragma unroll
                     for (int s = 0; s < 4; s++) bf[nf][s] = Bs[boff[nf][s] + 16 * kc * B];
+                if (kc == B / 16 - 1) {
+                    // Every read of this stage is issued: release it before the last chunk's
+                    // DMMAs (which only need registers), so the refill starts a quarter task
+                    // earlier and the fence's wait overlaps the previous chunk's DMMAs.  The
+                    // refill is a TMA (async-proxy) write: order this thread's generic-proxy
+                    // reads before it (cross-proxy WAR).
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
+                }
 #pragma unroll
                 for (int s = 0; s < 4; s++)
 #pragma unroll
@@ -226,11 +239,6 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
                         for (int nf = 0; nf < NF; nf++)
                             dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s], bf[nf][s]);
             }
-            // The stage is refilled by TMA (async proxy) after this release: order this
-            // thread's generic-proxy reads of it before those writes (cross-proxy WAR).
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
