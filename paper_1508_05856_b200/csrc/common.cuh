@@ -260,6 +260,10 @@ struct Cull {
 // on capacity overflow.
 spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
                       int transA = 0);
+spamm_status cull_start(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
+                        int transA = 0);
+spamm_status cull_complete(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
+                           int transA = 0);
 void cull_free(spamm_ctx ctx, Cull *cw);
 spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj_host, int64_t cap, int64_t *n);
 
@@ -271,6 +275,9 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
                       spamm_mat C, int epi, double *trace_part, const int32_t *seg_order = nullptr,
                       int64_t nseg = -1, int ticket = 0, int transA = 0);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
+// as diag_fixup without the host round trip: the count of appended blocks lands in
+// *dcount (device); the caller fetches it and sets H->nblk = nseg + count
+spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value, int64_t *dcount);
 // out[0..n) = the segments of `in` (nullable => 0..n-1), longest first (a schedule only)
 spamm_status lpt_order(spamm_ctx ctx, const int32_t *seg_len, const int32_t *in, int64_t n, int32_t *out);
 // scaled / stabilised NS map in place over X: coef <- {alpha, eps, sqrt(alpha)/2}(t)

@@ -441,7 +441,27 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     return SPAMM_OK;
 }
 
-spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1, int transA)
+// counts of a query that did not overflow -> host state, stats, next capacity hint
+static void cull_accept(spamm_ctx ctx, Cull *cw)
+{
+    cw->ntasks = cw->hcnt[cw->L];
+    cw->nsegs = cw->hcnt[CNT_NSEG];
+    spamm_stats &s = cw->stats;
+    s = spamm_stats{};
+    s.tasks = cw->ntasks;
+    s.segments = cw->nsegs;
+    for (int l = cw->l0; l <= cw->L && l < 24; l++) s.level_survivors[l] = cw->hcnt[l];
+    s.candidates = cw->L > cw->l0 ? 8 * (int64_t)cw->hcnt[cw->L - 1] : ((int64_t)1 << (3 * cw->L));
+    s.flops = 2.0 * (double)cw->b * cw->b * cw->b * (double)cw->ntasks;
+    // next capacity hint: 25% headroom over the largest level seen
+    int64_t mx = 0;
+    for (int l = cw->l0; l <= cw->L; l++) mx = cw->hcnt[l] > mx ? cw->hcnt[l] : mx;
+    int64_t h = mx + mx / 4 + 1024;
+    if (h > cw->hint) cw->hint = h;
+    ctx->last = cw;
+}
+
+static spamm_status cull_ensure(spamm_ctx ctx, Cull *cw, spamm_mat A)
 {
     int64_t nb = A->nb;
     int64_t want = cw->hint > 0 ? cw->hint : (int64_t)1 << 16;
@@ -449,26 +469,37 @@ spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double 
         int64_t cap = want > cw->cap ? want : cw->cap;
         ST(cull_alloc(ctx, cw, cap, nb * nb));
     }
+    return SPAMM_OK;
+}
+
+// Split form for batching several queries behind one host round trip: cull_start
+// enqueues, the caller fetches cw->counters into cw->hcnt (with other small values),
+// cull_complete accepts the counts or, after an overflow, grows and re-runs.
+spamm_status cull_start(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1, int transA)
+{
+    ST(cull_ensure(ctx, cw, A));
+    return cull_enqueue(ctx, cw, A, B, tau, r0, r1, transA);
+}
+
+spamm_status cull_complete(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
+                           int transA)
+{
+    if (!cw->hcnt[CNT_OVERFLOW]) {
+        cull_accept(ctx, cw);
+        return SPAMM_OK;
+    }
+    return cull_run(ctx, cw, A, B, tau, r0, r1, transA);
+}
+
+spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1, int transA)
+{
+    const int64_t nb = A->nb;
+    ST(cull_ensure(ctx, cw, A));
     for (int attempt = 0; attempt < 8; attempt++) {
         ST(cull_enqueue(ctx, cw, A, B, tau, r0, r1, transA));
         ST(fetch1(ctx, cw->counters, cw->hcnt, sizeof(int32_t) * 64));
         if (!cw->hcnt[CNT_OVERFLOW]) {
-            cw->ntasks = cw->hcnt[cw->L];
-            cw->nsegs = cw->hcnt[CNT_NSEG];
-            spamm_stats &s = cw->stats;
-            s = spamm_stats{};
-            s.tasks = cw->ntasks;
-            s.segments = cw->nsegs;
-            for (int l = cw->l0; l <= cw->L && l < 24; l++) s.level_survivors[l] = cw->hcnt[l];
-            s.candidates = cw->L > cw->l0 ? 8 * (int64_t)cw->hcnt[cw->L - 1]
-                                          : ((int64_t)1 << (3 * cw->L));
-            s.flops = 2.0 * (double)cw->b * cw->b * cw->b * (double)cw->ntasks;
-            // next capacity hint: 25% headroom over the largest level seen
-            int64_t mx = 0;
-            for (int l = cw->l0; l <= cw->L; l++) mx = cw->hcnt[l] > mx ? cw->hcnt[l] : mx;
-            int64_t h = mx + mx / 4 + 1024;
-            if (h > cw->hint) cw->hint = h;
-            ctx->last = cw;
+            cull_accept(ctx, cw);
             return SPAMM_OK;
         }
         // grow: the largest count seen (the first overflowing level) times 2

@@ -478,6 +478,19 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
     return SPAMM_OK;
 }
 
+spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value, int64_t *dcount)
+{
+    int32_t *newslot = dalloc<int32_t>(ctx, H->nb);
+    if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
+    k_diag_assign<1024><<<1, 1024, 0, ctx->stream>>>(H->slot, H->coord, H->nb, H->r0, H->r1, nseg, newslot, dcount);
+    CKL(ctx);
+    k_diag_fill<<<H->nb, 256, 0, ctx->stream>>>(newslot, H->pool, H->b, value, H->norm2 + pyr_off(H->L));
+    CKL(ctx);
+    dev_free(ctx, newslot, sizeof(int32_t) * H->nb);
+    H->nblk = nseg;   // provisional until the caller has fetched *dcount
+    return SPAMM_OK;
+}
+
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value)
 {
     int64_t added = 0;

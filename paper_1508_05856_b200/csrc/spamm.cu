@@ -266,18 +266,25 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
 }
 
 // product with a given workspace and epilogue; C allocated here
+// cull_done: the query already ran (cull_start + batched fetch + cull_complete);
+// diag_dcount (EPI_NS_H only): append the absent diagonal blocks without a host round
+// trip, their count lands there and the caller sets C->nblk after its next fetch.
 static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
-                            double *trace_part, spamm_mat *C, int transA = 0, double alpha = 1.0)
+                            double *trace_part, spamm_mat *C, int transA = 0, double alpha = 1.0,
+                            bool cull_done = false, int64_t *diag_dcount = nullptr)
 {
     cw->alpha = alpha;
     if (transA && A->dist)
         return set_err(ctx, SPAMM_EINVAL, "A^T (x) B is not available on a row-partitioned context");
     if (A->dist != B->dist || A->r0 != B->r0 || A->r1 != B->r1)
         return set_err(ctx, SPAMM_ESHAPE, "operands have different row partitions");
-    int pc = prof_begin(ctx, SPAMM_PH_CULL);
-    spamm_status sc = cull_run(ctx, cw, A, B, tau, A->r0, A->r1, transA);
-    prof_end(ctx, pc);
-    if (sc) return sc;
+    spamm_status sc = SPAMM_OK;
+    if (!cull_done) {
+        int pc = prof_begin(ctx, SPAMM_PH_CULL);
+        sc = cull_run(ctx, cw, A, B, tau, A->r0, A->r1, transA);
+        prof_end(ctx, pc);
+        if (sc) return sc;
+    }
     g_product_id++;
     if (selfcheck_mode()) selfcheck_cull(ctx, cw, A, B, tau, transA);
     const bool overlap = A->dist && A->parts.world > 1;
@@ -321,7 +328,8 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
         m->nblk = cw->nsegs;
         // absent diagonal blocks of X: H_ii = 1.5 I (plain map) or X_ii = 0 (scaled map,
         // mapped with the other blocks once alpha(t_k), eps(t_k) are known)
-        if (epi == EPI_NS_H) st = diag_fixup(ctx, m, cw->nsegs, 1.5);
+        if (epi == EPI_NS_H && diag_dcount) st = diag_fixup_async(ctx, m, cw->nsegs, 1.5, diag_dcount);
+        else if (epi == EPI_NS_H) st = diag_fixup(ctx, m, cw->nsegs, 1.5);
         if (epi == EPI_NS_X) st = diag_fixup(ctx, m, cw->nsegs, 0.0);
     }
     if (!st && epi != EPI_NS_X) st = norms_finish(ctx, m);
@@ -374,6 +382,57 @@ struct FinalScale {
     bool applied;    // out: Y', Z' were written unscaled
 };
 
+// Single device: the step with three host round trips instead of five.  The X product
+// appends H's absent diagonal blocks without reading their count back; then the Y' and
+// Z' culls are both enqueued and ONE fetch brings back both queries' counters, the
+// diagonal count, and t_k (which decides whether this is the last step, whose Y', Z'
+// GEMMs carry the fused unscale).
+static spamm_status ns_step_batched(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s, int32_t map,
+                                    double *trace_part, spamm_mat *Hp, spamm_mat *Ynp, spamm_mat *Znp,
+                                    spamm_stats stats[3], FinalScale *fs)
+{
+    const int nb = Y->nb;
+    int64_t *ddiag = ctx->iscratch + 1;
+    spamm_mat H = nullptr;
+    spamm_status st = product(ctx, ctx->cw[0], Z, Y, tau, map ? EPI_NS_X : EPI_NS_H, trace_part, &H, 0, 1.0,
+                              false, map ? nullptr : ddiag);
+    const int64_t nseg = ctx->cw[0]->nsegs;
+    if (!st) st = trace_finish(ctx, trace_part, nb, Y->n, ctx->dscratch);
+    if (!st && map) st = ns_scaled_map(ctx, H, ctx->dscratch, ctx->dscratch + 8);
+    if (!st && map) st = norms_finish(ctx, H);
+    if (!st && stats) stats[0] = ctx->cw[0]->stats;
+    Cull *c1 = ctx->cw[1], *c2 = ctx->cw[2];
+    int pc = prof_begin(ctx, SPAMM_PH_CULL);
+    if (!st) st = cull_start(ctx, c1, Y, H, tau_s, Y->r0, Y->r1);
+    if (!st) st = cull_start(ctx, c2, H, Z, tau, H->r0, H->r1);
+    int64_t added = 0;
+    double tt = 0.0;
+    if (!st) {
+        FetchItem it[4] = {{c1->counters, c1->hcnt, 256}, {c2->counters, c2->hcnt, 256}, {ctx->dscratch, &tt, 8},
+                           {ddiag, &added, 8}};
+        st = fetch(ctx, it, map ? 3 : 4);
+    }
+    if (!st && !map) H->nblk = nseg + added;
+    if (!st) st = cull_complete(ctx, c1, Y, H, tau_s, Y->r0, Y->r1);
+    if (!st) st = cull_complete(ctx, c2, H, Z, tau, H->r0, H->r1);
+    prof_end(ctx, pc);
+    double ay = 1.0, az = 1.0;
+    if (!st && fs && (fs->force || (fs->t_stop > 0.0 && std::fabs(tt) <= fs->t_stop))) {
+        ay = fs->f;
+        az = 1.0 / fs->f;
+        fs->applied = true;
+    }
+    spamm_mat Yn = nullptr, Zn = nullptr;
+    if (!st) st = product(ctx, c1, Y, H, tau_s, EPI_STORE, nullptr, &Yn, 0, ay, true);
+    if (!st && stats) stats[1] = c1->stats;
+    if (!st) st = product(ctx, c2, H, Z, tau, EPI_STORE, nullptr, &Zn, 0, az, true);
+    if (!st && stats) stats[2] = c2->stats;
+    *Hp = H;
+    *Ynp = Yn;
+    *Znp = Zn;
+    return st;
+}
+
 static spamm_status ns_step_impl(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s, int32_t map,
                                  spamm_mat *Y_next, spamm_mat *Z_next, spamm_mat *H_out, double *t_k,
                                  spamm_stats stats[3], double *alpha_eps, FinalScale *fs)
@@ -387,6 +446,34 @@ static spamm_status ns_step_impl(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double
     if (!trace_part) return set_err(ctx, SPAMM_ENOMEM, "trace partials");
     CK(cudaMemsetAsync(trace_part, 0, sizeof(double) * nb, ctx->stream));
     spamm_mat H = nullptr, Yn = nullptr, Zn = nullptr;
+    if (!Y->dist) {
+        spamm_status sb = ns_step_batched(ctx, Y, Z, tau, tau_s, map, trace_part, &H, &Yn, &Zn, stats, fs);
+        double hv[3] = {0, 0, 0}, ae[2] = {1.0, 0.0};
+        if (!sb) {
+            FetchItem it[4] = {{ctx->dscratch, &hv[0], 8}, {Yn->norm2, &hv[1], 8}, {Zn->norm2, &hv[2], 8},
+                               {ctx->dscratch + 8, ae, 16}};
+            sb = fetch(ctx, it, map ? 4 : 3);
+        }
+        dev_free(ctx, trace_part, sizeof(double) * nb);
+        if (sb) {
+            spamm_mat_free(H);
+            spamm_mat_free(Yn);
+            spamm_mat_free(Zn);
+            return sb;
+        }
+        if (t_k) *t_k = hv[0];
+        if (alpha_eps) {
+            alpha_eps[0] = ae[0];
+            alpha_eps[1] = ae[1];
+        }
+        if (H_out) *H_out = H;
+        else spamm_mat_free(H);
+        *Y_next = Yn;
+        *Z_next = Zn;
+        if (!std::isfinite(hv[0]) || !std::isfinite(hv[1]) || !std::isfinite(hv[2]))
+            return set_err(ctx, SPAMM_ENOTFINITE, "non-finite trace error or root norm");
+        return SPAMM_OK;
+    }
     // X = Z (x)_tau Y  ->  H = 1/2 (3I - X), tr X partials (X never stored); scaled map:
     // X stored, then H = h_alpha[(1-2eps)X + eps I] in place once t_k is known
     spamm_status st = product(ctx, ctx->cw[0], Z, Y, tau, map ? EPI_NS_X : EPI_NS_H, trace_part, &H);
