@@ -140,15 +140,7 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
     }
 }
 
-// ------------------------------------------------- TMA-staged SpMV (b = 64)
-// One persistent CTA per SM streams whole 32 KiB blocks into a 6-stage shared
-// memory ring with TMA bulk copies (thread 0 issues, mbarrier transaction counts
-// signal arrival), so ~192 KiB per SM are in flight without holding them in
-// registers.  Work units are quarters of block rows (a quarter of the row's blocks,
-// ascending), taken from a ticket; a thread owns one 16-byte chunk of 8 rows of
-// each block (consecutive lanes read consecutive chunks: conflict-free) and keeps
-// 8 row accumulators across the unit's blocks.  Each unit writes its 64 partial row
-// sums; k_spmv_fix adds the 4 quarters in a fixed order (deterministic).
+// ------------------------------------------------- TMA-staged SpMV configuration
 constexpr int SPT_Q = 4;                       // work unit = a quarter of a block row
 // stages of the ring per leaf size: 6 x 32 KiB (b=64), 16 x 8 KiB (b=32), 32 x 2 KiB (b=16)
 template <int B> struct SptCfg {
@@ -168,30 +160,83 @@ struct SpmvTmaArgs {
     int nunits;         // nb * SPT_Q
 };
 
-template <int B>
-__global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
+// ------------------------------------------------- TMA-staged SpMV kernel
+// One persistent CTA per SM streams whole blocks into a shared-memory ring with TMA
+// bulk copies.  Warp 8 is the producer: its lane 0 takes work units from a ticket,
+// reads the unit's slot / column indices in batches and refills stage st as soon
+// as the 8 consumer warps have released it (empty[st]); the consumers never wait
+// for the producer's index loads or ticket atomics, only for data (full[st]).
+// Consumer thread t owns double2 chunk q = t + 256 m of each block (consecutive
+// lanes, consecutive 16 B: conflict-free) and keeps its row accumulators across
+// the unit's blocks; at the unit's last block each block row's LPR lanes reduce with
+// a fixed xor tree into part[unit*b + r], and k_spmv_fix adds the SPT_Q quarters in
+// a fixed order (deterministic).
+//
+// SYM (s symmetric, checked bitwise by k_sym_check): units cover only the blocks on
+// and above the diagonal, [up[I], rowptr[I+1]) — half the HBM reads.  An
+// off-diagonal block (I, J) also contributes S_IJ^T v_I to the rows of J: a second
+// pass over the staged tile forms the column sums sum_r S_IJ[r,c] v_I[r] (NSUB row
+// subsets per column, reduced in a fixed order after a consumer-only named barrier)
+// and stores them at colpart[p'*b ..], p' = the CSR position of the mirror (J, I),
+// so k_spmv_sym_fix reads the column parts of row block J contiguously, ascending I.
+template <int B, bool SYM>
+__global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_t *up, const int32_t *mir,
+                                                          double *colpart)
 {
     using Cf = SptCfg<B>;
     constexpr int TILE = B * B, STAGES = Cf::STAGES, LPR = Cf::LPR, M = Cf::M, RPW = Cf::RPW, N2 = Cf::N2;
+    constexpr int NSUB = 256 / B, RS = B / NSUB;   // column pass: row subsets, rows per subset
     extern __shared__ __align__(1024) double sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + STAGES * TILE);
-    int4 *meta = reinterpret_cast<int4 *>(full + STAGES);   // {unit, column block, last, -}
-    __shared__ int s_total;
+    uint64_t *empty = full + STAGES;
+    int4 *meta = reinterpret_cast<int4 *>(empty + STAGES);   // {unit (-1: end), column block, last, mirror}
+    __shared__ double red[SYM ? 2 : 1][NSUB][B];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // issuer state (thread 0); the unit's slot / column indices are fetched in one
-    // batch of independent loads (UCH at a time), not one dependent load per issue
-    constexpr int UCH = 32;
-    int issued = 0, unit = -1, p = 0, pend = 0, ubase = 0;
-    int us[UCH], uc[UCH];
-    bool done = false;
     if (tid == 0) {
-        for (int st = 0; st < STAGES; st++) mbar_init(&full[st], 1);
+        for (int st = 0; st < STAGES; st++) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], 8);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        s_total = -1;
     }
     __syncthreads();
-    // thread tid owns double2 chunk q = tid + 256 m of each block: block row
-    // q / LPR, chunk q % LPR (consecutive lanes, consecutive 16 B: conflict-free)
+    if (warp == 8) {   // ---------------------------------------------- producer
+        if (lane != 0) return;
+        constexpr int UCH = 32;
+        int issued = 0;
+        for (;;) {
+            const int unit = atomicAdd(g.ticket, 1);
+            if (unit >= g.nunits) break;
+            const int I = unit / SPT_Q, q = unit % SPT_Q;
+            const int r0 = SYM ? up[I] : g.rowptr[I], len = g.rowptr[I + 1] - r0;
+            const int pb = r0 + (q * len) / SPT_Q, pend = r0 + ((q + 1) * len) / SPT_Q;
+            for (int p0 = pb; p0 < pend; p0 += UCH) {
+                int us[UCH], uc[UCH], um[UCH];
+#pragma unroll
+                for (int i = 0; i < UCH; i++) {
+                    us[i] = p0 + i < pend ? __ldg(g.slots + p0 + i) : 0;
+                    uc[i] = p0 + i < pend ? __ldg(g.cols + p0 + i) : 0;
+                    um[i] = SYM && p0 + i < pend ? __ldg(mir + p0 + i) : 0;
+                }
+#pragma unroll 1
+                for (int i = 0; i < UCH && p0 + i < pend; i++) {
+                    const int st = issued % STAGES;
+                    if (issued >= STAGES) mbar_wait(&empty[st], ((issued / STAGES) - 1) & 1);
+                    meta[st] = make_int4(unit, uc[i], p0 + i + 1 == pend, um[i]);
+                    mbar_expect_tx(&full[st], TILE * 8);
+                    bulk_g2s(sm + st * TILE, g.pool + (int64_t)us[i] * TILE, TILE * 8, &full[st]);
+                    issued++;
+                }
+            }
+        }
+        const int st = issued % STAGES;   // end marker
+        if (issued >= STAGES) mbar_wait(&empty[st], ((issued / STAGES) - 1) & 1);
+        meta[st] = make_int4(-1, 0, 0, 0);
+        mbar_arrive(&full[st]);
+        return;
+    }
+    // ----------------------------------------------------------------- consumers
+    const int cc = tid % B, sub = tid / B;   // column pass: column, row subset
     double acc[M];
     int lc[M];
 #pragma unroll
@@ -200,46 +245,15 @@ __global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
         acc[m] = 0.0;
         lc[m] = ((q % LPR) ^ swz(r)) << 1;   // logical column pair (pool swizzle)
     }
+    int vunit = -1, nred = 0;
+    double vi[SYM ? RS : 1];   // v_I at this thread's column-pass rows
     for (int j = 0;; j++) {
-        if (tid == 0) {
-            // keep the ring full: blocks j .. j + STAGES - 1 in flight
-            while (!done && issued < j + STAGES) {
-                if (p == pend) {
-                    unit = atomicAdd(g.ticket, 1);
-                    if (unit >= g.nunits) {
-                        done = true;
-                        s_total = issued;
-                        break;
-                    }
-                    const int I = unit / SPT_Q, q = unit % SPT_Q;
-                    const int p0 = g.rowptr[I], len = g.rowptr[I + 1] - p0;
-                    p = p0 + (q * len) / SPT_Q;
-                    pend = p0 + ((q + 1) * len) / SPT_Q;
-                    ubase = p - UCH;   // forces a fetch below
-                    continue;
-                }
-                if (p - ubase >= UCH) {
-                    ubase = p;
-#pragma unroll
-                    for (int i = 0; i < UCH; i++) {
-                        us[i] = p + i < pend ? __ldg(g.slots + p + i) : 0;
-                        uc[i] = p + i < pend ? __ldg(g.cols + p + i) : 0;
-                    }
-                }
-                const int st = issued % STAGES;
-                meta[st] = make_int4(unit, uc[p - ubase], p + 1 == pend, 0);
-                mbar_expect_tx(&full[st], TILE * 8);
-                bulk_g2s(sm + st * TILE, g.pool + (int64_t)us[p - ubase] * TILE, TILE * 8, &full[st]);
-                issued++;
-                p++;
-            }
-        }
-        __syncthreads();
-        if (s_total >= 0 && j >= s_total) break;
         const int st = j % STAGES;
         mbar_wait(&full[st], (j / STAGES) & 1);
         const int4 mt = meta[st];
-        const double2 *x2 = reinterpret_cast<const double2 *>(sm + st * TILE);
+        if (mt.x < 0) break;
+        const double *tile = sm + st * TILE;
+        const double2 *x2 = reinterpret_cast<const double2 *>(tile);
         const double *vv = g.v + (int64_t)mt.y * B;
 #pragma unroll
         for (int m = 0; m < M; m++) {
@@ -249,8 +263,20 @@ __global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
             acc[m] = fma(x.x, w.x, acc[m]);
             acc[m] = fma(x.y, w.y, acc[m]);
         }
+        const int I = mt.x / SPT_Q;
+        const bool offdiag = SYM && mt.y != I;   // CTA-uniform
+        if (offdiag) {
+            if (mt.x != vunit) {
+                vunit = mt.x;
+#pragma unroll
+                for (int i = 0; i < RS; i++) vi[i] = g.v[(int64_t)I * B + sub * RS + i];
+            }
+            double cs = 0.0;
+#pragma unroll
+            for (int i = 0; i < RS; i++) cs = fma(tile[pool_at(sub * RS + i, cc, B)], vi[i], cs);
+            red[nred & 1][sub][cc] = cs;
+        }
         if (mt.z) {
-            // last block of the unit: each block row's LPR lanes reduce with a fixed xor tree
 #pragma unroll
             for (int m = 0; m < M; m++) {
                 if (tid + 256 * m >= N2) break;
@@ -262,24 +288,164 @@ __global__ void __launch_bounds__(256, 1) k_spmv_tma(SpmvTmaArgs g)
                 acc[m] = 0.0;
             }
         }
-        __syncthreads();   // stage st may be refilled from the next iteration on
+        // generic-proxy reads of stage st before its async-proxy (TMA) refill
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (offdiag) {
+            asm volatile("bar.sync 1, 256;\n" ::: "memory");   // consumers only: red[nred & 1] complete
+            if (tid < B) {
+                double t = red[nred & 1][0][tid];
+#pragma unroll
+                for (int s2 = 1; s2 < NSUB; s2++) t += red[nred & 1][s2][tid];
+                colpart[(int64_t)mt.w * B + tid] = t;
+            }
+            nred++;
+        }
     }
 }
 
-// w[I*b + r] = (P0 + P1) + (P2 + P3), P_q = quarter q's partial (0 if the quarter is empty)
-__global__ void k_spmv_fix(const int32_t *rowptr, const double *part, int nb, int b, double *w)
+// Sum of w^2 over the CTA's 256 threads in a fixed order (xor tree in each warp,
+// then the 8 warp sums in warp order): the normalisation's partial for this CTA.
+__device__ __forceinline__ void cta_sumsq_part(double x, double *nrm_part)
+{
+    __shared__ double ws[8];
+    double t = x * x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double u = ws[0];
+        for (int k = 1; k < 8; k++) u += ws[k];
+        nrm_part[blockIdx.x] = u;
+    }
+}
+
+// w[J*b + c] = (P0 + P1) + (P2 + P3) over J's upper quarters, then + the column
+// parts of the blocks (I, J), I < J, ascending I: colpart rows [rowptr[J], up[J]).
+// Also the CTA's partial of ||w||^2 (fused normalisation, k_norm_apply).
+__global__ void __launch_bounds__(256) k_spmv_sym_fix(const int32_t *rowptr, const int32_t *up,
+                                                      const double *part, const double *colpart, int nb,
+                                                      int b, double *w, double *nrm_part)
 {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= (int64_t)nb * b) return;
-    const int I = (int)(e / b), r = (int)(e % b);
-    const int p0 = rowptr[I], len = rowptr[I + 1] - p0;
-    double P[SPT_Q];
+    double t = 0.0;
+    if (e < (int64_t)nb * b) {
+        const int J = (int)(e / b), c = (int)(e % b);
+        const int p0 = up[J], len = rowptr[J + 1] - p0;
+        double P[SPT_Q];
 #pragma unroll
-    for (int q = 0; q < SPT_Q; q++) {
-        const bool any = ((q + 1) * len) / SPT_Q > (q * len) / SPT_Q;
-        P[q] = any ? part[((int64_t)I * SPT_Q + q) * b + r] : 0.0;
+        for (int q = 0; q < SPT_Q; q++) {
+            const bool any = ((q + 1) * len) / SPT_Q > (q * len) / SPT_Q;
+            P[q] = any ? part[((int64_t)J * SPT_Q + q) * b + c] : 0.0;
+        }
+        t = (P[0] + P[1]) + (P[2] + P[3]);
+        const double *cp = colpart + c;
+#pragma unroll 4
+        for (int p = rowptr[J]; p < p0; p++) t += cp[(int64_t)p * b];
+        w[e] = t;
     }
-    w[e] = (P[0] + P[1]) + (P[2] + P[3]);
+    cta_sumsq_part(t, nrm_part);
+}
+
+// Structure of the symmetric SpMV, one CTA per block row J:
+//   up[J]   = first CSR position of row J with column >= J;
+//   mir[p]  = CSR position of the mirror (I, J) of the entry p = (J, I) (p itself on
+//             the diagonal).
+// *bad = 1 if some block has no mirror (the pattern is not symmetric).
+__global__ void k_sym_index(const int32_t *rowptr, const int32_t *cols, int nb, int32_t *up,
+                            int32_t *mir, int32_t *bad)
+{
+    const int J = blockIdx.x, p0 = rowptr[J], p1 = rowptr[J + 1];
+    if (threadIdx.x == 0 && (p1 == p0 || cols[p0] >= J)) up[J] = p0;
+    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const int I = cols[p];
+        if (I < J && (p + 1 == p1 || cols[p + 1] >= J)) up[J] = p + 1;
+        if (I == J) {
+            mir[p] = p;
+            continue;
+        }
+        int lo = rowptr[I], hi = rowptr[I + 1];   // binary search for J in row I
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (cols[mid] < J) lo = mid + 1;
+            else hi = mid;
+        }
+        const bool found = lo < rowptr[I + 1] && cols[lo] == J;
+        if (!found) *bad = 1;
+        else mir[p] = lo;
+    }
+}
+
+// *bad = 1 unless S_JI == S_IJ^T bitwise for every block on or below the diagonal
+// (one CTA per CSR position; positions above the diagonal return at once)
+template <int B>
+__global__ void __launch_bounds__(256) k_sym_check(const double *pool, const int32_t *rowptr,
+                                                   const int32_t *cols, const int32_t *slots,
+                                                   const int32_t *mir, int nb, int32_t *bad)
+{
+    __shared__ double t[B * B];
+    const int p = blockIdx.x;
+    int lo = 0, hi = nb;   // row of p: last J with rowptr[J] <= p
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (rowptr[mid] <= p) lo = mid;
+        else hi = mid;
+    }
+    const int J = lo, I = cols[p];
+    if (I > J || *(volatile int32_t *)bad) return;   // upper entry, or k_sym_index found no mirror
+    const int q = mir[p];
+    const double *a = pool + (int64_t)slots[p] * B * B, *m = pool + (int64_t)slots[q] * B * B;
+    for (int e = threadIdx.x; e < B * B; e += 256) t[e] = m[e];
+    __syncthreads();
+    bool ok = true;
+    for (int e = threadIdx.x; e < B * B; e += 256) {
+        const int r = e / B, c = pool_col(e, B);
+        ok &= __double_as_longlong(a[e]) == __double_as_longlong(t[pool_at(c, r, B)]);
+    }
+    if (__syncthreads_or(!ok) && threadIdx.x == 0) *bad = 1;
+}
+
+// w[I*b + r] = (P0 + P1) + (P2 + P3), P_q = quarter q's partial (0 if the quarter is
+// empty); also the CTA's partial of ||w||^2
+__global__ void __launch_bounds__(256) k_spmv_fix(const int32_t *rowptr, const double *part, int nb, int b,
+                                                  double *w, double *nrm_part)
+{
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double t = 0.0;
+    if (e < (int64_t)nb * b) {
+        const int I = (int)(e / b), r = (int)(e % b);
+        const int p0 = rowptr[I], len = rowptr[I + 1] - p0;
+        double P[SPT_Q];
+#pragma unroll
+        for (int q = 0; q < SPT_Q; q++) {
+            const bool any = ((q + 1) * len) / SPT_Q > (q * len) / SPT_Q;
+            P[q] = any ? part[((int64_t)I * SPT_Q + q) * b + r] : 0.0;
+        }
+        t = (P[0] + P[1]) + (P[2] + P[3]);
+        w[e] = t;
+    }
+    cta_sumsq_part(t, nrm_part);
+}
+
+// v = w / sqrt(sum of the np partials); every CTA sums the partials in the same fixed
+// order (strided per thread, then a tree), so all agree bitwise on the norm
+__global__ void __launch_bounds__(256) k_norm_apply(const double *w, int64_t n, const double *nrm_part, int np,
+                                                    double *v)
+{
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < np; i += 256) s += nrm_part[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int k = 128; k > 0; k >>= 1) {
+        if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+        __syncthreads();
+    }
+    const double nrm = sqrt(sh[0]);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = w[i] / nrm;
 }
 
 // single CTA: nrm = sqrt(sum w^2) (fixed order); v = w / nrm
@@ -354,18 +520,44 @@ __global__ void k_dot(const double *a, const double *b, int64_t n, double *out)
 
 template <int B>
 static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
-                             const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part)
+                             const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part,
+                             double *nrm_part)
 {
     constexpr int STAGES = SptCfg<B>::STAGES;
-    const size_t smem = sizeof(double) * STAGES * B * B + STAGES * (sizeof(uint64_t) + sizeof(int4));
+    const size_t smem = sizeof(double) * STAGES * B * B + STAGES * (2 * sizeof(uint64_t) + sizeof(int4));
     static std::atomic<uint64_t> configured{0};
     CK(once_per_device(configured, ctx->device, [&]() {
-        return cudaFuncSetAttribute(k_spmv_tma<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return cudaFuncSetAttribute(k_spmv_tma<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }));
     SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
-    k_spmv_tma<B><<<ctx->sm_count, 256, smem, ctx->stream>>>(g);
+    k_spmv_tma<B, false><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, nullptr, nullptr, nullptr);
     CKL(ctx);
-    k_spmv_fix<<<cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream>>>(rowptr, part, s->nb, B, w);
+    k_spmv_fix<<<cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream>>>(rowptr, part, s->nb, B, w, nrm_part);
+    CKL(ctx);
+    return SPAMM_OK;
+}
+
+struct SymSpmv {
+    const int32_t *up, *mir;
+    double *colpart;
+};
+
+template <int B>
+static spamm_status spmv_sym(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
+                             const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part,
+                             double *nrm_part, const SymSpmv &y)
+{
+    constexpr int STAGES = SptCfg<B>::STAGES;
+    const size_t smem = sizeof(double) * STAGES * B * B + STAGES * (2 * sizeof(uint64_t) + sizeof(int4));
+    static std::atomic<uint64_t> configured{0};
+    CK(once_per_device(configured, ctx->device, [&]() {
+        return cudaFuncSetAttribute(k_spmv_tma<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }));
+    SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
+    k_spmv_tma<B, true><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, y.up, y.mir, y.colpart);
+    CKL(ctx);
+    k_spmv_sym_fix<<<cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream>>>(rowptr, y.up, part, y.colpart,
+                                                                          s->nb, B, w, nrm_part);
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -389,13 +581,23 @@ static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_
     ctx->launches++;
 }
 
-// SPAMM_SPMV_TMA=0 selects the register-streaming SpMV (k_spmv) instead
-static bool spmv_tma_mode()
+// SPAMM_SPMV_TMA=0 selects the register-streaming SpMV (k_spmv) instead of the TMA
+// ring; SPAMM_SPMV_SYM=0 disables the symmetric (upper-half) SpMV
+// 0 = off, 1 = b = 64 (default), 2 = every leaf size (measurement)
+static int spmv_tma_mode()
 {
-    // function-local static: initialised once, thread-safely (C++11)
-    static const bool m = [] {
+    static const int m = [] {   // function-local static: thread-safe init
         const char *e = getenv("SPAMM_SPMV_TMA");
-        return !(e && *e == '0');
+        return e && *e ? atoi(e) : 1;
+    }();
+    return m;
+}
+// 0 = off, 1 = b = 64 (default), 2 = every leaf size (measurement)
+static int spmv_sym_mode()
+{
+    static const int m = [] {
+        const char *e = getenv("SPAMM_SPMV_SYM");
+        return e && *e ? atoi(e) : 1;
     }();
     return m;
 }
@@ -412,9 +614,17 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     int32_t *tickets = dalloc<int32_t>(ctx, K + 1);   // one per SpMV launch
     // TMA staging pays for 32 KiB blocks; for b = 16 / 32 the per-block barrier of the
     // ring dominates (C2 setup 4.3 -> 8.4 ms measured), so those keep the register kernel
-    const bool tma = spmv_tma_mode() && s->b == 64;
-    double *part = tma ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * s->b) : nullptr;
-    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets || (tma && !part))
+    const int tmam = spmv_tma_mode();
+    const bool tma = tmam == 2 || (tmam == 1 && s->b == 64);
+    // symmetric s (checked below): read only the upper half of the blocks
+    const int symm = spmv_sym_mode();
+    bool sym = !s->dist && tmam != 0 && (symm == 2 || (symm == 1 && s->b == 64));
+    double *part = tma || sym ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * s->b) : nullptr;
+    // the TMA kernels' fix-up launch also writes per-CTA partials of ||w||^2 (np of them)
+    const int np = (int)cdiv(n, 256);
+    const bool fused = (tma || sym) && !s->dist;
+    double *nrm_part = tma || sym ? dalloc<double>(ctx, np) : nullptr;
+    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets || ((tma || sym) && (!part || !nrm_part)))
         return set_err(ctx, SPAMM_ENOMEM, "power");
     CK(cudaMemsetAsync(tickets, 0, sizeof(int32_t) * (K + 1), ctx->stream));
     int nmv = 0;
@@ -424,15 +634,48 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     k_row_fill<<<nb, 256, 0, st>>>(s->slot, nb, rowptr, cols, slots);
     k_fill<<<cdiv(n, 256), 256, 0, st>>>(v, n, 1.0 / sqrt((double)n));
     ctx->launches += 4;
+    SymSpmv sy{nullptr, nullptr, nullptr};
+    int32_t *up = nullptr, *mir = nullptr;
+    double *colpart = nullptr;
+    if (sym) {
+        up = dalloc<int32_t>(ctx, nb);
+        mir = dalloc<int32_t>(ctx, nblk);
+        colpart = dalloc<double>(ctx, nblk * s->b);
+        int32_t *bad = reinterpret_cast<int32_t *>(c);   // c[0] is written only by the final dot
+        if (!up || !mir || !colpart) return set_err(ctx, SPAMM_ENOMEM, "power");
+        CK(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
+        k_sym_index<<<nb, 256, 0, st>>>(rowptr, cols, nb, up, mir, bad);
+        ctx->launches++;
+        if (s->nblk > 0) {
+            switch (s->b) {
+            case 16: k_sym_check<16><<<(int)s->nblk, 256, 0, st>>>(s->pool, rowptr, cols, slots, mir, nb, bad); break;
+            case 32: k_sym_check<32><<<(int)s->nblk, 256, 0, st>>>(s->pool, rowptr, cols, slots, mir, nb, bad); break;
+            default: k_sym_check<64><<<(int)s->nblk, 256, 0, st>>>(s->pool, rowptr, cols, slots, mir, nb, bad); break;
+            }
+            ctx->launches++;
+        }
+        CKL(ctx);
+        int32_t hbad = 1;
+        ST(fetch1(ctx, bad, &hbad, sizeof(int32_t)));
+        sym = hbad == 0;
+        sy = SymSpmv{up, mir, colpart};
+    }
     // row partition: local block rows of w = s v, then all ranks gather the full w
     // (each row is computed by one rank with the single-device kernel: bitwise G-invariant)
     auto mv = [&](const double *x, double *y) -> spamm_status {
         int32_t *tk = tickets + nmv++;
+        if (sym) {
+            switch (s->b) {
+            case 16: return spmv_sym<16>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+            case 32: return spmv_sym<32>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+            default: return spmv_sym<64>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+            }
+        }
         if (tma) {
             switch (s->b) {
-            case 16: ST(spmv_tma<16>(ctx, s, rowptr, cols, slots, x, y, tk, part)); break;
-            case 32: ST(spmv_tma<32>(ctx, s, rowptr, cols, slots, x, y, tk, part)); break;
-            default: ST(spmv_tma<64>(ctx, s, rowptr, cols, slots, x, y, tk, part)); break;
+            case 16: ST(spmv_tma<16>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part)); break;
+            case 32: ST(spmv_tma<32>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part)); break;
+            default: ST(spmv_tma<64>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part)); break;
             }
             return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
         }
@@ -445,7 +688,9 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     };
     for (int it = 0; it < K; it++) {
         ST(mv(v, w));
-        if (n >= (1 << 16)) {
+        if (fused) {
+            k_norm_apply<<<(int)std::min<int64_t>(NRM_CTAS, np), 256, 0, st>>>(w, n, nrm_part, np, v);
+        } else if (n >= (1 << 16)) {
             k_sumsq_part<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1);
             k_scale_by_norm<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1, v);
             ctx->launches++;
@@ -469,5 +714,9 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     dev_free(ctx, c, sizeof(double) * (1 + NRM_CTAS));
     dev_free(ctx, tickets, sizeof(int32_t) * (K + 1));
     dev_free(ctx, part, sizeof(double) * (int64_t)nb * SPT_Q * s->b);
+    dev_free(ctx, nrm_part, sizeof(double) * np);
+    dev_free(ctx, up, sizeof(int32_t) * nb);
+    dev_free(ctx, mir, sizeof(int32_t) * nblk);
+    dev_free(ctx, colpart, sizeof(double) * nblk * s->b);
     return SPAMM_OK;
 }

@@ -232,6 +232,30 @@ def test_power_scale(ctx):
         assert sp().spamm_power_scale(ctx, S, 100) == pytest.approx(O.power_scale(So, 100), rel=1e-12)
 
 
+@pytest.mark.parametrize("case", ["sym", "sym_holes", "asym_values", "asym_pattern"])
+def test_power_scale_symmetric_and_fallback(ctx, case):
+    """b = 64: a bitwise-symmetric s takes the upper-half SpMV (column parts of the
+    off-diagonal blocks), anything else the full SpMV; both match the oracle's
+    plain power iteration (reading L12).  Holes: absent off-diagonal blocks in a
+    symmetric pattern, and an empty block row tail."""
+    n, b = 2048, 64                     # nb = 32: several units per row, ragged quarters
+    m = np.abs(decaying(n, 0.01, 7))
+    m = m + m.T
+    nb = n // b
+    if case in ("sym_holes", "asym_pattern"):
+        r = np.random.default_rng(3)
+        for I in range(nb):
+            for J in range(I + 1, nb):
+                if r.random() < 0.4:
+                    m[I * b:(I + 1) * b, J * b:(J + 1) * b] = 0
+                    if case == "sym_holes":
+                        m[J * b:(J + 1) * b, I * b:(I + 1) * b] = 0
+    if case == "asym_values":
+        m[5, 700] *= 1.0 + 2.0 ** -40
+    S, So = build_pair(ctx, "dense", m, b, n)
+    assert sp().spamm_power_scale(ctx, S, 100) == pytest.approx(O.power_scale(So, 100), rel=1e-12)
+
+
 def test_ns_step_lockstep(ctx):
     """One dual step from identical inputs: H, t, Y', Z' and the three task counts."""
     c = si.CONFIGS["C2"]
