@@ -87,7 +87,7 @@ def load():
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = _build.LIB
+    path = os.environ.get("SPAMM_LIB", _build.LIB)   # SPAMM_LIB: an experimental build (A/B timing)
     if not os.path.exists(path):
         path = _build.build()
     L = C.CDLL(path)

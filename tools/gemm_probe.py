@@ -1,0 +1,50 @@
+"""A/B timing of single SpAMM products on realistic iterates: runs k dual NS steps of a config,
+then times spamm_multiply(Z, Y) (the X product's task set, plain store epilogue) and
+spamm_multiply(Y, Z) with CUDA events (cull + GEMM), best of --reps.
+SPAMM_LIB=<path> selects an experimental build of the library."""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1508_05856_b200 as sp  # noqa: E402
+import spamm_inputs as si  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C3")
+ap.add_argument("-k", type=int, default=8)
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+cfg = si.CONFIGS[a.config]
+tau, tau_s = cfg.tau, cfg.tau * cfg.tau_s_factor
+kind, payload = si.make_input(cfg)
+ctx = sp.spamm_ctx_create(0)
+if kind == "dense":
+    S = sp.spamm_build_tree(ctx, torch.from_numpy(payload).cuda(), cfg.b)
+else:
+    S = sp.spamm_build_tree_blocks(ctx, cfg.n, cfg.b, *(torch.from_numpy(x).cuda() for x in payload))
+c = sp.spamm_power_scale(ctx, S, 100)
+Y = sp.spamm_ns_y0(ctx, S, c, cfg.mu)
+Z = sp.spamm_identity(ctx, cfg.n, cfg.b)
+S.free()
+for _ in range(a.k):
+    Yn, Zn, _, _ = sp.spamm_ns_step(ctx, Y, Z, tau, tau_s)
+    Y.free()
+    Z.free()
+    Y, Z = Yn, Zn
+for name, (A, B) in (("Z*Y", (Z, Y)), ("Y*Z", (Y, Z))):
+    best, st = 1e30, None
+    for _ in range(a.reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream) if hasattr(ctx, "stream") and ctx.stream is not None else e0.record()
+        C, st = sp.spamm_multiply(ctx, A, B, tau, want_stats=True)
+        e1.record(ctx.stream) if hasattr(ctx, "stream") and ctx.stream is not None else e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+        C.free()
+    print(f"{a.config} k={a.k} {name}: tasks {st['tasks']} segments {st['segments']} "
+          f"({st['tasks'] / max(st['segments'], 1):.2f} per segment) {best:.3f} ms "
+          f"{st['flops'] / best / 1e9:.2f} TFLOP/s", flush=True)
