@@ -153,6 +153,29 @@ def oracle_sample(cfg, payload, tau, iters, scale, tau_s=None):
     return dt, flops, O.num_threads()
 
 
+def run_config(args, cfg, ws, in_bytes):
+    """The `config` object of the JSON line, identical for both arms at the same flags and N."""
+    tau = args.tau if args.tau is not None else cfg.tau
+    iters = args.iters if args.iters is not None else cfg.iters
+    tau_s = tau * (args.tau_s_factor if args.tau_s_factor is not None else cfg.tau_s_factor)
+    t_stop = args.t_stop if args.t_stop is not None else cfg.t_stop
+    dist_path = ws > 1 or args.dist_world1
+    return {
+        "workload": workload_name(cfg, tau, iters), "n": cfg.n, "leaf": cfg.b, "tau": tau,
+        "tau_s": tau_s, "iters": iters, "t_stop": t_stop, "map": args.map, "channel": args.channel,
+        "parallelism": (f"row-partitioned over {ws} GPUs ({args.partition} split), NCCL halo "
+                        "exchange + norm all-gather") if dist_path else "single",
+        "l2": (f"inputs larger than L2 (s ~ {in_bytes / 1e6:.0f} MB of blocks, iterates > 126 MB)"
+               if in_bytes > 126e6 else
+               f"s ~ {in_bytes / 1e6:.1f} MB fits in L2, no flush between steps (latency-bound parity "
+               "config, not the bench workload)"),
+    }
+
+
+def payload_bytes(kind, payload):
+    return payload.nbytes if kind == "dense" else sum(x.nbytes for x in payload)
+
+
 # ---------------------------------------------------------- reference arm
 def run_reference(args):
     ws, rank, local = dist_env()
@@ -162,6 +185,7 @@ def run_reference(args):
     tau = args.tau if args.tau is not None else cfg.tau
     iters = args.iters if args.iters is not None else cfg.iters
     kind, payload = si.make_input(cfg)
+    config = run_config(args, cfg, ws, payload_bytes(kind, payload))
     import oracle as O
     if kind == "dense":
         So = O.OMat.from_dense(payload, cfg.b)
@@ -184,7 +208,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": workload_name(cfg, tau, iters), "sample": sample},
+        "data": "synthetic", "config": config,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -463,13 +487,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {
-                "workload": workload_name(cfg, tau, iters), "n": cfg.n, "leaf": cfg.b, "tau": tau,
-                "tau_s": tau_s, "iters": iters, "t_stop": t_stop, "map": args.map, "channel": args.channel,
-                "parallelism": (f"row-partitioned over {ws} GPUs ({args.partition} split), NCCL halo "
-                                "exchange + norm all-gather") if comm is not None else "single",
-                "l2": f"inputs larger than L2 (s ~ {blocks_mb:.0f} MB of blocks, iterates > 126 MB)",
-            },
+            "config": run_config(args, cfg, ws, blocks_mb * 1e6),
             "iters_run": int(r["iters"]),
             "s_per_ns_iteration": prof["loop_ms"] / args.steps / max(int(r["iters"]), 1) / 1e3,
             "setup_ms_per_step": prof["setup_ms"] / args.steps,
