@@ -21,6 +21,7 @@
 //   B: lane (g,t) reads B[4t+s][g] (LDS.64).
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -61,7 +62,7 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
 // TA = 1: the left operand is A^T (single channel, §8(f) f2): the A tile is read
 // with the column pattern of the B fragments (A^T[m][k] = A[k][m]).
 template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
-__global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
+__global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
 {
     static_assert(WM * WN == CW, "warp grid");
     constexpr int TM = B / WM, TN = B / WN;
@@ -176,6 +177,98 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
         for (int s = 0; s < 4; s++) boff[nf][s] = (4 * t4 + s) * B + ((((col >> 1) ^ ((t4 << 1) | (s & 1)))) << 1) + (col & 1);
     }
 
+    // Deferred epilogue: a segment's accumulators are parked in pacc and its epilogue
+    // (value map, ||C_ij||^2 / tr partials, stores, shuffle reduction) runs in NKC
+    // slices interleaved with the kc chunks of the NEXT segment's first task, so the
+    // two warps of an SMSP keep issuing DMMAs instead of both idling in the epilogue.
+    constexpr int NKC = B / 16;
+    double pacc[MF][NF][2];
+    int pseg = -1, pslot = 0;
+    uint32_t pcode = 0;
+    double pss = 0.0, ptr = 0.0;
+    // slice kc of the pending epilogue (kc = 0 also maps the values and forms the partials)
+    auto epi_slice = [&](int kc) {
+        const int I = morton_i(pcode), J = morton_j(pcode);
+        const bool diag = (I == J);
+        if (kc == 0) {
+            pss = 0.0;
+            ptr = 0.0;
+#pragma unroll
+            for (int mf = 0; mf < MF; mf++)
+#pragma unroll
+                for (int nf = 0; nf < NF; nf++) {
+                    const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
+                    double y0 = pacc[mf][nf][0], y1 = pacc[mf][nf][1];
+                    if (EPI == EPI_STORE) {
+                        y0 *= g.alpha;   // alpha = 1 (exact) except for the fused final unscale
+                        y1 *= g.alpha;
+                    }
+                    if (EPI != EPI_STORE) {
+                        if (diag && r == c) ptr += y0;
+                        if (diag && r == c + 1) ptr += y1;
+                    }
+                    if (EPI == EPI_NS_H) {
+                        // H = 1/2 (3 delta - X) written as 1.5 delta - 0.5 x (the 1/2 is exact)
+                        const double d0 = (diag && r == c) ? 1.5 : 0.0, d1 = (diag && r == c + 1) ? 1.5 : 0.0;
+                        y0 = d0 - 0.5 * y0;
+                        y1 = d1 - 0.5 * y1;
+                    }
+                    pss = fma(y0, y0, pss);
+                    pss = fma(y1, y1, pss);
+                    pacc[mf][nf][0] = y0;
+                    pacc[mf][nf][1] = y1;
+                }
+        }
+        double *dst = g.c_pool + (int64_t)pseg * TILE;
+#pragma unroll
+        for (int mf = 0; mf < MF; mf++) {
+            if (mf % NKC != kc) continue;
+#pragma unroll
+            for (int nf = 0; nf < NF; nf++) {
+                const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
+                *reinterpret_cast<double2 *>(dst + r * B + ((((c >> 1) ^ swz(r))) << 1)) =
+                    make_double2(pacc[mf][nf][0], pacc[mf][nf][1]);
+            }
+        }
+        // xor-tree levels 16, 8, 4, 2, 1: level i in slice min(i, NKC - 1)
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            if ((i < NKC - 1 ? i : NKC - 1) != kc) continue;
+            const int o = 16 >> i;
+            pss += __shfl_xor_sync(0xffffffffu, pss, o);
+            if (EPI != EPI_STORE) ptr += __shfl_xor_sync(0xffffffffu, ptr, o);
+        }
+    };
+    // after the last slice: deposit the warp's partials; the last warp of the CTA to
+    // arrive sums the CW partials in warp order (deterministic) and writes the block's
+    // metadata.  No CTA barrier; warps drift apart by < QN segments (queue entries are
+    // released only when every warp has taken them) and a segment's deposit happens
+    // before its warp takes the segment after next, so RS = 2 QN slots are never
+    // reused early.
+    auto epi_deposit = [&]() {
+        if (lane == 0) {
+            double *rp = red + pslot * 2 * CW;
+            rp[warp] = pss;
+            rp[CW + warp] = ptr;
+            __threadfence_block();
+            if (atomicAdd(&rcnt[pslot], 1) == CW - 1) {
+                __threadfence_block();
+                double s2 = 0.0, t2 = 0.0;
+#pragma unroll
+                for (int w = 0; w < CW; w++) {
+                    s2 += *(volatile double *)&rp[w];
+                    t2 += *(volatile double *)&rp[CW + w];
+                }
+                rcnt[pslot] = 0;
+                const int I = morton_i(pcode), J = morton_j(pcode);
+                g.c_leaf_n2[pcode] = s2;
+                g.c_coord[pseg] = (int32_t)pcode;
+                g.c_slot[pcode] = pseg;
+                if (EPI != EPI_STORE && I == J) g.trace_part[I] = t2;
+            }
+        }
+    };
+
     int stage = 0, q = 0;
     uint32_t phase = 0, qphase = 0;
     int slot = 0;
@@ -198,12 +291,16 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
 #pragma unroll
             for (int j = 0; j < NF; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-        for (int it = 0; it < len; it++) {
+        // one task: wait for its stage, 16-wide k chunks of fragment loads + DMMAs; the
+        // WITH_EPI instance (first task of a segment with an epilogue pending) carries the
+        // epilogue slices in the same straight-line code as the DMMAs
+        auto task = [&](auto with_epi) {
+            constexpr bool WITH_EPI = decltype(with_epi)::value;
             mbar_wait(&full[stage], phase);
             const double *As = smem + (2 * stage) * TILE;
             const double *Bs = As + TILE;
 #pragma unroll
-            for (int kc = 0; kc < B / 16; kc++) {
+            for (int kc = 0; kc < NKC; kc++) {
                 // contraction index permuted inside the 16-wide chunk: k = 16kc + 4t + s
                 double a[MF][4], bf[NF][4];
 #pragma unroll
@@ -221,7 +318,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
                 for (int nf = 0; nf < NF; nf++)
 #pragma unroll
                     for (int s = 0; s < 4; s++) bf[nf][s] = Bs[boff[nf][s] + 16 * kc * B];
-                if (kc == B / 16 - 1) {
+                if (kc == NKC - 1) {
                     // Every read of this stage is issued: release it before the last chunk's
                     // DMMAs (which only need registers), so the refill starts a quarter task
                     // earlier and the fence's wait overlaps the previous chunk's DMMAs.  The
@@ -238,73 +335,34 @@ __global__ void __launch_bounds__(32 * (CW + 1)) k_leaf_gemm(GemmArgs g)
 #pragma unroll
                         for (int nf = 0; nf < NF; nf++)
                             dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s], bf[nf][s]);
+                if constexpr (WITH_EPI) epi_slice(kc);
             }
+            if constexpr (WITH_EPI) epi_deposit();
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
             }
-        }
-
-        // ---------------------------------------------------------- epilogue
-        const int I = morton_i(code), J = morton_j(code);
-        const bool diag = (I == J);
-        double *dst = g.c_pool + (int64_t)seg * TILE;
-        double ss = 0.0, tr = 0.0;
+        };
+        if (pseg >= 0) task(std::true_type{});
+        else task(std::false_type{});
+        for (int it = 1; it < len; it++) task(std::false_type{});
+        // park this segment's epilogue until the next segment's first task
 #pragma unroll
-        for (int mf = 0; mf < MF; mf++)
+        for (int i = 0; i < MF; i++)
 #pragma unroll
-            for (int nf = 0; nf < NF; nf++) {
-                const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
-                double y0 = acc[mf][nf][0], y1 = acc[mf][nf][1];
-                if (EPI == EPI_STORE) {
-                    y0 *= g.alpha;   // alpha = 1 (exact) except for the fused final unscale
-                    y1 *= g.alpha;
-                }
-                if (EPI != EPI_STORE) {
-                    if (diag && r == c) tr += y0;
-                    if (diag && r == c + 1) tr += y1;
-                }
-                if (EPI == EPI_NS_H) {
-                    // H = 1/2 (3 delta - X) written as 1.5 delta - 0.5 x (the 1/2 is exact)
-                    const double d0 = (diag && r == c) ? 1.5 : 0.0, d1 = (diag && r == c + 1) ? 1.5 : 0.0;
-                    y0 = d0 - 0.5 * y0;
-                    y1 = d1 - 0.5 * y1;
-                }
-                ss = fma(y0, y0, ss);
-                ss = fma(y1, y1, ss);
-                *reinterpret_cast<double2 *>(dst + r * B + ((((c >> 1) ^ swz(r))) << 1)) = make_double2(y0, y1);
+            for (int j = 0; j < NF; j++) {
+                pacc[i][j][0] = acc[i][j][0];
+                pacc[i][j][1] = acc[i][j][1];
             }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            tr += __shfl_xor_sync(0xffffffffu, tr, o);
-        }
-        // No CTA barrier: each warp deposits its partials in this segment's slot and
-        // the last warp to arrive sums the CW partials in warp order (deterministic)
-        // and writes the block's metadata; the others go on to the next segment.
-        // Warps drift apart by < QN segments (queue entries are released only when
-        // every warp has taken them), so RS = 2 QN slots are never reused early.
-        if (lane == 0) {
-            double *rp = red + slot * 2 * CW;
-            rp[warp] = ss;
-            rp[CW + warp] = tr;
-            __threadfence_block();
-            if (atomicAdd(&rcnt[slot], 1) == CW - 1) {
-                __threadfence_block();
-                double s2 = 0.0, t2 = 0.0;
-#pragma unroll
-                for (int w = 0; w < CW; w++) {
-                    s2 += *(volatile double *)&rp[w];
-                    t2 += *(volatile double *)&rp[CW + w];
-                }
-                rcnt[slot] = 0;
-                g.c_leaf_n2[code] = s2;
-                g.c_coord[seg] = (int32_t)code;
-                g.c_slot[code] = seg;
-                if (EPI != EPI_STORE && diag) g.trace_part[I] = t2;
-            }
-        }
+        pseg = seg;
+        pcode = code;
+        pslot = slot;
         if (++slot == RS) slot = 0;
+    }
+    if (pseg >= 0) {   // the CTA's last segment
+#pragma unroll
+        for (int kc = 0; kc < NKC; kc++) epi_slice(kc);
+        epi_deposit();
     }
 }
 

@@ -16,7 +16,34 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("-k", type=int, default=8)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--dense", type=int, default=0, help="instead: dense random n x n (b = 64), tau = 0")
 a = ap.parse_args()
+
+
+def timed(ctx, A, B, tau, reps):
+    best, st = 1e30, None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream) if ctx.stream is not None else e0.record()
+        C, st = sp.spamm_multiply(ctx, A, B, tau, want_stats=True)
+        e1.record(ctx.stream) if ctx.stream is not None else e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+        C.free()
+    return best, st
+
+
+if a.dense:
+    ctx = sp.spamm_ctx_create(0)
+    g = torch.Generator().manual_seed(1)
+    M = sp.spamm_build_tree(ctx, torch.randn(a.dense, a.dense, generator=g, dtype=torch.float64).cuda(), 64)
+    for _ in range(2):
+        best, st = timed(ctx, M, M, 0.0, a.reps)
+        print(f"dense n={a.dense}: tasks {st['tasks']} segments {st['segments']} "
+              f"({st['tasks'] / max(st['segments'], 1):.1f} per segment) {best:.3f} ms "
+              f"{st['flops'] / best / 1e9:.2f} TFLOP/s", flush=True)
+    sys.exit(0)
 cfg = si.CONFIGS[a.config]
 tau, tau_s = cfg.tau, cfg.tau * cfg.tau_s_factor
 kind, payload = si.make_input(cfg)
@@ -35,16 +62,7 @@ for _ in range(a.k):
     Z.free()
     Y, Z = Yn, Zn
 for name, (A, B) in (("Z*Y", (Z, Y)), ("Y*Z", (Y, Z))):
-    best, st = 1e30, None
-    for _ in range(a.reps):
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(ctx.stream) if hasattr(ctx, "stream") and ctx.stream is not None else e0.record()
-        C, st = sp.spamm_multiply(ctx, A, B, tau, want_stats=True)
-        e1.record(ctx.stream) if hasattr(ctx, "stream") and ctx.stream is not None else e1.record()
-        torch.cuda.synchronize()
-        best = min(best, e0.elapsed_time(e1))
-        C.free()
+    best, st = timed(ctx, A, B, tau, a.reps)
     print(f"{a.config} k={a.k} {name}: tasks {st['tasks']} segments {st['segments']} "
           f"({st['tasks'] / max(st['segments'], 1):.2f} per segment) {best:.3f} ms "
           f"{st['flops'] / best / 1e9:.2f} TFLOP/s", flush=True)
