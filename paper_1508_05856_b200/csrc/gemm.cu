@@ -27,6 +27,10 @@
 #include "scan.cuh"
 #include "tma.cuh"
 
+// EPI_STORE with alpha != 1 (C = alpha (A (x) B)): a separate instance, so the plain
+// store epilogue carries no multiply
+constexpr int EPI_STORE_SCALED = 3;
+
 struct GemmArgs {
     const double *a_pool, *b_pool;
     const double *b_halo;   // remote right-operand tiles (row partition): tB = -(h+1)
@@ -65,6 +69,7 @@ template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
 __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
 {
     static_assert(WM * WN == CW, "warp grid");
+    constexpr bool STORE = EPI == EPI_STORE || EPI == EPI_STORE_SCALED;
     constexpr int TM = B / WM, TN = B / WN;
     constexpr int MF = TM / 8, NF = TN / 8;
     constexpr int TILE = B * B;
@@ -199,11 +204,11 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
                 for (int nf = 0; nf < NF; nf++) {
                     const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
                     double y0 = pacc[mf][nf][0], y1 = pacc[mf][nf][1];
-                    if (EPI == EPI_STORE) {
-                        y0 *= g.alpha;   // alpha = 1 (exact) except for the fused final unscale
+                    if (EPI == EPI_STORE_SCALED) {   // the fused final unscale of an NS run
+                        y0 *= g.alpha;
                         y1 *= g.alpha;
                     }
-                    if (EPI != EPI_STORE) {
+                    if (!STORE) {
                         if (diag && r == c) ptr += y0;
                         if (diag && r == c + 1) ptr += y1;
                     }
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
             if ((i < NKC - 1 ? i : NKC - 1) != kc) continue;
             const int o = 16 >> i;
             pss += __shfl_xor_sync(0xffffffffu, pss, o);
-            if (EPI != EPI_STORE) ptr += __shfl_xor_sync(0xffffffffu, ptr, o);
+            if (!STORE) ptr += __shfl_xor_sync(0xffffffffu, ptr, o);
         }
     };
     // after the last slice: deposit the warp's partials; the last warp of the CTA to
@@ -264,7 +269,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
                 g.c_leaf_n2[pcode] = s2;
                 g.c_coord[pseg] = (int32_t)pcode;
                 g.c_slot[pcode] = pseg;
-                if (EPI != EPI_STORE && I == J) g.trace_part[I] = t2;
+                if (!STORE && I == J) g.trace_part[I] = t2;
             }
         }
     };
@@ -415,10 +420,12 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
     if (transA) {
         if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 1>(ctx, A->b, g);
         if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 1>(ctx, A->b, g);
+        if (g.alpha != 1.0) return gemm_dispatch<EPI_STORE_SCALED, 1>(ctx, A->b, g);
         return gemm_dispatch<EPI_STORE, 1>(ctx, A->b, g);
     }
     if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 0>(ctx, A->b, g);
     if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 0>(ctx, A->b, g);
+    if (g.alpha != 1.0) return gemm_dispatch<EPI_STORE_SCALED, 0>(ctx, A->b, g);
     return gemm_dispatch<EPI_STORE, 0>(ctx, A->b, g);
 }
 
