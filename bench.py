@@ -513,8 +513,26 @@ def run_ours(args):
     return 0
 
 
+def watchdog(seconds: float):
+    """A multi-rank run whose peer died would wait in a collective forever: after `seconds`
+    this rank reports and exits non-zero instead (SPAMM_BENCH_TIMEOUT, default 1 h; 0 = off)."""
+    if seconds <= 0:
+        return
+    import threading
+
+    def fire():
+        ws, rank, _ = dist_env()
+        print(json.dumps({"error": f"bench.py watchdog: rank {rank}/{ws} still running after {seconds:.0f} s"}),
+              file=sys.stderr, flush=True)
+        os._exit(3)
+    t = threading.Timer(seconds, fire)
+    t.daemon = True
+    t.start()
+
+
 def main():
     args = parse()
+    watchdog(float(os.environ.get("SPAMM_BENCH_TIMEOUT", "3600")))
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
