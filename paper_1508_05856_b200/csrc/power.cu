@@ -1,8 +1,13 @@
 // power.cu — c ~ ||s||_2 for the spectral rescale s <- s / s_{N-1} (P:380-381,
 // "easily obtained largest eigenvalue"; reading L12): K power steps from
-// v0 = 1/sqrt(n) * ones, then the Rayleigh quotient c = v^T s v.
-// Block-CSR SpMV (one CTA per block row, blocks in ascending column order,
-// warp-per-row dot products with fixed-order shuffle reductions: deterministic).
+// v0 = 1/sqrt(n) * ones, v <- w / ||w||, w = s v, then the Rayleigh quotient
+// c = v^T s v.  Block-CSR SpMV over the pool, every sum in a fixed order
+// (deterministic, no atomics):
+//   b = 64 : k_spmv_tma<64, SYM> — persistent, warp-specialised TMA ring; with s
+//            checked bitwise symmetric (k_sym_check) only the blocks on and above
+//            the block diagonal are read (SYM), the rest via column sums;
+//   b < 64 : k_spmv — register streaming (the ring's per-block synchronisation
+//            costs more than it saves on 8 / 2 KiB blocks).
 #include <cstdlib>
 
 #include "common.cuh"
