@@ -156,6 +156,31 @@ __host__ __device__ static inline int pool_col(int e, int b)
     return ((((q >> 1) ^ swz(r)) << 1) | (q & 1));
 }
 
+// Programmatic dependent launch, for chains of small dependent kernels on one stream
+// (the cull's levels, the power iteration): each kernel lets its successor launch at
+// once (griddepcontrol.launch_dependents) and each successor waits for its
+// predecessor's completion and memory (griddepcontrol.wait) before touching anything,
+// so the next launch's latency overlaps this kernel's tail.  Without the launch
+// attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // ------------------------------------------------------ small device->host reads
 // Counts and scalars are read back through a kernel that stores into mapped pinned
 // host memory, not cudaMemcpy: a small D2H copy queues behind any large transfer on

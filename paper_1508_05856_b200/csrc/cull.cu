@@ -75,8 +75,21 @@ __device__ __forceinline__ int clamp_n(const int32_t *cnt, int l, int64_t cap)
 // and counters[l0].  (Starting at l0 = 5 with <= 32 candidates per thread measured
 // slower than the extra scan/scatter pair: 6.6 vs 6.0 ms of cull per C2 run.)
 constexpr int INIT_L0 = 4;
+// zero the counters and the look-back tile flags of all levels (a kernel rather than
+// two memsets, so the whole query is one programmatic-dependent-launch chain)
+__global__ void k_cull_reset(int32_t *cnt, int ncnt, int32_t *flags, int64_t nflags)
+{
+    pdl_wait();
+    pdl_trigger();
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = i0; i < ncnt; i += stride) cnt[i] = 0;
+    for (int64_t i = i0; i < nflags; i += stride) flags[i] = 0;
+}
+
 __global__ void __launch_bounds__(1024) k_cull_init(CullArgs g, int l0, int4 *rec, int32_t *cnt)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int sw[32];
     __shared__ int gpre[(1 << (2 * INIT_L0)) + 1];   // exclusive prefix at each group (I,J) start
     const int S = 1 << l0;
@@ -141,6 +154,8 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
     __shared__ int4 sw[CT / 32];
     __shared__ int s_tile;
     __shared__ int4 s_excl;
+    pdl_wait();
+    pdl_trigger();
     // after a capacity overflow the truncated level's group indices point past the
     // arrays: skip the rest of the query (the host grows the workspace and re-runs)
     if (__ldcg(&cnt[CNT_OVERFLOW])) return;   // written by an earlier launch: a plain L2 load
@@ -231,6 +246,8 @@ __global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const i
                                                       int4 *rec_out, int32_t *tA, int32_t *tB,
                                                       int32_t *tK, const int32_t *cnt)
 {
+    pdl_wait();
+    pdl_trigger();
     if (cnt[CNT_OVERFLOW]) return;   // see k_cull_scan
     const int n = clamp_n(cnt, l, g.cap);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
@@ -276,6 +293,8 @@ __global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const i
 __global__ void k_cull_leaf_direct(CullArgs g, int l, const int4 *rec, int32_t *tA, int32_t *tB,
                                    int32_t *tK, const int32_t *cnt)
 {
+    pdl_wait();
+    pdl_trigger();
     if (cnt[CNT_OVERFLOW]) return;
     const int n = clamp_n(cnt, l, g.cap);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
@@ -295,6 +314,7 @@ __global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, in
 {
     __shared__ V1 sw[CT / 32];
     __shared__ int s_tile, s_excl;
+    pdl_wait();
     if (__ldcg(&cnt[CNT_OVERFLOW])) return;   // written by an earlier launch: a plain L2 load
     const int n = clamp_n(cnt, L, cap);
     int tile;
@@ -402,10 +422,19 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     cw->b = A->b;
     CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap, L, r0, r1, transA};
     cudaStream_t s = ctx->stream;
-    CK(cudaMemsetAsync(cw->counters, 0, sizeof(int32_t) * 64, s));
-    CK(cudaMemsetAsync(cw->tile_flag, 0, sizeof(int32_t) * (SPAMM_MAX_L + 2) * cw->tiles, s));
+    const int64_t nflags = (int64_t)(SPAMM_MAX_L + 2) * cw->tiles;
+    const int pdl = A->dist ? 0 : 1;   // row partition: the predecessor may be a collective
+    if (pdl) {
+        CK(launch_pdl(k_cull_reset, (int)std::min<int64_t>(cdiv(nflags, 256), 4 * ctx->sm_count), 256, 0, s,
+                      cw->counters, 64, cw->tile_flag, nflags));
+        CKL(ctx);
+    } else {
+        CK(cudaMemsetAsync(cw->counters, 0, sizeof(int32_t) * 64, s));
+        CK(cudaMemsetAsync(cw->tile_flag, 0, sizeof(int32_t) * nflags, s));
+    }
     int cur = 0;
-    k_cull_init<<<1, 1024, 0, s>>>(g, l0, cw->rec[cur], cw->counters);
+    if (pdl) CK(launch_pdl(k_cull_init, 1, 1024, 0, s, g, l0, cw->rec[cur], cw->counters));
+    else k_cull_init<<<1, 1024, 0, s>>>(g, l0, cw->rec[cur], cw->counters);
     CKL(ctx);
     const int persist = 2 * ctx->sm_count;
     int grid_scan = cw->tiles < persist ? (int)cw->tiles : persist;
@@ -414,29 +443,28 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     for (int l = l0; l < L; l++) {
         ScanTiles<int4> st{cw->tile_flag + (int64_t)(l - l0) * cw->tiles, cw->tile_agg, cw->tile_pre,
                            cw->counters + CNT_TICKET + l};
-        k_cull_scan<<<grid_scan, CT, 0, s>>>(g, l, cw->rec[cur], cw->mask, cw->pre, st, cw->counters);
+        CK(launch_pdl(k_cull_scan, grid_scan, CT, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre, st, cw->counters));
         CKL(ctx);
         if (l + 1 == L)
-            k_cull_scatter<true><<<grid_sc, 256, 0, s>>>(g, l, cw->rec[cur], cw->mask, cw->pre,
-                                                         cw->rec[cur ^ 1], cw->tA, cw->tB, cw->tK,
-                                                         cw->counters);
+            CK(launch_pdl(k_cull_scatter<true>, grid_sc, 256, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre,
+                          cw->rec[cur ^ 1], cw->tA, cw->tB, cw->tK, cw->counters));
         else
-            k_cull_scatter<false><<<grid_sc, 256, 0, s>>>(g, l, cw->rec[cur], cw->mask, cw->pre,
-                                                          cw->rec[cur ^ 1], nullptr, nullptr, nullptr,
-                                                          cw->counters);
+            CK(launch_pdl(k_cull_scatter<false>, grid_sc, 256, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre,
+                          cw->rec[cur ^ 1], (int32_t *)nullptr, (int32_t *)nullptr, (int32_t *)nullptr,
+                          cw->counters));
         CKL(ctx);
         cur ^= 1;
     }
     if (l0 == L) {
-        k_cull_leaf_direct<<<grid_sc, 256, 0, s>>>(g, L, cw->rec[cur], cw->tA, cw->tB, cw->tK,
-                                                   cw->counters);
+        CK(launch_pdl(k_cull_leaf_direct, grid_sc, 256, 0, s, g, L, cw->rec[cur], cw->tA, cw->tB, cw->tK,
+                      cw->counters));
         CKL(ctx);
     }
     cw->final_buf = cur;
     ScanTiles<V1> st{cw->tile_flag + (int64_t)(SPAMM_MAX_L + 1) * cw->tiles, (V1 *)cw->tile_agg,
                      (V1 *)cw->tile_pre, cw->counters + CNT_TICKET + SPAMM_MAX_L + 1};
-    k_cull_segments<<<grid_scan, CT, 0, s>>>(cw->rec[cur], L, cw->cap, cw->cap_segs, st, cw->seg_code,
-                                             cw->seg_start, cw->seg_len, cw->counters);
+    CK(launch_pdl(k_cull_segments, grid_scan, CT, 0, s, cw->rec[cur], L, cw->cap, cw->cap_segs, st, cw->seg_code,
+                  cw->seg_start, cw->seg_len, cw->counters));
     CKL(ctx);
     return SPAMM_OK;
 }

@@ -79,6 +79,8 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
                                               const int32_t *cols, const int32_t *slots,
                                               const double *v, double *w, int32_t *ticket, int nunits)
 {
+    pdl_wait();
+    pdl_trigger();
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
     __shared__ int s_unit;
     for (;;) {
@@ -188,6 +190,8 @@ template <int B, bool SYM>
 __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_t *up, const int32_t *mir,
                                                           double *colpart)
 {
+    pdl_wait();
+    pdl_trigger();
     using Cf = SptCfg<B>;
     constexpr int TILE = B * B, STAGES = Cf::STAGES, LPR = Cf::LPR, M = Cf::M, RPW = Cf::RPW, N2 = Cf::N2;
     constexpr int NSUB = 256 / B, RS = B / NSUB;   // column pass: row subsets, rows per subset
@@ -334,6 +338,8 @@ __global__ void __launch_bounds__(256) k_spmv_sym_fix(const int32_t *rowptr, con
                                                       const double *part, const double *colpart, int nb,
                                                       int b, double *w, double *nrm_part)
 {
+    pdl_wait();
+    pdl_trigger();
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double t = 0.0;
     if (e < (int64_t)nb * b) {
@@ -417,6 +423,8 @@ __global__ void __launch_bounds__(256) k_sym_check(const double *pool, const int
 __global__ void __launch_bounds__(256) k_spmv_fix(const int32_t *rowptr, const double *part, int nb, int b,
                                                   double *w, double *nrm_part)
 {
+    pdl_wait();
+    pdl_trigger();
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double t = 0.0;
     if (e < (int64_t)nb * b) {
@@ -439,6 +447,8 @@ __global__ void __launch_bounds__(256) k_spmv_fix(const int32_t *rowptr, const d
 __global__ void __launch_bounds__(256) k_norm_apply(const double *w, int64_t n, const double *nrm_part, int np,
                                                     double *v)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double sh[256];
     double s = 0.0;
     for (int i = threadIdx.x; i < np; i += 256) s += nrm_part[i];
@@ -456,6 +466,8 @@ __global__ void __launch_bounds__(256) k_norm_apply(const double *w, int64_t n, 
 // single CTA: nrm = sqrt(sum w^2) (fixed order); v = w / nrm
 __global__ void k_normalize(const double *w, int64_t n, double *v)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double sh[1024];
     double s = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += 1024) s = fma(w[i], w[i], s);
@@ -475,6 +487,8 @@ __global__ void k_normalize(const double *w, int64_t n, double *v)
 constexpr int NRM_CTAS = 128;
 __global__ void __launch_bounds__(256) k_sumsq_part(const double *w, int64_t n, double *part)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double sh[256];
     const int64_t chunk = (n + NRM_CTAS - 1) / NRM_CTAS, i0 = blockIdx.x * chunk;
     const int64_t i1 = i0 + chunk < n ? i0 + chunk : n;
@@ -491,6 +505,8 @@ __global__ void __launch_bounds__(256) k_sumsq_part(const double *w, int64_t n, 
 
 __global__ void __launch_bounds__(256) k_scale_by_norm(const double *w, int64_t n, const double *part, double *v)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double nrm;
     if (threadIdx.x == 0) {
         double t = 0.0;
@@ -511,6 +527,8 @@ __global__ void k_fill(double *v, int64_t n, double val)
 
 __global__ void k_dot(const double *a, const double *b, int64_t n, double *out)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double sh[1024];
     double s = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += 1024) s = fma(a[i], b[i], s);
@@ -535,9 +553,17 @@ static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, 
         return cudaFuncSetAttribute(k_spmv_tma<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }));
     SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
-    k_spmv_tma<B, false><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, nullptr, nullptr, nullptr);
-    CKL(ctx);
-    k_spmv_fix<<<cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream>>>(rowptr, part, s->nb, B, w, nrm_part);
+    if (s->dist) {   // the predecessor is a collective: plain launches
+        k_spmv_tma<B, false><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, nullptr, nullptr, nullptr);
+        CKL(ctx);
+        k_spmv_fix<<<cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream>>>(rowptr, part, s->nb, B, w, nrm_part);
+    } else {
+        CK(launch_pdl(k_spmv_tma<B, false>, ctx->sm_count, 288, smem, ctx->stream, g, (const int32_t *)nullptr,
+                      (const int32_t *)nullptr, (double *)nullptr));
+        CKL(ctx);
+        CK(launch_pdl(k_spmv_fix, (int)cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream, rowptr, part, s->nb, B, w,
+                      nrm_part));
+    }
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -559,10 +585,10 @@ static spamm_status spmv_sym(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, 
         return cudaFuncSetAttribute(k_spmv_tma<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }));
     SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
-    k_spmv_tma<B, true><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, y.up, y.mir, y.colpart);
+    CK(launch_pdl(k_spmv_tma<B, true>, ctx->sm_count, 288, smem, ctx->stream, g, y.up, y.mir, y.colpart));
     CKL(ctx);
-    k_spmv_sym_fix<<<cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream>>>(rowptr, y.up, part, y.colpart,
-                                                                          s->nb, B, w, nrm_part);
+    CK(launch_pdl(k_spmv_sym_fix, (int)cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream, rowptr, y.up, part,
+                  (const double *)y.colpart, s->nb, B, w, nrm_part));
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -582,7 +608,8 @@ static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_
     const int nunits = s->nb * CPR;
     int grid = ctx->sm_count * occ;
     if (grid > nunits) grid = nunits;
-    k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
+    if (s->dist) k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
+    else launch_pdl(k_spmv<B>, grid, 256, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits);
     ctx->launches++;
 }
 
@@ -694,13 +721,15 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     for (int it = 0; it < K; it++) {
         ST(mv(v, w));
         if (fused) {
-            k_norm_apply<<<(int)std::min<int64_t>(NRM_CTAS, np), 256, 0, st>>>(w, n, nrm_part, np, v);
+            CK(launch_pdl(k_norm_apply, (int)std::min<int64_t>(NRM_CTAS, np), 256, 0, st, (const double *)w, n,
+                          (const double *)nrm_part, np, v));
         } else if (n >= (1 << 16)) {
             k_sumsq_part<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1);
             k_scale_by_norm<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1, v);
             ctx->launches++;
         } else {
-            k_normalize<<<1, 1024, 0, st>>>(w, n, v);
+            if (s->dist) k_normalize<<<1, 1024, 0, st>>>(w, n, v);
+            else CK(launch_pdl(k_normalize, 1, 1024, 0, st, (const double *)w, n, v));
         }
         ctx->launches++;
     }
