@@ -181,6 +181,21 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, size_t s
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// with PDL on a single device; a plain launch when the context has a communicator
+// (row partition: the predecessor on the stream may be a collective or a copy)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(spamm_ctx ctx, void (*k)(KArgs...), int grid, int block, size_t smem, Args... args)
+{
+    if (ctx->comm == nullptr) return launch_pdl(k, grid, block, smem, ctx->stream, args...);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cfg.numAttrs = 0;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // ------------------------------------------------------ small device->host reads
 // Counts and scalars are read back through a kernel that stores into mapped pinned
 // host memory, not cudaMemcpy: a small D2H copy queues behind any large transfer on

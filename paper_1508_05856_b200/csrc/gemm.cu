@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
     int *rcnt = reinterpret_cast<int *>(red + RS * 2 * CW);   // [RS] warps done per slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    pdl_trigger();   // the epilogue-side kernels that follow may stage their launch now
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full[s], 1);
@@ -490,6 +491,8 @@ template <int THREADS>
 __global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int r0, int r1, int64_t base,
                               int32_t *newslot, int64_t *count_out)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ V1 sw[THREADS / 32];
     int64_t run = 0;
     for (int i0 = 0; i0 < nb; i0 += THREADS) {
@@ -515,6 +518,8 @@ __global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int r0,
 __global__ void k_diag_fill(const int32_t *newslot, double *pool, int b, double value,
                             double *leaf_n2)
 {
+    pdl_wait();
+    pdl_trigger();
     int i = blockIdx.x;
     int s = newslot[i];
     if (s < 0) return;
@@ -531,10 +536,11 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
 {
     int32_t *newslot = dalloc<int32_t>(ctx, m->nb);
     if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
-    k_diag_assign<1024><<<1, 1024, 0, ctx->stream>>>(m->slot, m->coord, m->nb, m->r0, m->r1, base, newslot,
-                                                    ctx->iscratch);
+    CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, m->slot, m->coord, m->nb, m->r0, m->r1, base, newslot,
+                ctx->iscratch));
     CKL(ctx);
-    k_diag_fill<<<m->nb, 256, 0, ctx->stream>>>(newslot, m->pool, m->b, value, m->norm2 + pyr_off(m->L));
+    CK(launch_k(ctx, k_diag_fill, m->nb, 256, 0, (const int32_t *)newslot, m->pool, m->b, value,
+                m->norm2 + pyr_off(m->L)));
     CKL(ctx);
     int64_t h = 0;
     ST(fetch1(ctx, ctx->iscratch, &h, sizeof(int64_t)));
@@ -547,9 +553,10 @@ spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double v
 {
     int32_t *newslot = dalloc<int32_t>(ctx, H->nb);
     if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
-    k_diag_assign<1024><<<1, 1024, 0, ctx->stream>>>(H->slot, H->coord, H->nb, H->r0, H->r1, nseg, newslot, dcount);
+    CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, nseg, newslot, dcount));
     CKL(ctx);
-    k_diag_fill<<<H->nb, 256, 0, ctx->stream>>>(newslot, H->pool, H->b, value, H->norm2 + pyr_off(H->L));
+    CK(launch_k(ctx, k_diag_fill, H->nb, 256, 0, (const int32_t *)newslot, H->pool, H->b, value,
+                H->norm2 + pyr_off(H->L)));
     CKL(ctx);
     dev_free(ctx, newslot, sizeof(int32_t) * H->nb);
     H->nblk = nseg;   // provisional until the caller has fetched *dcount
@@ -567,6 +574,8 @@ spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value)
 // t = (n - sum_i trace_part[i]) / n, fixed-order single-CTA reduction
 __global__ void k_trace_finish(const double *part, int nb, double n, double *t_out)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double sh[256];
     double s = 0.0;
     for (int i = threadIdx.x; i < nb; i += 256) s += part[i];
@@ -581,7 +590,7 @@ __global__ void k_trace_finish(const double *part, int nb, double n, double *t_o
 
 spamm_status trace_finish(spamm_ctx ctx, const double *trace_part, int nb, int64_t n, double *t_out)
 {
-    k_trace_finish<<<1, 256, 0, ctx->stream>>>(trace_part, nb, (double)n, t_out);
+    CK(launch_k(ctx, k_trace_finish, 1, 256, 0, trace_part, nb, (double)n, t_out));
     CKL(ctx);
     return SPAMM_OK;
 }

@@ -286,6 +286,8 @@ __global__ void k_build_scatter(BlockSrc src, int64_t count, const int32_t *slot
 template <int LV>
 __global__ void k_pyramid(double *norm2, int lf, int levels)
 {
+    pdl_wait();
+    pdl_trigger();
     constexpr int N = 1 << (2 * LV);
     __shared__ double buf[N];
     const int64_t base = (int64_t)blockIdx.x * N;
@@ -322,11 +324,11 @@ static spamm_status pyramid_kernels(spamm_ctx ctx, spamm_mat m)
         int64_t cnt = int64_t(1) << (2 * lf);
         int grid = cdiv(cnt, int64_t(1) << (2 * lv));
         switch (lv) {
-        case 5: k_pyramid<5><<<grid, 256, 0, ctx->stream>>>(m->norm2, lf, 5); break;
-        case 4: k_pyramid<4><<<grid, 256, 0, ctx->stream>>>(m->norm2, lf, 4); break;
-        case 3: k_pyramid<3><<<grid, 64, 0, ctx->stream>>>(m->norm2, lf, 3); break;
-        case 2: k_pyramid<2><<<grid, 16, 0, ctx->stream>>>(m->norm2, lf, 2); break;
-        default: k_pyramid<1><<<grid, 4, 0, ctx->stream>>>(m->norm2, lf, 1); break;
+        case 5: CK(launch_k(ctx, k_pyramid<5>, grid, 256, 0, m->norm2, lf, 5)); break;
+        case 4: CK(launch_k(ctx, k_pyramid<4>, grid, 256, 0, m->norm2, lf, 4)); break;
+        case 3: CK(launch_k(ctx, k_pyramid<3>, grid, 64, 0, m->norm2, lf, 3)); break;
+        case 2: CK(launch_k(ctx, k_pyramid<2>, grid, 16, 0, m->norm2, lf, 2)); break;
+        default: CK(launch_k(ctx, k_pyramid<1>, grid, 4, 0, m->norm2, lf, 1)); break;
         }
         CKL(ctx);
         lf -= lv;
