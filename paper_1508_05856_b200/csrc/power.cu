@@ -594,8 +594,8 @@ static spamm_status spmv_sym(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, 
 }
 
 template <int B>
-static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
-                 const int32_t *slots, const double *v, double *w, int32_t *ticket)
+static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
+                         const int32_t *slots, const double *v, double *w, int32_t *ticket)
 {
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
     static std::atomic<int> occ_cache{0};
@@ -609,8 +609,9 @@ static void spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_
     int grid = ctx->sm_count * occ;
     if (grid > nunits) grid = nunits;
     if (s->dist) k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
-    else launch_pdl(k_spmv<B>, grid, 256, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits);
-    ctx->launches++;
+    else CK(launch_pdl(k_spmv<B>, grid, 256, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits));
+    CKL(ctx);
+    return SPAMM_OK;
 }
 
 // SPAMM_SPMV_TMA=0 selects the register-streaming SpMV (k_spmv) instead of the TMA
@@ -712,9 +713,9 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
             return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
         }
         switch (s->b) {
-        case 16: spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk); break;
-        case 32: spmv<32>(ctx, s, rowptr, cols, slots, x, y, tk); break;
-        default: spmv<64>(ctx, s, rowptr, cols, slots, x, y, tk); break;
+        case 16: ST(spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk)); break;
+        case 32: ST(spmv<32>(ctx, s, rowptr, cols, slots, x, y, tk)); break;
+        default: ST(spmv<64>(ctx, s, rowptr, cols, slots, x, y, tk)); break;
         }
         return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
     };
