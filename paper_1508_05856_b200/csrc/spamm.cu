@@ -380,6 +380,11 @@ struct FinalScale {
     double t_stop;   // > 0: also last when |t_k| <= t_stop
     double f;
     bool applied;    // out: Y', Z' were written unscaled
+    // single device: the next step's X = Z' (x) Y' cull is enqueued before this step's
+    // closing fetch and read back with it (one host round trip per step fewer)
+    bool chain = false;        // in: a next step follows unless this one is the last
+    bool x_ready = false;      // in: ctx->cw[0] already holds this step's X cull
+    bool x_next_ready = false; // out: ctx->cw[0] holds the next step's X cull
 };
 
 // Single device: the step with three host round trips instead of five.  The X product
@@ -395,7 +400,7 @@ static spamm_status ns_step_batched(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, dou
     int64_t *ddiag = ctx->iscratch + 1;
     spamm_mat H = nullptr;
     spamm_status st = product(ctx, ctx->cw[0], Z, Y, tau, map ? EPI_NS_X : EPI_NS_H, trace_part, &H, 0, 1.0,
-                              false, map ? nullptr : ddiag);
+                              fs && fs->x_ready, map ? nullptr : ddiag);
     const int64_t nseg = ctx->cw[0]->nsegs;
     if (!st) st = trace_finish(ctx, trace_part, nb, Y->n, ctx->dscratch);
     if (!st && map) st = ns_scaled_map(ctx, H, ctx->dscratch, ctx->dscratch + 8);
@@ -449,10 +454,23 @@ static spamm_status ns_step_impl(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double
     if (!Y->dist) {
         spamm_status sb = ns_step_batched(ctx, Y, Z, tau, tau_s, map, trace_part, &H, &Yn, &Zn, stats, fs);
         double hv[3] = {0, 0, 0}, ae[2] = {1.0, 0.0};
+        // the next step's X cull rides on this step's closing fetch (wasted only if the
+        // step turns out non-finite)
+        const bool chain = !sb && fs && fs->chain && !fs->applied;
+        if (chain) {
+            int pc = prof_begin(ctx, SPAMM_PH_CULL);
+            sb = cull_start(ctx, ctx->cw[0], Zn, Yn, tau, Zn->r0, Zn->r1);
+            prof_end(ctx, pc);
+        }
         if (!sb) {
-            FetchItem it[4] = {{ctx->dscratch, &hv[0], 8}, {Yn->norm2, &hv[1], 8}, {Zn->norm2, &hv[2], 8},
-                               {ctx->dscratch + 8, ae, 16}};
-            sb = fetch(ctx, it, map ? 4 : 3);
+            FetchItem it[5] = {{ctx->dscratch, &hv[0], 8}, {Yn->norm2, &hv[1], 8}, {Zn->norm2, &hv[2], 8},
+                               {ctx->dscratch + 8, ae, 16}, {ctx->cw[0]->counters, ctx->cw[0]->hcnt, 256}};
+            if (chain && !map) it[3] = it[4];
+            sb = fetch(ctx, it, 3 + (map ? 1 : 0) + (chain ? 1 : 0));
+        }
+        if (!sb && chain && std::isfinite(hv[0]) && std::isfinite(hv[1]) && std::isfinite(hv[2])) {
+            sb = cull_complete(ctx, ctx->cw[0], Zn, Yn, tau, Zn->r0, Zn->r1);
+            if (!sb) fs->x_next_ready = true;
         }
         dev_free(ctx, trace_part, sizeof(double) * nb);
         if (sb) {
@@ -579,12 +597,16 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
     int pl = prof_begin(ctx, SPAMM_PH_LOOP);
     const double f = std::sqrt(c * (1.0 + mu));
     bool unscaled = false;   // Y, Z already hold the outputs (final unscale fused)
+    bool x_ready = false;    // ctx->cw[0] holds the coming step's X cull (chained fetch)
     for (int k = 0; k < iters && !st; k++) {
         spamm_mat Yn = nullptr, Zn = nullptr;
         double t = 0.0;
         spamm_stats sts[3];
         FinalScale fs{k == iters - 1, o.t_stop, f, false};
+        fs.chain = k + 1 < iters;
+        fs.x_ready = x_ready;
         st = ns_step_impl(ctx, Y, Z, tau, tau_s, o.map, &Yn, &Zn, nullptr, &t, sts, nullptr, &fs);
+        x_ready = fs.x_next_ready;
         if (o.t_history && (st == SPAMM_OK || st == SPAMM_ENOTFINITE)) o.t_history[k] = t;
         if (o.per_product && st == SPAMM_OK) memcpy(o.per_product + 3 * k, sts, sizeof(sts));
         if (st) {
