@@ -76,3 +76,33 @@ def test_selfcheck_reports_no_mismatch(gpu):
     assert p.returncode == 0, p.stderr[-2000:]
     assert "ok 12" in p.stdout
     assert "SELFCHECK" not in p.stderr, p.stderr[-2000:]
+
+
+def test_ns_sqrt_chained_equals_step_loop(gpu):
+    """spamm_ns_sqrt enqueues each step's X cull before the previous step's closing fetch
+    (and fuses the final unscale); a plain loop of spamm_ns_step does neither.  Same t_k
+    sequence bitwise, same task counts, same iterates (up to the unscale's rounding)."""
+    n, b, iters, c = 4096, 64, 6, 11.0
+    cfg = si.Config("t", "gauss", n, b, 1e-7, 30, sigma=0.8, shift=1e-3, seed=150805856, tau_min=1e-7)
+    payload = si.make_input(cfg)[1]
+    ctx = sp().spamm_ctx_create(0)
+    S = sp().spamm_build_tree_blocks(ctx, n, b, *payload)
+    r = sp().spamm_ns_sqrt(ctx, S, 1e-7, iters, tau_s=1e-9, scale=c)
+    Y, Z = sp().spamm_ns_y0(ctx, S, c), sp().spamm_identity(ctx, n, b)
+    ts, counts = [], []
+    for _ in range(iters):
+        Yn, Zn, t, st = sp().spamm_ns_step(ctx, Y, Z, 1e-7, 1e-9)
+        ts.append(t)
+        counts.append([s["tasks"] for s in st])
+        Y.free()
+        Z.free()
+        Y, Z = Yn, Zn
+    assert np.array_equal(np.asarray(ts), r["t"])
+    assert counts == [[s["tasks"] for s in k] for k in r["stats"]]
+    f = np.sqrt(c)
+    for M, ref, scale in ((r["Y"], Y, f), (r["Z"], Z, 1.0 / f)):
+        bi, bj, blk = sp().spamm_export_blocks(ctx, M)
+        ri, rj, rblk = sp().spamm_export_blocks(ctx, ref)
+        o, q = np.lexsort((bj, bi)), np.lexsort((rj, ri))
+        assert np.array_equal(bi[o], ri[q]) and np.array_equal(bj[o], rj[q])
+        np.testing.assert_allclose(blk[o], rblk[q] * scale, rtol=4e-16, atol=0)
