@@ -248,7 +248,12 @@ spamm_status spamm_ns_sqrt_single(spamm_ctx ctx, spamm_mat s, double tau, int32_
 spamm_status spamm_regularized_factor(spamm_ctx ctx, spamm_mat s, double tau0, double tau1, const double *mu,
                                       int32_t nslices, int32_t iters, double t_stop, double scale, spamm_mat *G,
                                       double *c_out, int32_t *slice_iters);
-/* Scale estimate c ~ ||s||_2: K power steps from 1/sqrt(n) * ones, Rayleigh quotient. */
+/* Scale estimate c ~ ||s||_2 ("easily obtained largest eigenvalue"; DESIGN.md
+ * reading L12): K power steps v <- w/||w||, w = s v, from v_0 = 1/sqrt(n) * ones, then the
+ * Rayleigh quotient c = v^T s v; every sum in a fixed order (deterministic).  s is read
+ * as stored: when it is bitwise symmetric (checked on the device once per call) only its
+ * blocks on and above the block diagonal are streamed (half the HBM traffic, same
+ * result up to summation order); otherwise all of it.  *c: host.  Synchronises. */
 spamm_status spamm_power_scale(spamm_ctx ctx, spamm_mat s, int32_t K, double *c);
 /* Y0 = s/c (mu = 0) or (s/c + mu I)/(1+mu). */
 spamm_status spamm_ns_y0(spamm_ctx ctx, spamm_mat s, double c, double mu, spamm_mat *Y0);
