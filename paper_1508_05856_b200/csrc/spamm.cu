@@ -103,7 +103,8 @@ static spamm_status check_pair(spamm_ctx ctx, spamm_mat A, spamm_mat B, double t
 }
 
 // SPAMM_LPT=1 turns on a longest-first GEMM schedule (measured: -0.4 % GEMM time but
-// +0.5 % step time on C3 from its three extra launches per product, so off by default)
+// +0.5 % step time on C3 from its three extra launches per product, and 4 % slower
+// products at C5, where it breaks the Morton order's L2 reuse; off by default)
 static int lpt_mode()
 {
     static const int m = [] {   // initialised once, thread-safely (C++11)
@@ -156,7 +157,7 @@ static void *snapshot(spamm_ctx ctx, const void *src, int64_t bytes)
     return p;
 }
 
-static int64_t g_product_id = 0;
+static std::atomic<int64_t> g_product_id{0};   // SELFCHECK log label (ranks may be threads)
 
 static void selfcheck_cull(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int transA)
 {
@@ -178,7 +179,7 @@ static void selfcheck_cull(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, do
     }
     if (m[0] || m[1] || m[2] || m[3] || m[4])
         fprintf(stderr, "SELFCHECK cull mismatch product %lld: counts %lld/%lld vs %lld/%lld, tA %lld tB %lld code %lld start %lld len %lld\n",
-                (long long)g_product_id, (long long)nt, (long long)ns, (long long)cw->ntasks, (long long)cw->nsegs,
+                (long long)g_product_id.load(), (long long)nt, (long long)ns, (long long)cw->ntasks, (long long)cw->nsegs,
                 m[0], m[1], m[2], m[3], m[4]);
     for (void *q : {tA, tB, sc, ss, sl}) dev_free(ctx, q, 1);
 }
@@ -199,7 +200,7 @@ static void selfcheck_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, co
     long long m1 = cmp_words(ctx, C->norm2 + pyr_off(C->L), m2->norm2 + pyr_off(C->L), 8 * (int64_t)A->nb * A->nb, &f1);
     if (m0 || m1)
         fprintf(stderr, "SELFCHECK gemm mismatch product %lld epi %d: pool words %lld (first block %lld), leaf n2 words %lld; tasks %lld segs %lld\n",
-                (long long)g_product_id, epi, m0, f0 / (2 * b2), m1, (long long)cw->ntasks, (long long)cw->nsegs);
+                (long long)g_product_id.load(), epi, m0, f0 / (2 * b2), m1, (long long)cw->ntasks, (long long)cw->nsegs);
     dev_free(ctx, tr, 8 * A->nb);
     spamm_mat_free(m2);
 }
