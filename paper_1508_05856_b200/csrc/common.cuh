@@ -293,6 +293,11 @@ struct Cull {
     int L = 0, l0 = 0, b = 0;
     int64_t ntasks = 0, nsegs = 0;  // host copies after cull_sync
     int64_t hint = 0;             // capacity hint for the next use
+    // level sizes of the previous accepted query on this workspace (grid sizing of the
+    // next one: consecutive NS products of one role have similar levels; the kernels
+    // loop over their work, so any grid is correct)
+    int prevL = -1;
+    int32_t prev[SPAMM_MAX_L + 2] = {};
     double alpha = 1.0;           // EPI_STORE output scale of the next GEMM (fused unscale)
     spamm_stats stats{};
 };

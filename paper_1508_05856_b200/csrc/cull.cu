@@ -437,33 +437,43 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     else k_cull_init<<<1, 1024, 0, s>>>(g, l0, cw->rec[cur], cw->counters);
     CKL(ctx);
     const int persist = 2 * ctx->sm_count;
-    int grid_scan = cw->tiles < persist ? (int)cw->tiles : persist;
-    int grid_sc = cdiv(cw->cap, 256);
-    if (grid_sc > 4 * ctx->sm_count) grid_sc = 4 * ctx->sm_count;
+    // grids sized from the previous query's level counts (+25 %), else the capacity
+    const bool have_prev = cw->prevL == L;
+    auto expect = [&](int l) -> int64_t {
+        return have_prev ? (int64_t)cw->prev[l] + cw->prev[l] / 4 + 1 : cw->cap;
+    };
+    auto scan_grid = [&](int l) -> int {
+        const int64_t t = cdiv(expect(l), (int64_t)CT * CI);
+        return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(t, cw->tiles), persist));
+    };
+    auto flat_grid = [&](int l) -> int {
+        return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::min(expect(l), cw->cap), 256),
+                                                            4 * ctx->sm_count));
+    };
     for (int l = l0; l < L; l++) {
         ScanTiles<int4> st{cw->tile_flag + (int64_t)(l - l0) * cw->tiles, cw->tile_agg, cw->tile_pre,
                            cw->counters + CNT_TICKET + l};
-        CK(launch_pdl(k_cull_scan, grid_scan, CT, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre, st, cw->counters));
+        CK(launch_pdl(k_cull_scan, scan_grid(l), CT, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre, st, cw->counters));
         CKL(ctx);
         if (l + 1 == L)
-            CK(launch_pdl(k_cull_scatter<true>, grid_sc, 256, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre,
+            CK(launch_pdl(k_cull_scatter<true>, flat_grid(l), 256, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre,
                           cw->rec[cur ^ 1], cw->tA, cw->tB, cw->tK, cw->counters));
         else
-            CK(launch_pdl(k_cull_scatter<false>, grid_sc, 256, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre,
+            CK(launch_pdl(k_cull_scatter<false>, flat_grid(l), 256, 0, s, g, l, cw->rec[cur], cw->mask, cw->pre,
                           cw->rec[cur ^ 1], (int32_t *)nullptr, (int32_t *)nullptr, (int32_t *)nullptr,
                           cw->counters));
         CKL(ctx);
         cur ^= 1;
     }
     if (l0 == L) {
-        CK(launch_pdl(k_cull_leaf_direct, grid_sc, 256, 0, s, g, L, cw->rec[cur], cw->tA, cw->tB, cw->tK,
+        CK(launch_pdl(k_cull_leaf_direct, flat_grid(L), 256, 0, s, g, L, cw->rec[cur], cw->tA, cw->tB, cw->tK,
                       cw->counters));
         CKL(ctx);
     }
     cw->final_buf = cur;
     ScanTiles<V1> st{cw->tile_flag + (int64_t)(SPAMM_MAX_L + 1) * cw->tiles, (V1 *)cw->tile_agg,
                      (V1 *)cw->tile_pre, cw->counters + CNT_TICKET + SPAMM_MAX_L + 1};
-    CK(launch_pdl(k_cull_segments, grid_scan, CT, 0, s, cw->rec[cur], L, cw->cap, cw->cap_segs, st, cw->seg_code,
+    CK(launch_pdl(k_cull_segments, scan_grid(L), CT, 0, s, cw->rec[cur], L, cw->cap, cw->cap_segs, st, cw->seg_code,
                   cw->seg_start, cw->seg_len, cw->counters));
     CKL(ctx);
     return SPAMM_OK;
@@ -481,6 +491,8 @@ static void cull_accept(spamm_ctx ctx, Cull *cw)
     for (int l = cw->l0; l <= cw->L && l < 24; l++) s.level_survivors[l] = cw->hcnt[l];
     s.candidates = cw->L > cw->l0 ? 8 * (int64_t)cw->hcnt[cw->L - 1] : ((int64_t)1 << (3 * cw->L));
     s.flops = 2.0 * (double)cw->b * cw->b * cw->b * (double)cw->ntasks;
+    cw->prevL = cw->L;
+    for (int l = 0; l <= cw->L && l < SPAMM_MAX_L + 2; l++) cw->prev[l] = l >= cw->l0 ? cw->hcnt[l] : 0;
     // next capacity hint: 25% headroom over the largest level seen
     int64_t mx = 0;
     for (int l = cw->l0; l <= cw->L; l++) mx = cw->hcnt[l] > mx ? cw->hcnt[l] : mx;
