@@ -106,3 +106,19 @@ def test_ns_sqrt_chained_equals_step_loop(gpu):
         o, q = np.lexsort((bj, bi)), np.lexsort((rj, ri))
         assert np.array_equal(bi[o], ri[q]) and np.array_equal(bj[o], rj[q])
         np.testing.assert_allclose(blk[o], rblk[q] * scale, rtol=4e-16, atol=0)
+
+
+def test_allocators_agree_bitwise(gpu):
+    """The library's own stream-ordered allocator (cudaMallocAsync: allocation nodes sit
+    between the programmatically dependent launches) and PyTorch's caching allocator give
+    the same NS run bitwise."""
+    c = si.CONFIGS["C2"]
+    s = si.kms(c.n, c.rho)
+    out = []
+    for torch_alloc in (True, False):
+        ctx = sp().spamm_ctx_create(0, torch_allocator=torch_alloc)
+        S = sp().spamm_build_tree(ctx, s, c.b)
+        r = sp().spamm_ns_sqrt(ctx, S, c.tau, 10)
+        out.append((r["t"].copy(), _hash(ctx, r["Y"]), _hash(ctx, r["Z"]), r["c"]))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1:] == out[1][1:]
