@@ -316,6 +316,26 @@ def run_ours(args):
     # ---- FP64 tensor peak on this GPU (DMMA issue-rate microbenchmark, ~2 s sustained)
     _, ms1 = sp.spamm_peak_dmma(ctx, 20000)
     peak_tflops, peak_ms = sp.spamm_peak_dmma(ctx, int(20000 * max(1.0, 2000.0 / max(ms1, 1e-3))))
+    # cross-check of the denominator: a library FP64 GEMM (cuBLAS DGEMM via torch.matmul),
+    # 8192^3, best of 5 (context only; not used in any ratio)
+    dgemm_tflops = None
+    try:
+        ga = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+        gb = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+        torch.matmul(ga, gb)
+        best = 1e30
+        for _ in range(5):
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            torch.matmul(ga, gb)
+            g1.record()
+            torch.cuda.synchronize()
+            best = min(best, g0.elapsed_time(g1))
+        dgemm_tflops = 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
+        del ga, gb
+        torch.cuda.empty_cache()
+    except RuntimeError:
+        pass
 
     # ---- warm-up
     for _ in range(args.warmup):
@@ -358,6 +378,7 @@ def run_ours(args):
         "bound": "tensor", "achieved": gemm_achieved, "peak": peak_tflops, "unit": "TFLOP/s",
         "frac": (gemm_achieved / peak_tflops) if gemm_achieved else None, "traffic": None,
         "kernel": "k_leaf_gemm (FP64 DMMA m8n8k4)",
+        "cublas_dgemm_8192_tflops": dgemm_tflops,
         "peak_source": "measured in this run: spamm_peak_dmma (back-to-back DMMA on all SMs, "
                        f"{peak_ms:.0f} ms); MEASURED_PEAKS.json has no FP64 figure",
         "launches": prof["gemm_count"], "avg_launch_ms": prof["gemm_ms"] / max(prof["gemm_count"], 1),
