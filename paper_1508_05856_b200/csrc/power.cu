@@ -332,30 +332,43 @@ __device__ __forceinline__ void cta_sumsq_part(double x, double *nrm_part)
 }
 
 // w[J*b + c] = (P0 + P1) + (P2 + P3) over J's upper quarters, then + the column
-// parts of the blocks (I, J), I < J, ascending I: colpart rows [rowptr[J], up[J]).
-// Also the CTA's partial of ||w||^2 (fused normalisation, k_norm_apply).
+// parts of the blocks (I, J), I < J: colpart rows [rowptr[J], up[J]), ascending I.
+// One CTA per block row J: SL = 256/b lanes per output element each sum every SL-th
+// column part in order, and the lane partials join in a fixed pairwise tree
+// (deterministic).  Also the CTA's partial of ||w||^2 (fused normalisation, k_norm_apply).
+template <int B>
 __global__ void __launch_bounds__(256) k_spmv_sym_fix(const int32_t *rowptr, const int32_t *up,
-                                                      const double *part, const double *colpart, int nb,
-                                                      int b, double *w, double *nrm_part)
+                                                      const double *part, const double *colpart,
+                                                      double *w, double *nrm_part)
 {
     pdl_wait();
     pdl_trigger();
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    constexpr int SL = 256 / B;
+    __shared__ double sp[SL][B];
+    const int J = blockIdx.x, c = threadIdx.x % B, q = threadIdx.x / B;
+    const int p0 = up[J];
+    double sl = 0.0;
+    for (int p = rowptr[J] + q; p < p0; p += SL) sl += colpart[(int64_t)p * B + c];
+    sp[q][c] = sl;
+    __syncthreads();
     double t = 0.0;
-    if (e < (int64_t)nb * b) {
-        const int J = (int)(e / b), c = (int)(e % b);
-        const int p0 = up[J], len = rowptr[J + 1] - p0;
+    if (q == 0) {
+        const int len = rowptr[J + 1] - p0;
         double P[SPT_Q];
 #pragma unroll
-        for (int q = 0; q < SPT_Q; q++) {
-            const bool any = ((q + 1) * len) / SPT_Q > (q * len) / SPT_Q;
-            P[q] = any ? part[((int64_t)J * SPT_Q + q) * b + c] : 0.0;
+        for (int k = 0; k < SPT_Q; k++) {
+            const bool any = ((k + 1) * len) / SPT_Q > (k * len) / SPT_Q;
+            P[k] = any ? part[((int64_t)J * SPT_Q + k) * B + c] : 0.0;
         }
-        t = (P[0] + P[1]) + (P[2] + P[3]);
-        const double *cp = colpart + c;
-#pragma unroll 4
-        for (int p = rowptr[J]; p < p0; p++) t += cp[(int64_t)p * b];
-        w[e] = t;
+        double u[SL];
+#pragma unroll
+        for (int i = 0; i < SL; i++) u[i] = sp[i][c];
+#pragma unroll
+        for (int h = SL / 2; h > 0; h >>= 1)
+#pragma unroll
+            for (int i = 0; i < h; i++) u[i] += u[i + h];
+        t = ((P[0] + P[1]) + (P[2] + P[3])) + u[0];
+        w[(int64_t)J * B + c] = t;
     }
     cta_sumsq_part(t, nrm_part);
 }
@@ -587,8 +600,8 @@ static spamm_status spmv_sym(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, 
     SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
     CK(launch_pdl(k_spmv_tma<B, true>, ctx->sm_count, 288, smem, ctx->stream, g, y.up, y.mir, y.colpart));
     CKL(ctx);
-    CK(launch_pdl(k_spmv_sym_fix, (int)cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream, rowptr, y.up, part,
-                  (const double *)y.colpart, s->nb, B, w, nrm_part));
+    CK(launch_pdl(k_spmv_sym_fix<B>, s->nb, 256, 0, ctx->stream, rowptr, y.up, (const double *)part,
+                  (const double *)y.colpart, w, nrm_part));
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -654,9 +667,10 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     bool sym = !s->dist && tmam != 0 && (symm == 2 || (symm == 1 && s->b == 64));
     double *part = tma || sym ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * s->b) : nullptr;
     // the TMA kernels' fix-up launch also writes per-CTA partials of ||w||^2 (np of them)
-    const int np = (int)cdiv(n, 256);
+    const int np = (int)cdiv(n, 256);   // partials of the full fix-up (one per 256 outputs)
     const bool fused = (tma || sym) && !s->dist;
-    double *nrm_part = tma || sym ? dalloc<double>(ctx, np) : nullptr;
+    const int np_alloc = np > nb ? np : nb;   // the symmetric fix-up writes one per block row
+    double *nrm_part = tma || sym ? dalloc<double>(ctx, np_alloc) : nullptr;
     if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets || ((tma || sym) && (!part || !nrm_part)))
         return set_err(ctx, SPAMM_ENOMEM, "power");
     CK(cudaMemsetAsync(tickets, 0, sizeof(int32_t) * (K + 1), ctx->stream));
@@ -722,8 +736,9 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     for (int it = 0; it < K; it++) {
         ST(mv(v, w));
         if (fused) {
-            CK(launch_pdl(k_norm_apply, (int)std::min<int64_t>(NRM_CTAS, np), 256, 0, st, (const double *)w, n,
-                          (const double *)nrm_part, np, v));
+            const int npu = sym ? nb : np;
+            CK(launch_pdl(k_norm_apply, (int)std::min<int64_t>(NRM_CTAS, npu), 256, 0, st, (const double *)w, n,
+                          (const double *)nrm_part, npu, v));
         } else if (n >= (1 << 16)) {
             k_sumsq_part<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1);
             k_scale_by_norm<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1, v);
@@ -749,7 +764,7 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     dev_free(ctx, c, sizeof(double) * (1 + NRM_CTAS));
     dev_free(ctx, tickets, sizeof(int32_t) * (K + 1));
     dev_free(ctx, part, sizeof(double) * (int64_t)nb * SPT_Q * s->b);
-    dev_free(ctx, nrm_part, sizeof(double) * np);
+    dev_free(ctx, nrm_part, sizeof(double) * np_alloc);
     dev_free(ctx, up, sizeof(int32_t) * nb);
     dev_free(ctx, mir, sizeof(int32_t) * nblk);
     dev_free(ctx, colpart, sizeof(double) * nblk * s->b);
