@@ -164,7 +164,8 @@ struct SpmvTmaArgs {
     const double *v;
     double *part;       // [nb * SPT_Q * b]
     int32_t *ticket;
-    int nunits;         // nb * SPT_Q
+    int nupper;         // nb * SPT_Q units over the upper parts of the block rows
+    int nunits;         // nupper (SYM) or nupper + nb (the lower parts, one unit per row)
 };
 
 // ------------------------------------------------- TMA-staged SpMV kernel
@@ -176,16 +177,21 @@ struct SpmvTmaArgs {
 // Consumer thread t owns double2 chunk q = t + 256 m of each block (consecutive
 // lanes, consecutive 16 B: conflict-free) and keeps its row accumulators across
 // the unit's blocks; at the unit's last block each block row's LPR lanes reduce with
-// a fixed xor tree into part[unit*b + r], and k_spmv_fix adds the SPT_Q quarters in
-// a fixed order (deterministic).
+// a fixed xor tree into part[unit*b + r], and k_spmv_sym_fix adds the SPT_Q quarters
+// and the column parts in a fixed order (deterministic).  Units: quarters of each
+// row's upper part [up[I], rowptr[I+1]) (the blocks on and above the diagonal), and,
+// without SYM, one unit per row for its lower part, whose blocks yield column parts
+// (below) instead of row sums.
 //
-// SYM (s symmetric, checked bitwise by k_sym_check): units cover only the blocks on
-// and above the diagonal, [up[I], rowptr[I+1]) — half the HBM reads.  An
-// off-diagonal block (I, J) also contributes S_IJ^T v_I to the rows of J: a second
-// pass over the staged tile forms the column sums sum_r S_IJ[r,c] v_I[r] (NSUB row
-// subsets per column, reduced in a fixed order after a consumer-only named barrier)
-// and stores them at colpart[p'*b ..], p' = the CSR position of the mirror (J, I),
-// so k_spmv_sym_fix reads the column parts of row block J contiguously, ascending I.
+// SYM (s symmetric, checked bitwise by k_sym_check): only the upper units run — half
+// the HBM reads.  An off-diagonal block (I, J) also contributes S_IJ^T v_I to the rows
+// of J: a second pass over the staged tile forms the column sums sum_r S_IJ[r,c] v_I[r]
+// (NSUB row subsets per column, reduced in a fixed order after a consumer-only named
+// barrier) and stores them at colpart[p'*b ..], p' = the CSR position of the mirror
+// (J, I), so k_spmv_sym_fix reads the column parts of row block J contiguously,
+// ascending I.  Without SYM the lower block (J, I) itself yields that column part,
+// sum_r S_JI[c, r] v_I[r] in the same order: for a symmetric s the two kernels (and
+// the row-partitioned path, which has only its own rows) give w bit for bit.
 template <int B, bool SYM>
 __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_t *up, const int32_t *mir,
                                                           double *colpart)
@@ -198,8 +204,8 @@ __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_
     extern __shared__ __align__(1024) double sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + STAGES * TILE);
     uint64_t *empty = full + STAGES;
-    int4 *meta = reinterpret_cast<int4 *>(empty + STAGES);   // {unit (-1: end), column block, last, mirror}
-    __shared__ double red[SYM ? 2 : 1][NSUB][B];
+    int4 *meta = reinterpret_cast<int4 *>(empty + STAGES);   // {unit (-1: end), column block, last, colpart pos}
+    __shared__ double red[2][NSUB][B];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         for (int st = 0; st < STAGES; st++) {
@@ -216,16 +222,25 @@ __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_
         for (;;) {
             const int unit = atomicAdd(g.ticket, 1);
             if (unit >= g.nunits) break;
-            const int I = unit / SPT_Q, q = unit % SPT_Q;
-            const int r0 = SYM ? up[I] : g.rowptr[I], len = g.rowptr[I + 1] - r0;
-            const int pb = r0 + (q * len) / SPT_Q, pend = r0 + ((q + 1) * len) / SPT_Q;
+            int pb, pend;
+            if (unit < g.nupper) {   // a quarter of the row's upper part [up[I], rowptr[I+1])
+                const int I = unit / SPT_Q, q = unit % SPT_Q;
+                const int r0 = up[I], len = g.rowptr[I + 1] - r0;
+                pb = r0 + (q * len) / SPT_Q;
+                pend = r0 + ((q + 1) * len) / SPT_Q;
+            } else {                 // (!SYM) the row's lower part [rowptr[I], up[I])
+                const int I = unit - g.nupper;
+                pb = g.rowptr[I];
+                pend = up[I];
+            }
             for (int p0 = pb; p0 < pend; p0 += UCH) {
                 int us[UCH], uc[UCH], um[UCH];
 #pragma unroll
                 for (int i = 0; i < UCH; i++) {
                     us[i] = p0 + i < pend ? __ldg(g.slots + p0 + i) : 0;
                     uc[i] = p0 + i < pend ? __ldg(g.cols + p0 + i) : 0;
-                    um[i] = SYM && p0 + i < pend ? __ldg(mir + p0 + i) : 0;
+                    // column-part position: the mirror (SYM) or the lower block itself (!SYM)
+                    um[i] = p0 + i < pend ? (SYM ? __ldg(mir + p0 + i) : p0 + i) : 0;
                 }
 #pragma unroll 1
                 for (int i = 0; i < UCH && p0 + i < pend; i++) {
@@ -255,7 +270,7 @@ __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_
         lc[m] = ((q % LPR) ^ swz(r)) << 1;   // logical column pair (pool swizzle)
     }
     int vunit = -1, nred = 0;
-    double vi[SYM ? RS : 1];   // v_I at this thread's column-pass rows
+    double vi[RS];   // v at this thread's column-pass rows
     for (int j = 0;; j++) {
         const int st = j % STAGES;
         mbar_wait(&full[st], (j / STAGES) & 1);
@@ -264,17 +279,21 @@ __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_
         const double *tile = sm + st * TILE;
         const double2 *x2 = reinterpret_cast<const double2 *>(tile);
         const double *vv = g.v + (int64_t)mt.y * B;
+        const bool lower = !SYM && mt.x >= g.nupper;   // CTA-uniform
+        const int I = lower ? mt.x - g.nupper : mt.x / SPT_Q;
+        const bool offdiag = SYM && mt.y != I;
+        if (!lower) {
 #pragma unroll
-        for (int m = 0; m < M; m++) {
-            if (tid + 256 * m >= N2) break;      // b = 16: warps 4..7 idle (warp-uniform)
-            const double2 x = x2[tid + 256 * m];
-            const double2 w = *reinterpret_cast<const double2 *>(vv + lc[m]);
-            acc[m] = fma(x.x, w.x, acc[m]);
-            acc[m] = fma(x.y, w.y, acc[m]);
+            for (int m = 0; m < M; m++) {
+                if (tid + 256 * m >= N2) break;      // b = 16: warps 4..7 idle (warp-uniform)
+                const double2 x = x2[tid + 256 * m];
+                const double2 w = *reinterpret_cast<const double2 *>(vv + lc[m]);
+                acc[m] = fma(x.x, w.x, acc[m]);
+                acc[m] = fma(x.y, w.y, acc[m]);
+            }
         }
-        const int I = mt.x / SPT_Q;
-        const bool offdiag = SYM && mt.y != I;   // CTA-uniform
         if (offdiag) {
+            // upper block (I, J): column sums sum_r S_IJ[r, c] v_I[r] for row block J
             if (mt.x != vunit) {
                 vunit = mt.x;
 #pragma unroll
@@ -285,7 +304,18 @@ __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_
             for (int i = 0; i < RS; i++) cs = fma(tile[pool_at(sub * RS + i, cc, B)], vi[i], cs);
             red[nred & 1][sub][cc] = cs;
         }
-        if (mt.z) {
+        if (lower) {
+            // lower block (I, J), J < I: the same sums from the block itself,
+            // sum_r S_IJ[c, r] v_J[r] in the column pass's order, so that for a
+            // symmetric s this equals the SYM kernel's column part bit for bit
+#pragma unroll
+            for (int i = 0; i < RS; i++) vi[i] = vv[sub * RS + i];
+            double cs = 0.0;
+#pragma unroll
+            for (int i = 0; i < RS; i++) cs = fma(tile[pool_at(cc, sub * RS + i, B)], vi[i], cs);
+            red[nred & 1][sub][cc] = cs;
+        }
+        if (mt.z && !lower) {
 #pragma unroll
             for (int m = 0; m < M; m++) {
                 if (tid + 256 * m >= N2) break;
@@ -301,7 +331,7 @@ __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
-        if (offdiag) {
+        if (offdiag || lower) {
             asm volatile("bar.sync 1, 256;\n" ::: "memory");   // consumers only: red[nred & 1] complete
             if (tid < B) {
                 double t = red[nred & 1][0][tid];
@@ -431,30 +461,6 @@ __global__ void __launch_bounds__(256) k_sym_check(const double *pool, const int
     if (__syncthreads_or(!ok) && threadIdx.x == 0) *bad = 1;
 }
 
-// w[I*b + r] = (P0 + P1) + (P2 + P3), P_q = quarter q's partial (0 if the quarter is
-// empty); also the CTA's partial of ||w||^2
-__global__ void __launch_bounds__(256) k_spmv_fix(const int32_t *rowptr, const double *part, int nb, int b,
-                                                  double *w, double *nrm_part)
-{
-    pdl_wait();
-    pdl_trigger();
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    double t = 0.0;
-    if (e < (int64_t)nb * b) {
-        const int I = (int)(e / b), r = (int)(e % b);
-        const int p0 = rowptr[I], len = rowptr[I + 1] - p0;
-        double P[SPT_Q];
-#pragma unroll
-        for (int q = 0; q < SPT_Q; q++) {
-            const bool any = ((q + 1) * len) / SPT_Q > (q * len) / SPT_Q;
-            P[q] = any ? part[((int64_t)I * SPT_Q + q) * b + r] : 0.0;
-        }
-        t = (P[0] + P[1]) + (P[2] + P[3]);
-        w[e] = t;
-    }
-    cta_sumsq_part(t, nrm_part);
-}
-
 // v = w / sqrt(sum of the np partials); every CTA sums the partials in the same fixed
 // order (strided per thread, then a tree), so all agree bitwise on the norm
 __global__ void __launch_bounds__(256) k_norm_apply(const double *w, int64_t n, const double *nrm_part, int np,
@@ -554,40 +560,17 @@ __global__ void k_dot(const double *a, const double *b, int64_t n, double *out)
     if (threadIdx.x == 0) *out = sh[0];
 }
 
-template <int B>
-static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
-                             const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part,
-                             double *nrm_part)
-{
-    constexpr int STAGES = SptCfg<B>::STAGES;
-    const size_t smem = sizeof(double) * STAGES * B * B + STAGES * (2 * sizeof(uint64_t) + sizeof(int4));
-    static std::atomic<uint64_t> configured{0};
-    CK(once_per_device(configured, ctx->device, [&]() {
-        return cudaFuncSetAttribute(k_spmv_tma<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }));
-    SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
-    if (s->dist) {   // the predecessor is a collective: plain launches
-        k_spmv_tma<B, false><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, nullptr, nullptr, nullptr);
-        CKL(ctx);
-        k_spmv_fix<<<cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream>>>(rowptr, part, s->nb, B, w, nrm_part);
-    } else {
-        CK(launch_pdl(k_spmv_tma<B, false>, ctx->sm_count, 288, smem, ctx->stream, g, (const int32_t *)nullptr,
-                      (const int32_t *)nullptr, (double *)nullptr));
-        CKL(ctx);
-        CK(launch_pdl(k_spmv_fix, (int)cdiv((int64_t)s->nb * B, 256), 256, 0, ctx->stream, rowptr, part, s->nb, B, w,
-                      nrm_part));
-    }
-    CKL(ctx);
-    return SPAMM_OK;
-}
-
 struct SymSpmv {
-    const int32_t *up, *mir;
+    const int32_t *up, *mir;   // mir only for SYM
     double *colpart;
 };
 
-template <int B>
-static spamm_status spmv_sym(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
+// w = s v with the TMA kernel.  SYM: the upper block triangle only (s symmetric);
+// otherwise the upper parts plus the lower blocks' column parts, which for a symmetric
+// s are bit for bit the SYM kernel's, so both (and the row-partitioned path) give the
+// same w.  Then the fix-up: w rows and their ||w||^2 partials (one per block row).
+template <int B, bool SYM>
+static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
                              const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part,
                              double *nrm_part, const SymSpmv &y)
 {
@@ -595,15 +578,33 @@ static spamm_status spmv_sym(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, 
     const size_t smem = sizeof(double) * STAGES * B * B + STAGES * (2 * sizeof(uint64_t) + sizeof(int4));
     static std::atomic<uint64_t> configured{0};
     CK(once_per_device(configured, ctx->device, [&]() {
-        return cudaFuncSetAttribute(k_spmv_tma<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return cudaFuncSetAttribute(k_spmv_tma<B, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }));
-    SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, s->nb * SPT_Q};
-    CK(launch_pdl(k_spmv_tma<B, true>, ctx->sm_count, 288, smem, ctx->stream, g, y.up, y.mir, y.colpart));
-    CKL(ctx);
-    CK(launch_pdl(k_spmv_sym_fix<B>, s->nb, 256, 0, ctx->stream, rowptr, y.up, (const double *)part,
-                  (const double *)y.colpart, w, nrm_part));
+    const int nupper = s->nb * SPT_Q;
+    SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, nupper, SYM ? nupper : nupper + s->nb};
+    if (s->dist) {   // the predecessor is a collective: plain launches
+        k_spmv_tma<B, SYM><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, y.up, y.mir, y.colpart);
+        CKL(ctx);
+        k_spmv_sym_fix<B><<<s->nb, 256, 0, ctx->stream>>>(rowptr, y.up, part, y.colpart, w, nrm_part);
+    } else {
+        CK(launch_pdl(k_spmv_tma<B, SYM>, ctx->sm_count, 288, smem, ctx->stream, g, y.up, y.mir, y.colpart));
+        CKL(ctx);
+        CK(launch_pdl(k_spmv_sym_fix<B>, s->nb, 256, 0, ctx->stream, rowptr, y.up, (const double *)part,
+                      (const double *)y.colpart, w, nrm_part));
+    }
     CKL(ctx);
     return SPAMM_OK;
+}
+
+// ||w||^2 partials per block row of the gathered w (row partition), with exactly the
+// reduction of k_spmv_sym_fix (threads 0..b-1 hold the row's entries)
+template <int B>
+__global__ void __launch_bounds__(256) k_row_sumsq(const double *w, double *nrm_part)
+{
+    pdl_wait();
+    pdl_trigger();
+    const double t = threadIdx.x < B ? w[(int64_t)blockIdx.x * B + threadIdx.x] : 0.0;
+    cta_sumsq_part(t, nrm_part);
 }
 
 template <int B>
@@ -662,16 +663,15 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     // ring dominates (C2 setup 4.3 -> 8.4 ms measured), so those keep the register kernel
     const int tmam = spmv_tma_mode();
     const bool tma = tmam == 2 || (tmam == 1 && s->b == 64);
-    // symmetric s (checked below): read only the upper half of the blocks
+    // symmetric s (checked below, single device): read only the upper half of the blocks
     const int symm = spmv_sym_mode();
-    bool sym = !s->dist && tmam != 0 && (symm == 2 || (symm == 1 && s->b == 64));
-    double *part = tma || sym ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * s->b) : nullptr;
-    // the TMA kernels' fix-up launch also writes per-CTA partials of ||w||^2 (np of them)
-    const int np = (int)cdiv(n, 256);   // partials of the full fix-up (one per 256 outputs)
-    const bool fused = (tma || sym) && !s->dist;
-    const int np_alloc = np > nb ? np : nb;   // the symmetric fix-up writes one per block row
-    double *nrm_part = tma || sym ? dalloc<double>(ctx, np_alloc) : nullptr;
-    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets || ((tma || sym) && (!part || !nrm_part)))
+    bool sym = tma && !s->dist && (symm == 2 || (symm == 1 && s->b == 64));
+    double *part = tma ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * s->b) : nullptr;
+    double *nrm_part = tma ? dalloc<double>(ctx, nb) : nullptr;   // ||w||^2 partials, one per block row
+    int32_t *up = tma ? dalloc<int32_t>(ctx, nb) : nullptr, *mir = tma ? dalloc<int32_t>(ctx, nblk) : nullptr;
+    double *colpart = tma ? dalloc<double>(ctx, nblk * s->b) : nullptr;
+    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets ||
+        (tma && (!part || !nrm_part || !up || !mir || !colpart)))
         return set_err(ctx, SPAMM_ENOMEM, "power");
     CK(cudaMemsetAsync(tickets, 0, sizeof(int32_t) * (K + 1), ctx->stream));
     int nmv = 0;
@@ -681,19 +681,16 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     k_row_fill<<<nb, 256, 0, st>>>(s->slot, nb, rowptr, cols, slots);
     k_fill<<<cdiv(n, 256), 256, 0, st>>>(v, n, 1.0 / sqrt((double)n));
     ctx->launches += 4;
-    SymSpmv sy{nullptr, nullptr, nullptr};
-    int32_t *up = nullptr, *mir = nullptr;
-    double *colpart = nullptr;
-    if (sym) {
-        up = dalloc<int32_t>(ctx, nb);
-        mir = dalloc<int32_t>(ctx, nblk);
-        colpart = dalloc<double>(ctx, nblk * s->b);
+    SymSpmv sy{up, mir, colpart};
+    if (tma) {
+        // up[] for every TMA SpMV; the mirror positions and the bitwise symmetry check
+        // only where the symmetric kernel may run (with a row partition some mirrors
+        // live on other ranks)
         int32_t *bad = reinterpret_cast<int32_t *>(c);   // c[0] is written only by the final dot
-        if (!up || !mir || !colpart) return set_err(ctx, SPAMM_ENOMEM, "power");
         CK(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
         k_sym_index<<<nb, 256, 0, st>>>(rowptr, cols, nb, up, mir, bad);
         ctx->launches++;
-        if (s->nblk > 0) {
+        if (sym && s->nblk > 0) {
             switch (s->b) {
             case 16: k_sym_check<16><<<(int)s->nblk, 256, 0, st>>>(s->pool, rowptr, cols, slots, mir, nb, bad); break;
             case 32: k_sym_check<32><<<(int)s->nblk, 256, 0, st>>>(s->pool, rowptr, cols, slots, mir, nb, bad); break;
@@ -702,29 +699,48 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
             ctx->launches++;
         }
         CKL(ctx);
-        int32_t hbad = 1;
-        ST(fetch1(ctx, bad, &hbad, sizeof(int32_t)));
-        sym = hbad == 0;
-        sy = SymSpmv{up, mir, colpart};
+        if (sym) {
+            int32_t hbad = 1;
+            ST(fetch1(ctx, bad, &hbad, sizeof(int32_t)));
+            sym = hbad == 0;
+        }
     }
-    // row partition: local block rows of w = s v, then all ranks gather the full w
-    // (each row is computed by one rank with the single-device kernel: bitwise G-invariant)
+    // row partition: local block rows of w = s v, then all ranks gather the full w and
+    // form the norm partials from it (each row is computed by one rank with the
+    // single-device arithmetic: bitwise G-invariant)
     auto mv = [&](const double *x, double *y) -> spamm_status {
         int32_t *tk = tickets + nmv++;
-        if (sym) {
-            switch (s->b) {
-            case 16: return spmv_sym<16>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
-            case 32: return spmv_sym<32>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
-            default: return spmv_sym<64>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
-            }
-        }
         if (tma) {
             switch (s->b) {
-            case 16: ST(spmv_tma<16>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part)); break;
-            case 32: ST(spmv_tma<32>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part)); break;
-            default: ST(spmv_tma<64>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part)); break;
+            case 16: {
+                spamm_status r = sym ? spmv_tma<16, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy)
+                                     : spmv_tma<16, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+                ST(r);
+                break;
             }
-            return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
+            case 32: {
+                spamm_status r = sym ? spmv_tma<32, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy)
+                                     : spmv_tma<32, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+                ST(r);
+                break;
+            }
+            default: {
+                spamm_status r = sym ? spmv_tma<64, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy)
+                                     : spmv_tma<64, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+                ST(r);
+                break;
+            }
+            }
+            if (s->dist) {
+                ST(gather_rows(ctx, s->parts, y, s->b));
+                switch (s->b) {
+                case 16: k_row_sumsq<16><<<nb, 256, 0, st>>>(y, nrm_part); break;
+                case 32: k_row_sumsq<32><<<nb, 256, 0, st>>>(y, nrm_part); break;
+                default: k_row_sumsq<64><<<nb, 256, 0, st>>>(y, nrm_part); break;
+                }
+                CKL(ctx);
+            }
+            return SPAMM_OK;
         }
         switch (s->b) {
         case 16: ST(spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk)); break;
@@ -735,10 +751,10 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     };
     for (int it = 0; it < K; it++) {
         ST(mv(v, w));
-        if (fused) {
-            const int npu = sym ? nb : np;
-            CK(launch_pdl(k_norm_apply, (int)std::min<int64_t>(NRM_CTAS, npu), 256, 0, st, (const double *)w, n,
-                          (const double *)nrm_part, npu, v));
+        if (tma) {   // the fix-up's (or, row partition, k_row_sumsq's) per-block-row partials
+            const int g = (int)std::min<int64_t>(NRM_CTAS, nb);
+            if (s->dist) k_norm_apply<<<g, 256, 0, st>>>(w, n, nrm_part, nb, v);
+            else CK(launch_pdl(k_norm_apply, g, 256, 0, st, (const double *)w, n, (const double *)nrm_part, nb, v));
         } else if (n >= (1 << 16)) {
             k_sumsq_part<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1);
             k_scale_by_norm<<<NRM_CTAS, 256, 0, st>>>(w, n, c + 1, v);
@@ -764,7 +780,7 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     dev_free(ctx, c, sizeof(double) * (1 + NRM_CTAS));
     dev_free(ctx, tickets, sizeof(int32_t) * (K + 1));
     dev_free(ctx, part, sizeof(double) * (int64_t)nb * SPT_Q * s->b);
-    dev_free(ctx, nrm_part, sizeof(double) * np_alloc);
+    dev_free(ctx, nrm_part, sizeof(double) * nb);
     dev_free(ctx, up, sizeof(int32_t) * nb);
     dev_free(ctx, mir, sizeof(int32_t) * nblk);
     dev_free(ctx, colpart, sizeof(double) * nblk * s->b);
