@@ -209,13 +209,21 @@ static void selfcheck_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, co
 // segments on the context stream || halo exchange on the communication stream,
 // then the GEMM over the segments that use remote tiles.  Each segment is owned
 // by one CTA and accumulated in ascending k, so the split changes no result.
-static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_mat m, int epi,
-                                    double *trace_part)
+// the context's second stream (+ events): the halo exchange (row partition) or the
+// second of two concurrent culls (single device)
+static spamm_status ensure_side_stream(spamm_ctx ctx)
 {
     if (!ctx->comm_stream) {
         CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
         for (auto &e : ctx->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+    return SPAMM_OK;
+}
+
+static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, spamm_mat m, int epi,
+                                    double *trace_part)
+{
+    ST(ensure_side_stream(ctx));
     const cudaStream_t main_s = ctx->stream, comm_s = ctx->comm_stream;
     int32_t *order = nullptr;
     int64_t nloc = 0;
@@ -409,8 +417,23 @@ static spamm_status ns_step_batched(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, dou
     if (!st && stats) stats[0] = ctx->cw[0]->stats;
     Cull *c1 = ctx->cw[1], *c2 = ctx->cw[2];
     int pc = prof_begin(ctx, SPAMM_PH_CULL);
+    // the Y' and Z' culls are independent, latency-bound chains of small kernels: the
+    // Z' cull runs on the side stream, concurrently with the Y' cull
+    const cudaStream_t main_s = ctx->stream;
+    if (!st) st = ensure_side_stream(ctx);
+    if (!st && cudaEventRecord(ctx->ev[0], main_s) == cudaSuccess &&
+        cudaStreamWaitEvent(ctx->comm_stream, ctx->ev[0], 0) == cudaSuccess) {
+        ctx->stream = ctx->comm_stream;
+        st = cull_start(ctx, c2, H, Z, tau, H->r0, H->r1);
+        ctx->stream = main_s;
+        if (!st && (cudaEventRecord(ctx->ev[1], ctx->comm_stream) != cudaSuccess))
+            st = set_err(ctx, SPAMM_ECUDA, "event record");
+    } else if (!st) {
+        st = set_err(ctx, SPAMM_ECUDA, "side stream join");
+    }
     if (!st) st = cull_start(ctx, c1, Y, H, tau_s, Y->r0, Y->r1);
-    if (!st) st = cull_start(ctx, c2, H, Z, tau, H->r0, H->r1);
+    if (!st && cudaStreamWaitEvent(main_s, ctx->ev[1], 0) != cudaSuccess)
+        st = set_err(ctx, SPAMM_ECUDA, "side stream join");
     int64_t added = 0;
     double tt = 0.0;
     if (!st) {
