@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <atomic>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -53,6 +54,7 @@ struct spamm_ctx_s {
     bool own_stream = false;
     spamm_allocator alloc{};
     bool has_alloc = false;
+    cudaMemPool_t pool = nullptr;   // the context's stream-ordered pool (no allocator given)
     std::string err;
     int64_t launches = 0;
     int sm_count = 148;
@@ -165,6 +167,16 @@ __host__ __device__ static inline int pool_col(int e, int b)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// SPAMM_PDL=0 turns the attribute off (plain stream-ordered launches)
+static inline bool pdl_enabled()
+{
+    static const bool on = [] {
+        const char *e = getenv("SPAMM_PDL");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args)
 {
@@ -177,7 +189,7 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, size_t s
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 

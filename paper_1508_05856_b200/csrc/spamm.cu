@@ -49,10 +49,17 @@ extern "C" spamm_status spamm_ctx_create(int device, void *cuda_stream, const sp
         // stream-ordered allocator: keep freed memory in the pool across synchronisations
         // (the default release threshold of 0 returns it to the driver at every sync, and
         // the next cudaMallocAsync pays for a fresh mapping: C3 ran 8x slower that way)
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        // A pool of the context's own (not the device's default pool, which other users
+        // of the process may trim or share).
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        if (cudaMemPoolCreate(&ctx->pool, &props) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        } else {
+            ctx->pool = nullptr;
         }
         cudaGetLastError();
     }
@@ -84,6 +91,7 @@ extern "C" void spamm_ctx_destroy(spamm_ctx ctx)
     dev_free(ctx, ctx->iscratch, sizeof(int64_t) * 64);
     cudaStreamSynchronize(ctx->stream);
     prof_destroy(ctx);
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -420,8 +428,15 @@ static spamm_status ns_step_batched(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, dou
     // the Y' and Z' culls are independent, latency-bound chains of small kernels: the
     // Z' cull runs on the side stream, concurrently with the Y' cull
     const cudaStream_t main_s = ctx->stream;
+    static const bool conc = [] {
+        const char *e = getenv("SPAMM_CONCURRENT_CULL");
+        return !(e && *e == '0');
+    }();
     if (!st) st = ensure_side_stream(ctx);
-    if (!st && cudaEventRecord(ctx->ev[0], main_s) == cudaSuccess &&
+    if (!st && !conc) {
+        st = cull_start(ctx, c2, H, Z, tau, H->r0, H->r1);
+        if (!st && cudaEventRecord(ctx->ev[1], main_s) != cudaSuccess) st = set_err(ctx, SPAMM_ECUDA, "event");
+    } else if (!st && cudaEventRecord(ctx->ev[0], main_s) == cudaSuccess &&
         cudaStreamWaitEvent(ctx->comm_stream, ctx->ev[0], 0) == cudaSuccess) {
         ctx->stream = ctx->comm_stream;
         st = cull_start(ctx, c2, H, Z, tau, H->r0, H->r1);

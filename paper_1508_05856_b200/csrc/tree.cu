@@ -55,7 +55,8 @@ void *dev_alloc(spamm_ctx ctx, size_t bytes)
     void *p = nullptr;
     if (ctx->has_alloc) {
         p = ctx->alloc.alloc(bytes, (void *)ctx->stream, ctx->alloc.user);
-    } else if (cudaMallocAsync(&p, bytes, ctx->stream) != cudaSuccess) {
+    } else if ((ctx->pool ? cudaMallocFromPoolAsync(&p, bytes, ctx->pool, ctx->stream)
+                          : cudaMallocAsync(&p, bytes, ctx->stream)) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
