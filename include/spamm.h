@@ -26,7 +26,10 @@
  *     "present" iff its fp64 sum of squares is > 0 (reading L6);
  *     absent blocks are exact zeros and never form leaf tasks.
  *   - spamm_mat handles returned through out-parameters are owned by the
- *     caller and released with spamm_mat_free (before spamm_ctx_destroy).
+ *     caller and released with spamm_mat_free.  Each matrix holds its context:
+ *     spamm_ctx_destroy while matrices are alive only marks the context, and
+ *     the teardown happens at the last spamm_mat_free (no other call may use a
+ *     destroyed context; freeing its remaining matrices is the one exception).
  *   - All device memory comes from the context allocator (the Python layer
  *     passes PyTorch's caching allocator), else cudaMallocAsync on the stream.
  */
@@ -203,6 +206,37 @@ spamm_status spamm_export_tasks(spamm_ctx ctx, int32_t *ikj, int64_t cap, int64_
  * triples (i,k,j); hist: HOST [nbins] int64, d >= nbins-1 counted in the last bin.
  * Exact integer counts.  Synchronises. */
 spamm_status spamm_task_distance_hist(spamm_ctx ctx, int64_t *hist, int32_t nbins);
+
+/* Per-product volume recorder: the paper's lensing evidence is
+ * per iteration and per product (the y_k and x_k volumes of P:740-745, "Locality"
+ * P:804-813; "sparse VTK output for visualization of the ijk product volumes",
+ * P:418-419).  While a sink is attached (spamm_ctx_set_volume_sink), EVERY SpAMM
+ * product the context runs (spamm_multiply[_t], the three products of each
+ * spamm_ns_step / spamm_ns_sqrt iteration in the order X, Y', Z', the single-channel
+ * and regularised paths) appends one record, after its cull and before its GEMM:
+ *   ntasks[p]            surviving leaf triples of product p;
+ *   hist[p*nbins + d]    triples with max(|i-j|, |i-k|, |j-k|) = d (last bin: >= nbins-1),
+ *                        when nbins > 0 and hist != NULL;
+ *   ikj                  the triples themselves (i,k,j), product after product, in the
+ *                        GEMM's order (output block Morton order, k ascending), while
+ *                        ikj_count < ikj_cap; ikj_needed counts all of them.
+ * Records beyond nprod_cap only advance nprod.  All arrays are HOST memory owned by
+ * the caller and must outlive the attachment.  Row partition: each rank records
+ * its own rows' triples.  Recording synchronises the stream once per product
+ * (instrumentation, not for timed runs).  Errors: EINVAL (nprod_cap < 0). */
+typedef struct {
+    int32_t nbins;          /* > 0: record the histogram */
+    int64_t *hist;          /* [nprod_cap * nbins], nullable */
+    int64_t *ntasks;        /* [nprod_cap], nullable */
+    int32_t *ikj;           /* [3 * ikj_cap], nullable */
+    int64_t ikj_cap;
+    int64_t nprod_cap;
+    int64_t nprod;          /* out (zero it before attaching) */
+    int64_t ikj_count;      /* out */
+    int64_t ikj_needed;     /* out */
+} spamm_volume_sink;
+/* sink == NULL detaches. */
+spamm_status spamm_ctx_set_volume_sink(spamm_ctx ctx, spamm_volume_sink *sink);
 
 /* -------------------------------------------------------- Newton-Schulz */
 /* One dual step (north_star form): X = Z (x)_tau Y; t = (n - tr X)/n;

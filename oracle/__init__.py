@@ -76,6 +76,7 @@ def lib():
             "or_ns_sqrt": (i32, [vp, dbl, dbl, i32, dbl, i32, dbl, dbl, i32, P(vp), P(vp), vp, vp,
                                  P(dbl), P(C.c_int)]),
             "or_ns_step_map": (i32, [vp, vp, dbl, dbl, i32, P(vp), P(vp), P(vp), P(dbl), vp]),
+            "or_ns_step_tasks": (i32, [vp, vp, dbl, dbl, i32, P(vp), P(vp), P(vp), P(dbl), vp, vp, vp, vp, i64]),
             "or_alpha": (dbl, [dbl]),
             "or_eps": (dbl, [dbl]),
             "or_num_threads": (i32, []),
@@ -204,17 +205,33 @@ def ns_y0(s: OMat, c: float, mu: float = 0.0) -> OMat:
     return OMat(lib().or_ns_y0(s.h, c, mu))
 
 
-def ns_step(Y: OMat, Z: OMat, tau: float, tau_s: float | None = None, scaled: bool = False):
-    """One dual NS step (north_star form). Returns (Y', Z', H, t, counts[3])."""
+def _sort_tasks(t):
+    return t[np.lexsort((t[:, 1], t[:, 2], t[:, 0]))]   # by (i, j, k)
+
+
+def ns_step(Y: OMat, Z: OMat, tau: float, tau_s: float | None = None, scaled: bool = False,
+            want_tasks: bool = False, task_cap: int = 1 << 16, allow_nonfinite: bool = False):
+    """One dual NS step (north_star form). Returns (Y', Z', H, t, counts[3]), plus the
+    three products' leaf triples [X, Y', Z'] (each [ntasks, 3] sorted by (i, j, k)) with
+    want_tasks.  allow_nonfinite: return the non-finite iterates instead of raising."""
     tau_s = tau if tau_s is None else tau_s
-    yn, zn, hn = C.c_void_p(), C.c_void_p(), C.c_void_p()
-    t = C.c_double(0)
-    counts = np.zeros(3, dtype=np.int64)
-    rc = lib().or_ns_step_map(Y.h, Z.h, tau, tau_s, int(scaled), C.byref(yn), C.byref(zn), C.byref(hn),
-                          C.byref(t), _ptr(counts))
-    out = (OMat(yn.value), OMat(zn.value), OMat(hn.value), t.value, counts)
-    if rc:
+    while True:
+        yn, zn, hn = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        t = C.c_double(0)
+        counts = np.zeros(3, dtype=np.int64)
+        bufs = [np.empty(3 * task_cap, dtype=np.int32) for _ in range(3)] if want_tasks else None
+        tp = [_ptr(x) for x in bufs] if want_tasks else [None, None, None]
+        rc = lib().or_ns_step_tasks(Y.h, Z.h, tau, tau_s, int(scaled), C.byref(yn), C.byref(zn), C.byref(hn),
+                                    C.byref(t), _ptr(counts), *tp, task_cap if want_tasks else 0)
+        out = (OMat(yn.value), OMat(zn.value), OMat(hn.value), t.value, counts)
+        if want_tasks and counts.max() > task_cap:
+            task_cap = int(counts.max())
+            continue
+        break
+    if rc and not allow_nonfinite:
         raise FloatingPointError("oracle NS step: non-finite iterate")
+    if want_tasks:
+        out = out + ([_sort_tasks(b[: 3 * c].reshape(-1, 3)) for b, c in zip(bufs, counts)],)
     return out
 
 

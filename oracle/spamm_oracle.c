@@ -591,21 +591,30 @@ double or_eps(double t) { return 0.1 * (1.0 / (1.0 + exp(-75.0 * (t - 0.30)))); 
 
 /* map 0: H = 1/2 (3I - X) (alpha = 1, eps = 0: the north_star form);
  * map 1: H = h_alpha[(1 - 2 eps) X + eps I] with alpha(t_k), eps(t_k). */
-int or_ns_step_map(const omat *Y, const omat *Z, double tau, double tau_s, int map,
-                   omat **Yn, omat **Zn, omat **Hout, double *t, int64_t counts[3])
+/* tasks (nullable): the leaf triples (i,k,j) of the three products [X, Y', Z'],
+ * tasks[p] holding up to cap triples (counts[] always receives the full counts) */
+int or_ns_step_tasks(const omat *Y, const omat *Z, double tau, double tau_s, int map,
+                     omat **Yn, omat **Zn, omat **Hout, double *t, int64_t counts[3],
+                     int32_t *tX, int32_t *tY, int32_t *tZ, int64_t cap)
 {
     int64_t c0 = 0, c1 = 0, c2 = 0;
-    omat *X = or_multiply(Z, Y, tau, NULL, 0, &c0);
+    omat *X = or_multiply(Z, Y, tau, tX, tX ? cap : 0, &c0);
     double tr = or_trace(X);
     *t = ((double)X->n - tr) / (double)X->n;
     omat *H = map ? map_mat(X, 6, or_alpha(*t), or_eps(*t)) : map_mat(X, 4, 0.0, 0.0);
     or_free(X);
-    *Yn = or_multiply(Y, H, tau_s, NULL, 0, &c1);
-    *Zn = or_multiply(H, Z, tau, NULL, 0, &c2);
+    *Yn = or_multiply(Y, H, tau_s, tY, tY ? cap : 0, &c1);
+    *Zn = or_multiply(H, Z, tau, tZ, tZ ? cap : 0, &c2);
     if (counts) { counts[0] = c0; counts[1] = c1; counts[2] = c2; }
     if (Hout) *Hout = H; else or_free(H);
     if (!isfinite(*t) || !isfinite(or_norm(*Yn)) || !isfinite(or_norm(*Zn))) return -1;
     return 0;
+}
+
+int or_ns_step_map(const omat *Y, const omat *Z, double tau, double tau_s, int map,
+                   omat **Yn, omat **Zn, omat **Hout, double *t, int64_t counts[3])
+{
+    return or_ns_step_tasks(Y, Z, tau, tau_s, map, Yn, Zn, Hout, t, counts, NULL, NULL, NULL, 0);
 }
 
 int or_ns_step(const omat *Y, const omat *Z, double tau, double tau_s,

@@ -31,6 +31,7 @@ __all__ = [
     "spamm_export_blocks", "spamm_profile_enable", "spamm_profile_read", "spamm_peak_dmma",
     "Comm", "spamm_comm_nccl_unique_id", "spamm_comm_nccl_create", "spamm_comm_local_group",
     "spamm_comm_destroy", "spamm_ctx_set_comm", "spamm_mat_rows", "spamm_row_task_counts",
+    "VolumeSink", "spamm_ctx_set_volume_sink",
 ]
 
 STATUS = {0: "SPAMM_OK", 1: "SPAMM_EINVAL", 2: "SPAMM_ESHAPE", 3: "SPAMM_ENOMEM",
@@ -69,6 +70,12 @@ class spamm_profile_t(C.Structure):
     _fields_ = [("ms", C.c_double * NPHASE), ("count", C.c_int64 * NPHASE),
                 ("gemm_flops", C.c_double), ("gemm_tasks", C.c_int64),
                 ("gemm_operand_bytes", C.c_double)]
+
+
+class spamm_volume_sink(C.Structure):
+    _fields_ = [("nbins", C.c_int32), ("hist", C.c_void_p), ("ntasks", C.c_void_p), ("ikj", C.c_void_p),
+                ("ikj_cap", C.c_int64), ("nprod_cap", C.c_int64), ("nprod", C.c_int64),
+                ("ikj_count", C.c_int64), ("ikj_needed", C.c_int64)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -131,6 +138,7 @@ def load():
         "spamm_ctx_set_comm": (i32, [vp, vp, vp]),
         "spamm_mat_rows": (i32, [vp, P(i32), P(i32)]),
         "spamm_row_task_counts": (i32, [vp, vp, vp, dbl, vp]),
+        "spamm_ctx_set_volume_sink": (i32, [vp, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -243,7 +251,10 @@ class Mat:
         self.h = h
 
     def free(self):
-        if getattr(self, "h", None) and getattr(self.ctx, "h", None):
+        # valid after ctx.close() too: the library defers a context's teardown to the
+        # last spamm_mat_free of its matrices (the allocator callbacks stay alive with
+        # self.ctx)
+        if getattr(self, "h", None):
             load().spamm_mat_free(self.h)
         self.h = None
 
@@ -608,3 +619,46 @@ def spamm_peak_dmma(ctx: Ctx, iters: int = 200000):
     t, ms = C.c_double(), C.c_double()
     ctx.check(load().spamm_peak_dmma(ctx.h, int(iters), C.byref(t), C.byref(ms)))
     return t.value, ms.value
+
+
+class VolumeSink:
+    """Host buffers of the per-product volume recorder (spamm_volume_sink, §8(f) f4).
+
+    After the recorded calls: ``ntasks[p]``, ``hist[p]`` (distance histogram) and
+    ``tasks(p)`` (the (i,k,j) triples of product p, if ikj_cap covered them)."""
+
+    def __init__(self, nprod_cap: int, nbins: int = 0, ikj_cap: int = 0):
+        self.hist_buf = np.zeros((nprod_cap, max(nbins, 1)), dtype=np.int64)
+        self.ntasks_buf = np.zeros(nprod_cap, dtype=np.int64)
+        self.ikj_buf = np.zeros((max(ikj_cap, 1), 3), dtype=np.int32)
+        self.s = spamm_volume_sink(int(nbins), self.hist_buf.ctypes.data if nbins > 0 else None,
+                                   self.ntasks_buf.ctypes.data, self.ikj_buf.ctypes.data if ikj_cap > 0 else None,
+                                   int(ikj_cap), int(nprod_cap), 0, 0, 0)
+
+    @property
+    def nprod(self) -> int:
+        return self.s.nprod
+
+    @property
+    def ntasks(self) -> np.ndarray:
+        return self.ntasks_buf[: min(self.s.nprod, len(self.ntasks_buf))]
+
+    @property
+    def hist(self) -> np.ndarray:
+        return self.hist_buf[: min(self.s.nprod, len(self.hist_buf))]
+
+    def complete(self) -> bool:
+        """True if every recorded triple fit in ikj_cap."""
+        return self.s.ikj_count == self.s.ikj_needed
+
+    def tasks(self, p: int) -> np.ndarray:
+        off = int(self.ntasks_buf[:p].sum())
+        n = int(self.ntasks_buf[p])
+        assert off + n <= self.s.ikj_count, "ikj_cap too small for product %d" % p
+        return self.ikj_buf[off: off + n]
+
+
+def spamm_ctx_set_volume_sink(ctx: Ctx, sink: VolumeSink | None):
+    """Attach (or detach with None) a per-product volume recorder to ctx."""
+    ctx.check(load().spamm_ctx_set_volume_sink(ctx.h, C.byref(sink.s) if sink is not None else None))
+    ctx._vsink = sink   # the library holds raw pointers into it

@@ -3,6 +3,7 @@ from __future__ import annotations
 
 import glob
 import os
+import shutil
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -13,10 +14,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "--cudart", "static",
     "-Xcompiler", "-fPIC,-O3",
-    "-shared",
 ]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "--cudart", "static", "-shared"]
 
 
 def sources():
@@ -38,12 +38,23 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
+    # one nvcc per translation unit, in parallel, then one link
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, *sources()]
+    objdir = os.path.join(HERE, "build", f"obj{os.getpid()}")
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in sources()]
+    cmds = [[NVCC, *NVCC_FLAGS, "-c", "-o", o, s] for s, o in zip(sources(), objs)]
     if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        for c in cmds:
+            print(" ".join(c))
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        rcs = list(ex.map(lambda c: subprocess.call(c), cmds))
+    if any(rcs):
+        raise subprocess.CalledProcessError(max(rcs), "nvcc (see the errors above)")
+    subprocess.check_call([NVCC, *LINK_FLAGS, "-o", tmp, *objs])
     os.replace(tmp, LIB)
+    shutil.rmtree(objdir, ignore_errors=True)
     return LIB
 
 

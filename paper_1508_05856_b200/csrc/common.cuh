@@ -74,7 +74,15 @@ struct spamm_ctx_s {
     void *zc = nullptr;            // mapped pinned host buffer for small device->host reads
     void *zc_dev = nullptr;        // its device alias
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    // matrices allocated from this context and not yet freed; spamm_ctx_destroy with
+    // live matrices defers the teardown to the last spamm_mat_free (their memory
+    // comes from the context's pool / allocator)
+    spamm_volume_sink *vsink = nullptr;   // per-product recorder (f4), nullable
+    std::atomic<int64_t> live_mats{0};
+    std::atomic<bool> destroy_pending{false};
 };
+// tear down a context whose matrices are all freed (spamm.cu)
+void ctx_teardown(spamm_ctx ctx);
 
 struct spamm_mat_s {
     spamm_ctx ctx = nullptr;
@@ -323,6 +331,8 @@ spamm_status cull_complete(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, do
                            int transA = 0);
 void cull_free(spamm_ctx ctx, Cull *cw);
 spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj_host, int64_t cap, int64_t *n);
+// append this product's record to ctx->vsink (no-op without a sink)
+spamm_status volume_record(spamm_ctx ctx, Cull *cw);
 
 // gemm.cu — FP64 DMMA leaf GEMM with fused epilogues
 enum { EPI_STORE = 0, EPI_NS_H = 1, EPI_NS_X = 2 };

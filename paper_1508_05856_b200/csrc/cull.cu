@@ -560,8 +560,12 @@ spamm_status cull_export(spamm_ctx ctx, Cull *cw, int32_t *ikj, int64_t cap, int
     if (m <= 0) return SPAMM_OK;
     int4 *h = nullptr;
     CK(cudaMallocHost(&h, sizeof(int4) * m));
-    CK(cudaMemcpyAsync(h, cw->rec[cw->final_buf], sizeof(int4) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    cudaError_t e = cudaMemcpyAsync(h, cw->rec[cw->final_buf], sizeof(int4) * m, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        cudaFreeHost(h);
+        return check_cuda(ctx, e, "task export");
+    }
     for (int64_t t = 0; t < m; t++) {
         uint32_t code = h[t].x;
         ikj[3 * t + 0] = (int32_t)morton_i(code);
@@ -617,11 +621,9 @@ __global__ void k_task_dist_hist(const int4 *rec, int64_t n, int nbins, unsigned
     }
 }
 
-extern "C" spamm_status spamm_task_distance_hist(spamm_ctx ctx, int64_t *hist, int32_t nbins)
+static spamm_status task_hist(spamm_ctx ctx, Cull *cw, int64_t *hist, int32_t nbins)
 {
-    if (!ctx || !hist || nbins < 1) return set_err(ctx, SPAMM_EINVAL, "bad argument");
     for (int b = 0; b < nbins; b++) hist[b] = 0;
-    Cull *cw = ctx->last;
     if (!cw || cw->ntasks == 0) return SPAMM_OK;
     unsigned long long *d = dalloc<unsigned long long>(ctx, nbins);
     if (!d) return set_err(ctx, SPAMM_ENOMEM, "histogram");
@@ -632,5 +634,36 @@ extern "C" spamm_status spamm_task_distance_hist(spamm_ctx ctx, int64_t *hist, i
     CK(cudaMemcpyAsync(hist, d, sizeof(int64_t) * nbins, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     dev_free(ctx, d, sizeof(unsigned long long) * nbins);
+    return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_task_distance_hist(spamm_ctx ctx, int64_t *hist, int32_t nbins)
+{
+    if (!ctx || !hist || nbins < 1) return set_err(ctx, SPAMM_EINVAL, "bad argument");
+    return task_hist(ctx, ctx->last, hist, nbins);
+}
+
+extern "C" spamm_status spamm_ctx_set_volume_sink(spamm_ctx ctx, spamm_volume_sink *sink)
+{
+    if (!ctx) return SPAMM_EINVAL;
+    if (sink && sink->nprod_cap < 0) return set_err(ctx, SPAMM_EINVAL, "nprod_cap < 0");
+    ctx->vsink = sink;
+    return SPAMM_OK;
+}
+
+spamm_status volume_record(spamm_ctx ctx, Cull *cw)
+{
+    spamm_volume_sink *v = ctx->vsink;
+    if (!v) return SPAMM_OK;
+    const int64_t p = v->nprod++;
+    v->ikj_needed += cw->ntasks;
+    if (p >= v->nprod_cap) return SPAMM_OK;
+    if (v->ntasks) v->ntasks[p] = cw->ntasks;
+    if (v->nbins > 0 && v->hist) ST(task_hist(ctx, cw, v->hist + p * v->nbins, v->nbins));
+    if (v->ikj && v->ikj_count < v->ikj_cap) {
+        int64_t n = 0;
+        ST(cull_export(ctx, cw, v->ikj + 3 * v->ikj_count, v->ikj_cap - v->ikj_count, &n));
+        v->ikj_count += std::min(n, v->ikj_cap - v->ikj_count);
+    }
     return SPAMM_OK;
 }

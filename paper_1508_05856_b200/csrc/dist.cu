@@ -213,8 +213,7 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
     int32_t *flags = dalloc<int32_t>(ctx, ntiles + 1);
     V1 *agg = dalloc<V1>(ctx, ntiles), *pre = dalloc<V1>(ctx, ntiles);
     int64_t *dbounds = dalloc<int64_t>(ctx, W + 1 + W + W * W);
-    if (!need || !excl || !flags || !agg || !pre || !dbounds) return set_err(ctx, SPAMM_ENOMEM, "halo workspace");
-    int64_t *dmine = dbounds + W + 1, *dall = dmine + W;
+    int64_t *dmine = dbounds ? dbounds + W + 1 : nullptr, *dall = dmine ? dmine + W : nullptr;
     std::vector<int64_t> hb(W + 1), M((size_t)W * W);
     std::vector<size_t> soff(W), scnt(W), roff(W), rcnt(W);
     int32_t *codes = nullptr, *rcodes = nullptr;
@@ -232,7 +231,9 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
         dev_free(ctx, rcodes, sizeof(int32_t) * serve);
         dev_free(ctx, sendblk, sizeof(double) * serve * b2);
     };
-    do {
+    // every exit (errors included) reaches cleanup()
+    st = [&]() -> spamm_status {
+        if (!need || !excl || !flags || !agg || !pre || !dbounds) return set_err(ctx, SPAMM_ENOMEM, "halo workspace");
         // 1. requests: mark, scan, per-owner bounds
         CK(cudaMemsetAsync(need, 0, sizeof(int32_t) * N, s));
         CK(cudaMemsetAsync(flags, 0, sizeof(int32_t) * (ntiles + 1), s));
@@ -250,7 +251,7 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
         std::vector<int64_t> mine(W);
         for (int p = 0; p < W; p++) mine[p] = hb[p + 1] - hb[p];
         CK(cudaMemcpyAsync(dmine, mine.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice, s));
-        if ((st = comm->allgather(ctx, dmine, dall, sizeof(int64_t) * W))) break;
+        if ((st = comm->allgather(ctx, dmine, dall, sizeof(int64_t) * W))) return st;
         ST(fetch1(ctx, dall, M.data(), sizeof(int64_t) * W * W));
         for (int q = 0; q < W; q++) serve += M[(size_t)q * W + me];
         // 3. request lists to the owners
@@ -258,7 +259,7 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
         rcodes = dalloc<int32_t>(ctx, serve);
         if (!codes || !rcodes) {
             st = set_err(ctx, SPAMM_ENOMEM, "halo request lists");
-            break;
+            return st;
         }
         k_req_list<<<cdiv(N, 256), 256, 0, s>>>(need, excl, N, codes);
         CKL(ctx);
@@ -270,13 +271,13 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
             roff[p] = sizeof(int32_t) * acc;
             acc += M[(size_t)p * W + me];
         }
-        if ((st = comm->alltoallv(ctx, codes, soff.data(), scnt.data(), rcodes, roff.data(), rcnt.data()))) break;
+        if ((st = comm->alltoallv(ctx, codes, soff.data(), scnt.data(), rcodes, roff.data(), rcnt.data()))) return st;
         // 4. owners pack, blocks come back into the halo in request order
         sendblk = dalloc<double>(ctx, serve * b2);
         hp = dalloc<double>(ctx, total * b2);
         if (!sendblk || !hp) {
             st = set_err(ctx, SPAMM_ENOMEM, "halo pool (%lld blocks)", (long long)total);
-            break;
+            return st;
         }
         if (serve) {
             k_pack_blocks<<<(int)serve, 256, 0, s>>>(rcodes, nb, B->slot, B->pool, b, sendblk);
@@ -291,13 +292,14 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
             roff[p] = sizeof(double) * b2 * hb[p];
             rcnt[p] = sizeof(double) * b2 * mine[p];
         }
-        if ((st = comm->alltoallv(ctx, sendblk, soff.data(), scnt.data(), hp, roff.data(), rcnt.data()))) break;
+        if ((st = comm->alltoallv(ctx, sendblk, soff.data(), scnt.data(), hp, roff.data(), rcnt.data()))) return st;
         // 5. tasks read remote tiles from the halo
         if (ntasks) {
             k_patch_tb<<<grid, 256, 0, s>>>(rec, ntasks, excl, nb, cw->tB);
             CKL(ctx);
         }
-    } while (0);
+        return SPAMM_OK;
+    }();
     cleanup();
     if (st) {
         dev_free(ctx, hp, sizeof(double) * total * b2);
@@ -346,10 +348,10 @@ spamm_status seg_split(spamm_ctx ctx, Cull *cw, int32_t **order, int64_t *nlocal
     const int ntiles = cdiv(std::max<int64_t>(ns, 1), 512);
     int32_t *flags = dalloc<int32_t>(ctx, ntiles + 1);
     V1 *agg = dalloc<V1>(ctx, ntiles), *pre = dalloc<V1>(ctx, ntiles);
-    if (!flag || !excl || !ord || !flags || !agg || !pre) return set_err(ctx, SPAMM_ENOMEM, "segment split");
     spamm_status st = SPAMM_OK;
     int32_t h = 0;
-    if (ns > 0) {
+    if (!flag || !excl || !ord || !flags || !agg || !pre) st = set_err(ctx, SPAMM_ENOMEM, "segment split");
+    else if (ns > 0) {
         k_seg_local<<<cdiv(ns, 8), 256, 0, s>>>(cw->seg_start, cw->seg_len, cw->tB, ns, flag);
         ctx->launches++;
         cudaMemsetAsync(flags, 0, sizeof(int32_t) * (ntiles + 1), s);

@@ -670,6 +670,8 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     double *nrm_part = tma ? dalloc<double>(ctx, nb) : nullptr;   // ||w||^2 partials, one per block row
     int32_t *up = tma ? dalloc<int32_t>(ctx, nb) : nullptr, *mir = tma ? dalloc<int32_t>(ctx, nblk) : nullptr;
     double *colpart = tma ? dalloc<double>(ctx, nblk * s->b) : nullptr;
+    // every exit (errors included) goes through the one cleanup below
+    auto body = [&]() -> spamm_status {
     if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets ||
         (tma && (!part || !nrm_part || !up || !mir || !colpart)))
         return set_err(ctx, SPAMM_ENOMEM, "power");
@@ -771,6 +773,9 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     double h = 0;
     ST(fetch1(ctx, c, &h, sizeof(double)));
     *c_host = h;
+    return SPAMM_OK;
+    };
+    const spamm_status result = body();
     dev_free(ctx, cnt, sizeof(int32_t) * nb);
     dev_free(ctx, rowptr, sizeof(int32_t) * (nb + 1));
     dev_free(ctx, cols, sizeof(int32_t) * nblk);
@@ -784,5 +789,5 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     dev_free(ctx, up, sizeof(int32_t) * nb);
     dev_free(ctx, mir, sizeof(int32_t) * nblk);
     dev_free(ctx, colpart, sizeof(double) * nblk * s->b);
-    return SPAMM_OK;
+    return result;
 }

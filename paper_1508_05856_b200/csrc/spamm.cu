@@ -77,6 +77,15 @@ extern "C" spamm_status spamm_ctx_create(int device, void *cuda_stream, const sp
 extern "C" void spamm_ctx_destroy(spamm_ctx ctx)
 {
     if (!ctx) return;
+    // matrices still alive: they own memory of this context (its pool / allocator) and
+    // point back at it, so the teardown waits for the last spamm_mat_free
+    ctx->destroy_pending.store(true);
+    if (ctx->live_mats.load() > 0) return;
+    ctx_teardown(ctx);
+}
+
+void ctx_teardown(spamm_ctx ctx)
+{
     cudaStreamSynchronize(ctx->stream);
     dist_free(ctx);
     for (int i = 0; i < 3; i++) {
@@ -271,6 +280,8 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
         prof_end(ctx, pg2);
         prof_gemm_work(ctx, cw->ntasks, cw->nsegs, A->b);
     }
+    // self-check re-runs the GEMM while the halo (remote tiles, patched tB) still exists
+    if (!st && selfcheck_mode()) selfcheck_gemm(ctx, cw, A, B, halo, m, epi);
     // the halo was allocated on the comm stream: free it there, after the GEMM read it
     CK(cudaEventRecord(ctx->ev[2], main_s));
     CK(cudaStreamWaitEvent(comm_s, ctx->ev[2], 0));
@@ -278,7 +289,6 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
     dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
     ctx->stream = main_s;
     dev_free(ctx, order, sizeof(int32_t) * cw->nsegs);
-    if (!st && selfcheck_mode()) selfcheck_gemm(ctx, cw, A, B, nullptr, m, epi);
     return st;
 }
 
@@ -304,6 +314,7 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
     }
     g_product_id++;
     if (selfcheck_mode()) selfcheck_cull(ctx, cw, A, B, tau, transA);
+    if (ctx->vsink) ST(volume_record(ctx, cw));
     const bool overlap = A->dist && A->parts.world > 1;
     double *halo = nullptr;
     int64_t nhalo = 0;
@@ -433,22 +444,31 @@ static spamm_status ns_step_batched(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, dou
         return !(e && *e == '0');
     }();
     if (!st) st = ensure_side_stream(ctx);
+    bool side_queued = false;   // work is queued on the side stream: it must be joined
     if (!st && !conc) {
         st = cull_start(ctx, c2, H, Z, tau, H->r0, H->r1);
-        if (!st && cudaEventRecord(ctx->ev[1], main_s) != cudaSuccess) st = set_err(ctx, SPAMM_ECUDA, "event");
-    } else if (!st && cudaEventRecord(ctx->ev[0], main_s) == cudaSuccess &&
-        cudaStreamWaitEvent(ctx->comm_stream, ctx->ev[0], 0) == cudaSuccess) {
-        ctx->stream = ctx->comm_stream;
-        st = cull_start(ctx, c2, H, Z, tau, H->r0, H->r1);
-        ctx->stream = main_s;
-        if (!st && (cudaEventRecord(ctx->ev[1], ctx->comm_stream) != cudaSuccess))
-            st = set_err(ctx, SPAMM_ECUDA, "event record");
     } else if (!st) {
-        st = set_err(ctx, SPAMM_ECUDA, "side stream join");
+        if (cudaEventRecord(ctx->ev[0], main_s) == cudaSuccess &&
+            cudaStreamWaitEvent(ctx->comm_stream, ctx->ev[0], 0) == cudaSuccess) {
+            side_queued = true;
+            ctx->stream = ctx->comm_stream;
+            st = cull_start(ctx, c2, H, Z, tau, H->r0, H->r1);
+            ctx->stream = main_s;
+        } else {
+            st = set_err(ctx, SPAMM_ECUDA, "side stream fork");
+        }
     }
     if (!st) st = cull_start(ctx, c1, Y, H, tau_s, Y->r0, Y->r1);
-    if (!st && cudaStreamWaitEvent(main_s, ctx->ev[1], 0) != cudaSuccess)
-        st = set_err(ctx, SPAMM_ECUDA, "side stream join");
+    // join the side stream whatever happened above: the caller frees H (whose pyramid
+    // and slot map the side cull reads) with stream-ordered frees on main_s
+    if (side_queued) {
+        const bool joined = cudaEventRecord(ctx->ev[1], ctx->comm_stream) == cudaSuccess &&
+                            cudaStreamWaitEvent(main_s, ctx->ev[1], 0) == cudaSuccess;
+        if (!joined) {
+            cudaStreamSynchronize(ctx->comm_stream);   // last resort: drain it from the host
+            if (!st) st = set_err(ctx, SPAMM_ECUDA, "side stream join");
+        }
+    }
     int64_t added = 0;
     double tt = 0.0;
     if (!st) {

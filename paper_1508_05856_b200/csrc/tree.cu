@@ -135,6 +135,7 @@ spamm_status mat_new(spamm_ctx ctx, int64_t n, int b, int64_t cap, spamm_mat *ou
     ST(mat_parts(ctx, (int)nb, &parts));
     spamm_mat m = new spamm_mat_s();
     m->ctx = ctx;
+    ctx->live_mats.fetch_add(1);
     m->n = n; m->b = b; m->nb = (int)nb; m->L = L;
     m->cap = cap;
     m->parts = parts;
@@ -163,6 +164,8 @@ extern "C" void spamm_mat_free(spamm_mat m)
     dev_free(ctx, m->pool, sizeof(double) * (size_t)(m->cap > 0 ? m->cap : 1) * m->b * m->b);
     dev_free(ctx, m->coord, sizeof(int32_t) * (m->cap > 0 ? m->cap : 1));
     delete m;
+    // the last matrix of a context whose destroy was deferred
+    if (ctx->live_mats.fetch_sub(1) == 1 && ctx->destroy_pending.load()) ctx_teardown(ctx);
 }
 
 spamm_status mat_reset_pattern(spamm_ctx ctx, spamm_mat m)

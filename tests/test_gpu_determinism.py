@@ -122,3 +122,28 @@ def test_allocators_agree_bitwise(gpu):
         out.append((r["t"].copy(), _hash(ctx, r["Y"]), _hash(ctx, r["Z"]), r["c"]))
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1:] == out[1][1:]
+
+
+def test_ab_switches_bitwise():
+    """The A/B switches change stream and launch ordering only: SPAMM_CONCURRENT_CULL=0/1
+    (the Z' cull on the side stream or after the Y' cull) and SPAMM_PDL=0/1 (programmatic
+    dependent launch or plain stream order) give the same NS run bitwise (t_k, Y, Z)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_1508_05856_b200 as sp, spamm_inputs as si\n"
+            "c = si.CONFIGS['C2']; s = si.kms(c.n, c.rho); ctx = sp.spamm_ctx_create(0)\n"
+            "S = sp.spamm_build_tree(ctx, s, c.b); r = sp.spamm_ns_sqrt(ctx, S, c.tau, 12)\n"
+            "h = hashlib.sha1(r['t'].tobytes())\n"
+            "for M in (r['Y'], r['Z']):\n"
+            "    bi, bj, blk = sp.spamm_export_blocks(ctx, M); o = np.lexsort((bj, bi))\n"
+            "    h.update(bi[o].tobytes() + bj[o].tobytes() + blk[o].tobytes())\n"
+            "print('hash', h.hexdigest())\n") % ROOT
+    seen = {}
+    for conc in ("0", "1"):
+        for pdl in ("0", "1"):
+            p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                               env={**os.environ, "SPAMM_CONCURRENT_CULL": conc, "SPAMM_PDL": pdl})
+            assert p.returncode == 0, p.stderr[-2000:]
+            seen[(conc, pdl)] = [l for l in p.stdout.splitlines() if l.startswith("hash")][-1]
+    assert len(set(seen.values())) == 1, seen

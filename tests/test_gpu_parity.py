@@ -12,6 +12,7 @@ import math
 import numpy as np
 import pytest
 
+import _parity as P
 import oracle as O
 import spamm_inputs as si
 
@@ -68,24 +69,20 @@ def rel(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-def window_set(A_o, B_o, tau):
-    """Triples within 1e-12 relative of the threshold (leaf norms from the oracle)."""
-    na, nb_ = A_o.leaf_norms(), B_o.leaf_norms()
-    thr = tau * A_o.norm() * B_o.norm()
-    prod = na[:, :, None] * nb_[None, :, :]
-    amb = (na[:, :, None] > 0) & (nb_[None, :, :] > 0) & (np.abs(prod - thr) <= 1e-12 * thr)
-    return {tuple(x) for x in np.argwhere(amb)}
-
-
-def check_product(ctx, A, Ao, B, Bo, tau, vals_tol=1e-12):
-    C, st = sp().spamm_multiply(ctx, A, B, tau, want_stats=True)
+def check_product(ctx, A, Ao, B, Bo, tau, vals_tol=1e-12, trans_a=False):
+    """SURVEY.md §8(c) protocol for one product: the task set equals the oracle's except
+    within the 1e-12 window; the values, flip-corrected, agree to vals_tol over the union
+    of both sides' blocks; the epilogue's leaf norms agree with the corrected blocks'."""
+    mul = sp().spamm_multiply_t if trans_a else sp().spamm_multiply
+    C, st = mul(ctx, A, B, tau, want_stats=True)
     tg = sp().spamm_export_tasks(ctx)
-    Co, to = O.multiply(Ao, Bo, tau, want_tasks=True)
-    sg = {tuple(x) for x in tg}
-    so = {tuple(x) for x in to}
+    Co, to = O.multiply(Ao, Bo, tau, want_tasks=True, trans_a=trans_a)
+    Al = O.transpose(Ao) if trans_a else Ao
+    sg, so = P.triples(tg), P.triples(to)
     assert len(sg) == len(tg) == st["tasks"]
-    diff = sg ^ so
-    assert diff <= window_set(Ao, Bo, tau), f"{len(diff)} task flips outside the window"
+    only_g, only_o = sg - so, so - sg
+    bad = P.outside_window(only_g | only_o, Al, Bo, tau)
+    assert not bad, f"{len(bad)} task flips outside the window: {bad[:5]}"
     # tasks grouped by output block (Morton order), k ascending inside a segment
     if len(tg):
         ij = tg[:, 0].astype(np.int64) * (1 << 20) + tg[:, 2]
@@ -94,23 +91,17 @@ def check_product(ctx, A, Ao, B, Bo, tau, vals_tol=1e-12):
         assert len(np.unique(ij)) == len(starts) == st["segments"]
         for s0, s1 in zip(starts, np.r_[starts[1:], len(tg)]):
             assert np.all(np.diff(tg[s0:s1, 1]) > 0)
-    if not diff:
-        Cg = gpu_to_oracle(ctx, C)
-        n = Ao.n
-        if n <= 4096:
-            assert rel(Cg.to_dense(), Co.to_dense()) <= vals_tol
-        else:
-            bi, bj = Co.block_coords()
-            err = 0.0
-            for I, J in zip(bi, bj):
-                g = Cg.block(I, J)
-                o = Co.block(I, J)
-                err += np.sum((g - o) ** 2)
-            assert math.sqrt(err) <= vals_tol * Co.norm()
-        # norms of C: leaf norm^2 from the epilogue
-        L = (n // Ao.b).bit_length() - 1
-        n2 = sp().spamm_level_norms2(ctx, C, L)
-        np.testing.assert_allclose(np.sqrt(n2), Co.leaf_norms(), rtol=1e-12, atol=1e-300)
+    gb = P.gpu_blocks(sp(), ctx, C)
+    ob = P.flip_correct(P.oracle_blocks(Co), Al, Bo, only_g, only_o)
+    assert P.rel_union(gb, ob) <= vals_tol
+    # every stored GPU block has a non-zero epilogue norm, and the norms match
+    L = (Ao.n // Ao.b).bit_length() - 1
+    n2 = sp().spamm_level_norms2(ctx, C, L)
+    ref = np.zeros_like(n2)
+    for (I, J), o in ob.items():
+        ref[I, J] = np.sqrt(np.sum(o * o))
+    assert set(zip(*np.nonzero(n2 > 0))) == set(gb)
+    np.testing.assert_allclose(np.sqrt(n2), ref, rtol=1e-12, atol=1e-300)
     return C, Co
 
 
@@ -369,15 +360,7 @@ def test_multiply_transposed(ctx, n, b, tau):
     a[:b, 2 * b:3 * b] = 0.0
     A, Ao = build_pair(ctx, "dense", a, b, n)
     B, Bo = build_pair(ctx, "dense", c, b, n)
-    Cg, st = sp().spamm_multiply_t(ctx, A, B, tau, want_stats=True)
-    tg = {tuple(x) for x in sp().spamm_export_tasks(ctx)}
-    Co, to = O.multiply(Ao, Bo, tau, want_tasks=True, trans_a=True)
-    so = {tuple(x) for x in to}
-    assert len(tg) == st["tasks"]
-    diff = tg ^ so
-    assert diff <= window_set(O.transpose(Ao), Bo, tau)
-    if not diff:
-        assert rel(gpu_to_oracle(ctx, Cg).to_dense(), Co.to_dense()) <= 1e-12
+    Cg, _ = check_product(ctx, A, Ao, B, Bo, tau, trans_a=True)
     if tau == 0.0:
         assert rel(sp().spamm_to_dense(ctx, Cg).cpu().numpy(), a.T @ c) <= 1e-13
 

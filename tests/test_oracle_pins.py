@@ -361,6 +361,42 @@ def test_power_scale():
     assert c >= 0.99 * lmax
 
 
+@pytest.mark.parametrize("K", [0, 1, 3, 10])
+def test_power_scale_rayleigh_closed_form(K):
+    """Reading L12: c = v_K^T s v_K after K normalised power steps from
+    v_0 = 1/sqrt(n) 1.  For s = diag(2 I_{n/2}, I_{n/2}), v_K is proportional to
+    [2^K 1, 1], so c = (2^(2K+1) + 1)/(2^(2K) + 1) exactly; the norm ||s v_K||
+    (a plausible mistake) would give sqrt((2^(2K+2) + 1)/(2^(2K) + 1)) instead."""
+    n, b = 64, 16
+    s = np.diag(np.r_[np.full(n // 2, 2.0), np.ones(n // 2)])
+    c = O.power_scale(O.OMat.from_dense(s, b), K)
+    exact = (2.0 ** (2 * K + 1) + 1) / (2.0 ** (2 * K) + 1)
+    wrong = np.sqrt((2.0 ** (2 * K + 2) + 1) / (2.0 ** (2 * K) + 1))
+    assert c == pytest.approx(exact, rel=1e-14)
+    assert wrong != pytest.approx(exact, rel=1e-10)   # the pin tells them apart
+
+
+def test_ns_y0_mu_fills_absent_diagonal_blocks():
+    """Op 1 (reading L13): Y0 = (s/c + mu I)/(1+mu) everywhere, including diagonal blocks
+    that s does not store (there Y0_ii = mu/(1+mu) I), against numpy on the dense s."""
+    n, b, c, mu = 128, 16, 3.0, 1e-2
+    s = np.abs(_rng(11).standard_normal((n, n)))
+    s = s + s.T
+    for I in (2, 5):                   # diagonal blocks absent from s
+        s[I * b:(I + 1) * b, I * b:(I + 1) * b] = 0.0
+    s[0:b, 3 * b:4 * b] = s[3 * b:4 * b, 0:b] = 0.0   # and an off-diagonal pair
+    S = O.OMat.from_dense(s, b)
+    assert S.block(2, 2) is None and S.block(5, 5) is None
+    Y0 = O.ns_y0(S, c, mu)
+    ref = (s / c + mu * np.eye(n)) / (1 + mu)
+    assert np.array_equal(Y0.to_dense(), ref)
+    assert np.array_equal(Y0.block(2, 2), mu / (1 + mu) * np.eye(b))
+    assert Y0.block(0, 3) is None       # only the diagonal is filled
+    assert Y0.nblocks() == S.nblocks() + 2
+    # mu = 0: the plain s/c, absent blocks stay absent
+    assert O.ns_y0(S, c).block(2, 2) is None
+
+
 # ------------------------------------------- scaled / stabilised map (§8(f) f1)
 def test_scaled_map_sigmoids_paper_values():
     """P:442-448: alpha(t) = 1 + 1.85/(1 + e^{-50(t-.35)}), eps(t) = .1/(1 + e^{-75(t-.30)}):
