@@ -78,6 +78,8 @@ struct spamm_ctx_s {
     // live matrices defers the teardown to the last spamm_mat_free (their memory
     // comes from the context's pool / allocator)
     spamm_volume_sink *vsink = nullptr;   // per-product recorder (f4), nullable
+    struct NsGraph *nsg = nullptr;        // cached graph-replayed NS step (spamm.cu)
+    bool capturing = false;               // inside a CUDA graph capture (no prof events)
     std::atomic<int64_t> live_mats{0};
     std::atomic<bool> destroy_pending{false};
 };
@@ -319,6 +321,7 @@ struct Cull {
     int prevL = -1;
     int32_t prev[SPAMM_MAX_L + 2] = {};
     double alpha = 1.0;           // EPI_STORE output scale of the next GEMM (fused unscale)
+    int64_t gen = 0;              // bumped by every (re)allocation (captured graphs check it)
     spamm_stats stats{};
 };
 // Enqueue the query, synchronise once to read the counts, and grow + re-run
@@ -327,6 +330,10 @@ spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double 
                       int transA = 0);
 spamm_status cull_start(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
                         int transA = 0);
+// enqueue only (fixed workspace, capacity-sized grids): for CUDA graph capture
+spamm_status cull_enqueue_fixed(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau);
+// (re)allocate a workspace for at least cap tasks per level and cap_segs segments
+spamm_status cull_reserve(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap_segs);
 spamm_status cull_complete(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
                            int transA = 0);
 void cull_free(spamm_ctx ctx, Cull *cw);
@@ -338,9 +345,15 @@ spamm_status volume_record(spamm_ctx ctx, Cull *cw);
 enum { EPI_STORE = 0, EPI_NS_H = 1, EPI_NS_X = 2 };
 // seg_order (nullable) / nseg (< 0 => all cw->nsegs) select the segments of this launch;
 // ticket = which of the GEMM ticket counters (zeroed by the cull) the launch uses
+// device_count: the launch reads the segment count from cw->counters (device-driven
+// steps, CUDA graph capture) and runs a full persistent grid
 spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
                       spamm_mat C, int epi, double *trace_part, const int32_t *seg_order = nullptr,
-                      int64_t nseg = -1, int ticket = 0, int transA = 0);
+                      int64_t nseg = -1, int ticket = 0, int transA = 0, bool device_count = false);
+// diag_fixup with the base slot read from the device (the X cull's segment count) and
+// caller-provided scratch (newslot [nb]); no allocation, no host round trip
+spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, double value, int32_t *newslot,
+                            int64_t *dcount);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
 // as diag_fixup without the host round trip: the count of appended blocks lands in
 // *dcount (device); the caller fetches it and sets H->nblk = nseg + count

@@ -384,6 +384,7 @@ void cull_free(spamm_ctx ctx, Cull *cw)
 static spamm_status cull_alloc(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap_segs)
 {
     cull_free(ctx, cw);
+    cw->gen++;
     cw->cap = cap;
     cw->cap_segs = cap_segs;
     cw->tiles = cdiv(cap + 1, CT * CI);
@@ -438,7 +439,7 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     CKL(ctx);
     const int persist = 2 * ctx->sm_count;
     // grids sized from the previous query's level counts (+25 %), else the capacity
-    const bool have_prev = cw->prevL == L;
+    const bool have_prev = cw->prevL == L && !ctx->capturing;
     auto expect = [&](int l) -> int64_t {
         return have_prev ? (int64_t)cw->prev[l] + cw->prev[l] / 4 + 1 : cw->cap;
     };
@@ -476,6 +477,19 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     CK(launch_pdl(k_cull_segments, scan_grid(L), CT, 0, s, cw->rec[cur], L, cw->cap, cw->cap_segs, st, cw->seg_code,
                   cw->seg_start, cw->seg_len, cw->counters));
     CKL(ctx);
+    return SPAMM_OK;
+}
+
+spamm_status cull_enqueue_fixed(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau)
+{
+    return cull_enqueue(ctx, cw, A, B, tau, 0, A->nb, 0);
+}
+
+spamm_status cull_reserve(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap_segs)
+{
+    if (cw->tA && cw->cap >= cap && cw->cap_segs >= cap_segs) return SPAMM_OK;
+    ST(cull_alloc(ctx, cw, std::max(cap, cw->cap), std::max(cap_segs, cw->cap_segs)));
+    if (cw->hint < cw->cap) cw->hint = cw->cap;
     return SPAMM_OK;
 }
 

@@ -44,6 +44,8 @@ struct GemmArgs {
     double *trace_part;
     int32_t *ticket;   // dynamic segment scheduler (zeroed before the launch)
     double alpha;      // EPI_STORE: C = alpha (A (x) B) (the final unscale of the NS run, fused)
+    const int32_t *nseg_dev;   // non-null: the segment count is read here (device-driven
+                               // steps: the cull's count, no host round trip)
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b)
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
             int seg = 0, start = 0, len = 0;
             if (lane == 0) {
                 seg = atomicAdd(g.ticket, 1);
-                if (seg >= g.nseg) seg = -1;
+                if (seg >= (g.nseg_dev ? *g.nseg_dev : g.nseg)) seg = -1;
                 else if (g.seg_order) seg = g.seg_order[seg];
                 int code = 0;
                 if (seg >= 0) {
@@ -390,10 +392,10 @@ static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
         if (e == cudaSuccess) occ_cache.store(o < 1 ? 1 : o);
         return e;
     }));
-    if (g.nseg == 0) return SPAMM_OK;
+    if (g.nseg == 0 && !g.nseg_dev) return SPAMM_OK;
     const int occ = occ_cache.load();
     int grid = ctx->sm_count * occ;
-    if (grid > g.nseg) grid = g.nseg;
+    if (!g.nseg_dev && grid > g.nseg) grid = g.nseg;
     kern<<<grid, NT, smem, ctx->stream>>>(g);
     CKL(ctx);
     return SPAMM_OK;
@@ -412,12 +414,13 @@ static spamm_status gemm_dispatch(spamm_ctx ctx, int b, const GemmArgs &g)
 
 spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
                       spamm_mat C, int epi, double *trace_part, const int32_t *seg_order, int64_t nseg,
-                      int ticket, int transA)
+                      int ticket, int transA, bool device_count)
 {
     if (nseg < 0) nseg = cw->nsegs;
     GemmArgs g{A->pool, B->pool, b_halo, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
                (int)nseg, seg_order, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
-               cw->counters + CNT_GEMM_TICKET + ticket, cw->alpha};
+               cw->counters + CNT_GEMM_TICKET + ticket, cw->alpha,
+               device_count ? cw->counters + CNT_NSEG : nullptr};
     if (transA) {
         if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 1>(ctx, A->b, g);
         if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 1>(ctx, A->b, g);
@@ -489,11 +492,12 @@ spamm_status lpt_order(spamm_ctx ctx, const int32_t *seg_len, const int32_t *in,
 // nseg.. in ascending i (single-CTA scan, deterministic), then filled in parallel.
 template <int THREADS>
 __global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int r0, int r1, int64_t base,
-                              int32_t *newslot, int64_t *count_out)
+                              int32_t *newslot, int64_t *count_out, const int32_t *base_dev)
 {
     pdl_wait();
     pdl_trigger();
     __shared__ V1 sw[THREADS / 32];
+    if (base_dev) base = *base_dev;   // device-driven step: after the X product's segments
     int64_t run = 0;
     for (int i0 = 0; i0 < nb; i0 += THREADS) {
         int i = i0 + threadIdx.x;
@@ -537,7 +541,7 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
     int32_t *newslot = dalloc<int32_t>(ctx, m->nb);
     if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
     CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, m->slot, m->coord, m->nb, m->r0, m->r1, base, newslot,
-                ctx->iscratch));
+                ctx->iscratch, (const int32_t *)nullptr));
     CKL(ctx);
     CK(launch_k(ctx, k_diag_fill, m->nb, 256, 0, (const int32_t *)newslot, m->pool, m->b, value,
                 m->norm2 + pyr_off(m->L)));
@@ -553,13 +557,26 @@ spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double v
 {
     int32_t *newslot = dalloc<int32_t>(ctx, H->nb);
     if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
-    CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, nseg, newslot, dcount));
+    CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, nseg, newslot, dcount,
+                (const int32_t *)nullptr));
     CKL(ctx);
     CK(launch_k(ctx, k_diag_fill, H->nb, 256, 0, (const int32_t *)newslot, H->pool, H->b, value,
                 H->norm2 + pyr_off(H->L)));
     CKL(ctx);
     dev_free(ctx, newslot, sizeof(int32_t) * H->nb);
     H->nblk = nseg;   // provisional until the caller has fetched *dcount
+    return SPAMM_OK;
+}
+
+spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, double value, int32_t *newslot,
+                            int64_t *dcount)
+{
+    CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, (int64_t)0, newslot,
+                dcount, nseg_dev));
+    CKL(ctx);
+    CK(launch_k(ctx, k_diag_fill, H->nb, 256, 0, (const int32_t *)newslot, H->pool, H->b, value,
+                H->norm2 + pyr_off(H->L)));
+    CKL(ctx);
     return SPAMM_OK;
 }
 

@@ -37,7 +37,7 @@ static cudaEvent_t ev_get(Prof *p)
 int prof_begin(spamm_ctx ctx, int phase)
 {
     Prof *p = (Prof *)ctx->prof;
-    if (!p || !p->on) return -1;
+    if (!p || !p->on || ctx->capturing) return -1;
     cudaEvent_t a = ev_get(p);
     cudaEventRecord(a, ctx->stream);
     p->ivs.push_back({phase, a, nullptr});

@@ -11,8 +11,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
+
+static void ns_graph_free(spamm_ctx ctx);
 
 extern "C" spamm_status spamm_ctx_create(int device, void *cuda_stream, const spamm_allocator *allocator,
                                          spamm_ctx *out)
@@ -79,6 +82,7 @@ extern "C" void spamm_ctx_destroy(spamm_ctx ctx)
     if (!ctx) return;
     // matrices still alive: they own memory of this context (its pool / allocator) and
     // point back at it, so the teardown waits for the last spamm_mat_free
+    ns_graph_free(ctx);   // its buffers are matrices of this context
     ctx->destroy_pending.store(true);
     if (ctx->live_mats.load() > 0) return;
     ctx_teardown(ctx);
@@ -627,6 +631,287 @@ extern "C" spamm_status spamm_power_scale(spamm_ctx ctx, spamm_mat s, int32_t K,
     return power_scale(ctx, s, K, c);
 }
 
+// ------------------------------------------------ graph-replayed NS steps
+// Small problems are latency-bound (C1: ~25 launches and 2 host round trips per step
+// for ~1 MFLOP).  When the worst-case workspace fits a memory budget, the dual step is
+// made device-driven and captured once as a CUDA graph:
+//   * every capacity is the worst case (cull levels <= nb^3 triples, segments and
+//     output blocks <= nb^2), so nothing can overflow and no count is needed on the host;
+//   * the GEMMs read their segment count from the cull's counters, the diagonal
+//     fix-up its base slot; grids are capacity-sized (the kernels loop over their work);
+//   * matrices ping-pong between two fixed buffer sets (Y_k, Z_k) -> (Y_k+1, Z_k+1);
+//   * a record kernel appends t_k, the three products' level counts and the root
+//     norms of Y', Z' to a device log, read once after the last replay.
+// Same kernels, same arguments, same orders as the host-driven step: the results are
+// bitwise those of the classic path (tests/test_gpu_determinism.py).  The last step
+// (fused final unscale) runs host-driven.  Any non-finite value in the log sends the
+// whole run back to the host-driven loop (which stops at the failing step).
+struct StepRec {
+    double t, ny2, nz2, pad;
+    int32_t cnt[3][20];   // per product: level counts [0..15], overflow [16], segments [17]
+};
+
+__global__ void k_step_record(double *t_dev, const int32_t *c0, const int32_t *c1, const int32_t *c2,
+                              const double *ny2, const double *nz2, StepRec *rec, int32_t *k)
+{
+    pdl_wait();
+    const int i = *k;
+    StepRec &r = rec[i];
+    const int32_t *c[3] = {c0, c1, c2};
+    for (int e = threadIdx.x; e < 60; e += blockDim.x) r.cnt[e / 20][e % 20] = c[e / 20][e % 20];
+    if (threadIdx.x == 0) {
+        r.t = *t_dev;
+        r.ny2 = *ny2;
+        r.nz2 = *nz2;
+        r.pad = 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *k = i + 1;
+}
+
+struct NsGraph {
+    int64_t n = 0;
+    int b = 0;
+    double tau = -1.0, tau_s = -1.0;
+    spamm_mat Yb[2] = {nullptr, nullptr}, Zb[2] = {nullptr, nullptr}, H = nullptr;
+    double *trace_part = nullptr;
+    int32_t *newslot = nullptr;
+    int64_t *hadd = nullptr;
+    StepRec *rec = nullptr;
+    int rec_cap = 0;
+    int32_t *kdev = nullptr;
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    int64_t kernels[2] = {0, 0};
+    int64_t gen[3] = {-1, -1, -1};
+};
+
+static void ns_graph_free(spamm_ctx ctx)
+{
+    NsGraph *g = ctx->nsg;
+    if (!g) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &e : g->exec)
+        if (e) cudaGraphExecDestroy(e);
+    for (spamm_mat m : {g->Yb[0], g->Yb[1], g->Zb[0], g->Zb[1], g->H}) spamm_mat_free(m);
+    const int nb = (int)(g->b ? g->n / g->b : 0);
+    dev_free(ctx, g->trace_part, sizeof(double) * nb);
+    dev_free(ctx, g->newslot, sizeof(int32_t) * nb);
+    dev_free(ctx, g->hadd, sizeof(int64_t));
+    dev_free(ctx, g->rec, sizeof(StepRec) * g->rec_cap);
+    dev_free(ctx, g->kdev, sizeof(int32_t));
+    delete g;
+    ctx->nsg = nullptr;
+}
+
+// SPAMM_GRAPH: 0 = off, 1 = auto (worst case <= 4 GiB, default), 2 = up to 32 GiB
+static int graph_mode()
+{
+    static const int m = [] {
+        const char *e = getenv("SPAMM_GRAPH");
+        return e && *e ? atoi(e) : 1;
+    }();
+    return m;
+}
+
+static bool ns_graph_eligible(spamm_ctx ctx, spamm_mat s, const spamm_ns_opts &o, int iters)
+{
+    const int gm = graph_mode();
+    if (!gm || s->dist || o.map != 0 || o.t_stop > 0.0 || iters < 2 || ctx->vsink || selfcheck_mode() ||
+        lpt_mode())
+        return false;
+    const double nb = (double)s->nb, b2 = (double)s->b * s->b;
+    const double mats = 5.0 * (nb * nb * (8.0 * b2 + 8.0) + 8.0 * (double)pyr_size(s->L));
+    const double culls = 3.0 * nb * nb * nb * 61.0;
+    return mats + culls <= (gm >= 2 ? 32.0 : 4.0) * (1u << 30);
+}
+
+// One device-driven dual step: (Y, Z) -> (Yn, Zn) through the fixed buffers (captured).
+static spamm_status graph_step(spamm_ctx ctx, NsGraph *g, spamm_mat Y, spamm_mat Z, spamm_mat Yn, spamm_mat Zn)
+{
+    Cull *c0 = ctx->cw[0], *c1 = ctx->cw[1], *c2 = ctx->cw[2];
+    spamm_mat H = g->H;
+    const int nb = Y->nb;
+    // X = Z (x)_tau Y -> H = 1/2 (3I - X), tr X partials, absent diagonal blocks 1.5 I
+    ST(cull_enqueue_fixed(ctx, c0, Z, Y, g->tau));
+    CK(cudaMemsetAsync(g->trace_part, 0, sizeof(double) * nb, ctx->stream));
+    ST(mat_reset_pattern(ctx, H));
+    c0->alpha = 1.0;
+    ST(gemm_run(ctx, c0, Z, Y, nullptr, H, EPI_NS_H, g->trace_part, nullptr, 0, 0, 0, true));
+    ST(diag_fixup_dev(ctx, H, c0->counters + CNT_NSEG, 1.5, g->newslot, g->hadd));
+    ST(pyramid_build(ctx, H));
+    ST(trace_finish(ctx, g->trace_part, nb, Y->n, ctx->dscratch));
+    // Y' and Z' culls as two branches (the Z' cull on the side stream)
+    const cudaStream_t main_s = ctx->stream;
+    CK(cudaEventRecord(ctx->ev[0], main_s));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev[0], 0));
+    ctx->stream = ctx->comm_stream;
+    spamm_status st = cull_enqueue_fixed(ctx, c2, H, Z, g->tau);
+    ctx->stream = main_s;
+    ST(st);
+    ST(cull_enqueue_fixed(ctx, c1, Y, H, g->tau_s));
+    CK(cudaEventRecord(ctx->ev[1], ctx->comm_stream));
+    CK(cudaStreamWaitEvent(main_s, ctx->ev[1], 0));
+    // Y' = Y (x)_tau_s H ; Z' = H (x)_tau Z
+    c1->alpha = c2->alpha = 1.0;
+    ST(mat_reset_pattern(ctx, Yn));
+    ST(gemm_run(ctx, c1, Y, H, nullptr, Yn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true));
+    ST(pyramid_build(ctx, Yn));
+    ST(mat_reset_pattern(ctx, Zn));
+    ST(gemm_run(ctx, c2, H, Z, nullptr, Zn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true));
+    ST(pyramid_build(ctx, Zn));
+    CK(launch_pdl(k_step_record, 1, 64, 0, ctx->stream, ctx->dscratch, (const int32_t *)c0->counters,
+                  (const int32_t *)c1->counters, (const int32_t *)c2->counters, (const double *)Yn->norm2,
+                  (const double *)Zn->norm2, g->rec, g->kdev));
+    CKL(ctx);
+    return SPAMM_OK;
+}
+
+static spamm_status ns_graph_prepare(spamm_ctx ctx, spamm_mat s, double tau, double tau_s, int steps)
+{
+    NsGraph *g = ctx->nsg;
+    const int64_t nb = s->nb;
+    const bool same = g && g->n == s->n && g->b == s->b && g->tau == tau && g->tau_s == tau_s;
+    if (!same) {
+        ns_graph_free(ctx);
+        g = ctx->nsg = new NsGraph();
+        g->n = s->n;
+        g->b = s->b;
+        g->tau = tau;
+        g->tau_s = tau_s;
+        spamm_mat *all[5] = {&g->Yb[0], &g->Yb[1], &g->Zb[0], &g->Zb[1], &g->H};
+        for (spamm_mat *m : all) ST(mat_new(ctx, s->n, s->b, nb * nb, m));
+        g->trace_part = dalloc<double>(ctx, nb);
+        g->newslot = dalloc<int32_t>(ctx, nb);
+        g->hadd = dalloc<int64_t>(ctx, 1);
+        g->kdev = dalloc<int32_t>(ctx, 1);
+        if (!g->trace_part || !g->newslot || !g->hadd || !g->kdev) return set_err(ctx, SPAMM_ENOMEM, "graph state");
+    }
+    if (g->rec_cap < steps) {
+        dev_free(ctx, g->rec, sizeof(StepRec) * g->rec_cap);
+        g->rec_cap = std::max(steps, 64);
+        g->rec = dalloc<StepRec>(ctx, g->rec_cap);
+        if (!g->rec) {
+            g->rec_cap = 0;
+            return set_err(ctx, SPAMM_ENOMEM, "graph log");
+        }
+        for (auto &e : g->exec)   // the log pointer is baked into the graphs
+            if (e) {
+                cudaGraphExecDestroy(e);
+                e = nullptr;
+            }
+    }
+    for (int i = 0; i < 3; i++) {
+        ST(cull_reserve(ctx, ctx->cw[i], nb * nb * nb, nb * nb));
+        if (ctx->cw[i]->gen != g->gen[i]) {
+            for (auto &e : g->exec)
+                if (e) {
+                    cudaGraphExecDestroy(e);
+                    e = nullptr;
+                }
+        }
+    }
+    ST(ensure_side_stream(ctx));
+    for (int p = 0; p < 2; p++) {
+        if (g->exec[p]) continue;
+        for (int i = 0; i < 3; i++) ctx->cw[i]->prevL = -1;
+        const int64_t l0 = ctx->launches;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        ctx->capturing = true;
+        spamm_status st = graph_step(ctx, g, g->Yb[p], g->Zb[p], g->Yb[p ^ 1], g->Zb[p ^ 1]);
+        ctx->capturing = false;
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+        g->kernels[p] = ctx->launches - l0;
+        ctx->launches = l0;
+        if (st) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (e != cudaSuccess) return check_cuda(ctx, e, "graph capture");
+        e = cudaGraphInstantiate(&g->exec[p], graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            g->exec[p] = nullptr;
+            return check_cuda(ctx, e, "graph instantiate");
+        }
+    }
+    for (int i = 0; i < 3; i++) g->gen[i] = ctx->cw[i]->gen;
+    return SPAMM_OK;
+}
+
+static spamm_status mat_copy_into(spamm_ctx ctx, spamm_mat dst, spamm_mat src)
+{
+    const int64_t nb = src->nb;
+    CK(cudaMemcpyAsync(dst->norm2, src->norm2, sizeof(double) * pyr_size(src->L), cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(dst->slot, src->slot, sizeof(int32_t) * nb * nb, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (src->nblk > 0) {
+        CK(cudaMemcpyAsync(dst->pool, src->pool, sizeof(double) * src->nblk * src->b * src->b,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(dst->coord, src->coord, sizeof(int32_t) * src->nblk, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+    }
+    dst->nblk = src->nblk;
+    return SPAMM_OK;
+}
+
+static void rec_stats(const StepRec &r, int L, int b, spamm_stats *out)
+{
+    const int l0 = L < 4 ? L : 4;   // cull.cu INIT_L0
+    for (int p = 0; p < 3; p++) {
+        spamm_stats &s = out[p];
+        s = spamm_stats{};
+        s.tasks = r.cnt[p][L];
+        s.segments = r.cnt[p][CNT_NSEG];
+        for (int l = l0; l <= L && l < 24; l++) s.level_survivors[l] = r.cnt[p][l];
+        s.candidates = L > l0 ? 8 * (int64_t)r.cnt[p][L - 1] : ((int64_t)1 << (3 * L));
+        s.flops = 2.0 * (double)b * b * b * (double)s.tasks;
+    }
+}
+
+// Runs `steps` dual steps from (Y, Z) by graph replay.  On success *Yk, *Zk are the
+// context's buffers holding (Y_steps, Z_steps) (borrowed: owned by ctx->nsg) and the
+// history is filled; *ok = false (and SPAMM_OK) when the log shows a non-finite value
+// or an overflow: the caller redoes the run host-driven.
+static spamm_status ns_graph_run(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double tau, double tau_s, int steps,
+                                 const spamm_ns_opts &o, spamm_mat *Yk, spamm_mat *Zk, bool *ok)
+{
+    *ok = false;
+    ST(ns_graph_prepare(ctx, Y, tau, tau_s, steps));
+    NsGraph *g = ctx->nsg;
+    ST(mat_copy_into(ctx, g->Yb[0], Y));
+    ST(mat_copy_into(ctx, g->Zb[0], Z));
+    CK(cudaMemsetAsync(g->kdev, 0, sizeof(int32_t), ctx->stream));
+    for (int k = 0; k < steps; k++) {
+        CK(cudaGraphLaunch(g->exec[k & 1], ctx->stream));
+        ctx->launches += g->kernels[k & 1];
+    }
+    std::vector<StepRec> rec(steps);
+    CK(cudaMemcpyAsync(rec.data(), g->rec, sizeof(StepRec) * steps, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const int L = Y->L, b = Y->b;
+    for (int k = 0; k < steps; k++) {
+        const StepRec &r = rec[k];
+        if (!std::isfinite(r.t) || !std::isfinite(r.ny2) || !std::isfinite(r.nz2)) return SPAMM_OK;
+        for (int p = 0; p < 3; p++)
+            if (r.cnt[p][CNT_OVERFLOW]) return SPAMM_OK;
+    }
+    for (int k = 0; k < steps; k++) {
+        spamm_stats st[3];
+        rec_stats(rec[k], L, b, st);
+        if (o.t_history) o.t_history[k] = rec[k].t;
+        if (o.per_product) memcpy(o.per_product + 3 * k, st, sizeof(st));
+        for (int p = 0; p < 3; p++) prof_gemm_work(ctx, st[p].tasks, st[p].segments, b);
+    }
+    const int q = steps & 1;
+    g->Yb[q]->nblk = rec[steps - 1].cnt[1][CNT_NSEG];
+    g->Zb[q]->nblk = rec[steps - 1].cnt[2][CNT_NSEG];
+    *Yk = g->Yb[q];
+    *Zk = g->Zb[q];
+    *ok = true;
+    return SPAMM_OK;
+}
+
 extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, int32_t iters, spamm_mat *Yout,
                                       spamm_mat *Zout, const spamm_ns_opts *opts)
 {
@@ -657,7 +942,23 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
     const double f = std::sqrt(c * (1.0 + mu));
     bool unscaled = false;   // Y, Z already hold the outputs (final unscale fused)
     bool x_ready = false;    // ctx->cw[0] holds the coming step's X cull (chained fetch)
-    for (int k = 0; k < iters && !st; k++) {
+    bool borrowed = false;   // Y, Z are the graph's buffers (not freed here)
+    int k0 = 0;
+    if (!st && ns_graph_eligible(ctx, s, o, iters)) {
+        spamm_mat Yk = nullptr, Zk = nullptr;
+        bool ok = false;
+        st = ns_graph_run(ctx, Y, Z, tau, tau_s, iters - 1, o, &Yk, &Zk, &ok);
+        if (!st && ok) {
+            spamm_mat_free(Y);
+            spamm_mat_free(Z);
+            Y = Yk;
+            Z = Zk;
+            borrowed = true;
+            k0 = iters - 1;
+            if (o.iters_done) *o.iters_done = k0;
+        }
+    }
+    for (int k = k0; k < iters && !st; k++) {
         spamm_mat Yn = nullptr, Zn = nullptr;
         double t = 0.0;
         spamm_stats sts[3];
@@ -673,8 +974,11 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
             spamm_mat_free(Zn);
             break;
         }
-        spamm_mat_free(Y);
-        spamm_mat_free(Z);
+        if (!borrowed) {
+            spamm_mat_free(Y);
+            spamm_mat_free(Z);
+        }
+        borrowed = false;
         Y = Yn;
         Z = Zn;
         unscaled = fs.applied;
@@ -684,7 +988,19 @@ extern "C" spamm_status spamm_ns_sqrt(spamm_ctx ctx, spamm_mat s, double tau, in
     prof_end(ctx, pl);
     std::string err = ctx->err;
     spamm_status st2 = SPAMM_OK;
-    if (Y && Z && unscaled) {
+    if (Y && Z && borrowed) {
+        // a failure right after the graph steps: hand out copies, the buffers stay cached
+        spamm_mat Yf = nullptr, Zf = nullptr;
+        st2 = mat_map(ctx, Y, 2, f, 0.0, &Yf);
+        if (!st2) st2 = mat_map(ctx, Z, 0, f, 0.0, &Zf);
+        if (!st2) {
+            *Yout = Yf;
+            *Zout = Zf;
+        } else {
+            spamm_mat_free(Yf);
+            spamm_mat_free(Zf);
+        }
+    } else if (Y && Z && unscaled) {
         *Yout = Y;
         *Zout = Z;
     } else if (Y && Z) {

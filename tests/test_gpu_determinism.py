@@ -147,3 +147,39 @@ def test_ab_switches_bitwise():
             assert p.returncode == 0, p.stderr[-2000:]
             seen[(conc, pdl)] = [l for l in p.stdout.splitlines() if l.startswith("hash")][-1]
     assert len(set(seen.values())) == 1, seen
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "gauss4096"])
+def test_graph_replay_equals_host_driven(case):
+    """Small runs replay a captured, device-driven dual step (SPAMM_GRAPH=1, the default
+    when the worst-case workspace fits): same kernels and orders as the host-driven loop
+    (SPAMM_GRAPH=0), so t_k, every product's counts and Y, Z are bitwise equal.  A second
+    run on the same context replays the cached graphs and must agree too."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    setup = {
+        "C1": "c = si.CONFIGS['C1']; S = sp.spamm_build_tree(ctx, si.kms(c.n, c.rho), c.b); tau, it = c.tau, c.iters\n",
+        "C2": "c = si.CONFIGS['C2']; S = sp.spamm_build_tree(ctx, si.kms(c.n, c.rho), c.b); tau, it = c.tau, c.iters\n",
+        "gauss4096": ("c = si.Config('t', 'gauss', 4096, 64, 1e-7, 30, sigma=0.8, shift=1e-3, seed=150805856, "
+                      "tau_min=1e-7); S = sp.spamm_build_tree_blocks(ctx, 4096, 64, *si.make_input(c)[1]); "
+                      "tau, it = 1e-7, 20\n"),
+    }[case]
+    code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_1508_05856_b200 as sp, spamm_inputs as si\n"
+            "ctx = sp.spamm_ctx_create(0)\n" + setup +
+            "for rep in range(2):\n"
+            "    r = sp.spamm_ns_sqrt(ctx, S, tau, it)\n"
+            "    h = hashlib.sha1(r['t'].tobytes() + repr([[p['tasks'], p['segments'], p['level_survivors']]"
+            " for k in r['stats'] for p in k]).encode())\n"
+            "    for M in (r['Y'], r['Z']):\n"
+            "        bi, bj, blk = sp.spamm_export_blocks(ctx, M); o = np.lexsort((bj, bi))\n"
+            "        h.update(bi[o].tobytes() + bj[o].tobytes() + blk[o].tobytes())\n"
+            "    print('hash', r['iters'], h.hexdigest())\n") % ROOT
+    out = {}
+    for gm in ("0", "1"):
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900,
+                           env={**os.environ, "SPAMM_GRAPH": gm})
+        assert p.returncode == 0, p.stderr[-3000:]
+        out[gm] = [l for l in p.stdout.splitlines() if l.startswith("hash")]
+        assert len(out[gm]) == 2 and out[gm][0] == out[gm][1], out[gm]
+    assert out["0"][0] == out["1"][0], out

@@ -456,3 +456,31 @@ def test_power_scale_sym_and_full_paths_bitwise(ctx):
         assert p.returncode == 0, p.stderr[-2000:]
         out.append(p.stdout.strip().splitlines()[-1])
     assert out[0] == out[1], out
+
+
+def test_volume_sink_whole_run_matches_oracle(ctx):
+    """§8(f) f4: the per-product recorder sees every product of an NS run (X, Y', Z' per
+    k).  On C2 (30 iterations) each product's ijk task set equals the oracle's (same
+    Y0, Z0, c; the oracle's own free run), its distance histogram equals the one counted
+    from the oracle's triples, and the recorded counts equal spamm_ns_sqrt's stats."""
+    c = si.CONFIGS["C2"]
+    kind, payload = si.make_input(c)
+    S, So = build_pair(ctx, kind, payload, c.b, c.n)
+    cs = O.power_scale(So)
+    nb = c.n // c.b
+    sink = sp().VolumeSink(3 * c.iters, nbins=nb, ikj_cap=400000)
+    sp().spamm_ctx_set_volume_sink(ctx, sink)
+    try:
+        r = sp().spamm_ns_sqrt(ctx, S, c.tau, c.iters, scale=cs)
+    finally:
+        sp().spamm_ctx_set_volume_sink(ctx, None)
+    assert sink.nprod == 3 * c.iters and sink.complete()
+    assert list(sink.ntasks) == [p["tasks"] for k in r["stats"] for p in k]
+    Y, Z = O.ns_y0(So, cs), O.OMat.identity(c.n, c.b)
+    for k in range(c.iters):
+        Y, Z, _, _, _, tasks = O.ns_step(Y, Z, c.tau, want_tasks=True)
+        for q in range(3):
+            g = sink.tasks(3 * k + q)
+            assert P.triples(g) == P.triples(tasks[q]), (k, q)
+            d = np.max(np.abs(np.stack([g[:, 0] - g[:, 2], g[:, 0] - g[:, 1], g[:, 2] - g[:, 1]])), axis=0)
+            assert np.array_equal(sink.hist[3 * k + q], np.bincount(np.minimum(d, nb - 1), minlength=nb))
