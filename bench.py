@@ -138,19 +138,41 @@ def workload_name(cfg, tau, iters):
             f"{iters} dual NS iterations")
 
 
+def cpu_model():
+    """lscpu model name / sockets / cores of this host (SURVEY.md §8(d) oracle timing)."""
+    info = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            info[k.strip()] = v.strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"model": info.get("Model name"), "sockets": info.get("Socket(s)"),
+            "cores_per_socket": info.get("Core(s) per socket"), "threads": os.cpu_count()}
+
+
 def oracle_sample(cfg, payload, tau, iters, scale, tau_s=None):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload:
-    build + Y0 (given scale) + `iters` NS iterations.  Returns (seconds, flops)."""
+    build + Y0 (given scale) + `iters` NS iterations, each NS iteration timed on its
+    own.  Returns (seconds, flops, threads, per_k_seconds, build_seconds)."""
     import oracle as O
     t0 = time.perf_counter()
     if cfg.kind == "kms":
         So = O.OMat.from_dense(payload, cfg.b)
     else:
         So = O.OMat.from_blocks(cfg.n, cfg.b, *payload)
-    r = O.ns_sqrt(So, tau, iters, tau_s=tau_s, scale=scale, mu=cfg.mu)
+    Y, Z = O.ns_y0(So, scale, cfg.mu), O.OMat.identity(cfg.n, cfg.b)
+    del So
+    t1 = time.perf_counter()
+    flops, per_k = 0.0, []
+    for _ in range(iters):
+        tk = time.perf_counter()
+        Y, Z, _, _, counts = O.ns_step(Y, Z, tau, tau_s, allow_nonfinite=True)
+        per_k.append(time.perf_counter() - tk)
+        flops += float(counts.sum()) * 2.0 * cfg.b ** 3
     dt = time.perf_counter() - t0
-    flops = float(r["counts"].sum()) * 2.0 * cfg.b ** 3
-    return dt, flops, O.num_threads()
+    return dt, flops, O.num_threads(), per_k, t1 - t0
 
 
 def run_config(args, cfg, ws, in_bytes):
@@ -196,11 +218,13 @@ def run_reference(args):
     del So
     for _ in range(args.warmup):
         oracle_sample(cfg, payload, tau, args.ref_iters, c, tau * cfg.tau_s_factor)
-    tot_t, tot_f, cores = 0.0, 0.0, 1
+    tot_t, tot_f, cores, per_k, build_s = 0.0, 0.0, 1, [], []
     for _ in range(args.steps):
-        dt, fl, cores = oracle_sample(cfg, payload, tau, args.ref_iters, c, tau * cfg.tau_s_factor)
+        dt, fl, cores, pk, bs = oracle_sample(cfg, payload, tau, args.ref_iters, c, tau * cfg.tau_s_factor)
         tot_t += dt
         tot_f += fl
+        per_k.append(pk)
+        build_s.append(bs)
     value = tot_f / tot_t / 1e12
     sample = (f"{args.config} input, oracle quadtree build + Y0 + the first {args.ref_iters} of "
               f"{iters} NS iterations per step (c given)")
@@ -209,7 +233,9 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu": cpu_model(), "s_per_k": [statistics.mean(x) for x in zip(*per_k)],
+                         "build_s": statistics.mean(build_s)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -394,79 +420,42 @@ def run_ours(args):
         except (OSError, ValueError):
             pass
 
-    # ---- e2e through the C ABI with HOST buffers: every step copies its input from
-    # pinned host memory (H2D) and its result Y, Z back to pinned host memory (D2H).
-    # The copies run on two copy streams, pipelined with the neighbouring steps' compute
-    # (double-buffered result buffers), as a serving pipeline would; all of them are
-    # inside the timed region.
+    # ---- e2e through the C ABI with HOST buffers: every step passes its input as pinned
+    # HOST pointers to spamm_build_tree[_blocks] (the library stages it to the device on
+    # its stream: H2D inside the step) and reads Y and Z back into pinned HOST buffers with
+    # spamm_export_blocks_async (the library's copy stream: each step's D2H overlaps the
+    # next step's compute); spamm_copies_join puts the last copies inside the timed region.
     e2e = None
     if not args.no_e2e:
-        h2d, copy = torch.cuda.Stream(dev), torch.cuda.Stream(dev)   # separate copy engines / queues
-        dbuf, hbuf, done = [{}, {}], [{}, {}], [None, None]
+        hout = [{}, {}]
 
-        def bufs(i, key, nblk):
-            d = dbuf[i].get(key)
-            if d is None or d[0].shape[0] < nblk:
+        def hbufs(i, key, nblk):
+            h = hout[i].get(key)
+            if h is None or h[0].shape[0] < nblk:
                 cap = int(nblk * 1.25) + 16
-                dbuf[i][key] = (torch.empty(cap, dtype=torch.int32, device=dev),
-                                torch.empty(cap, dtype=torch.int32, device=dev),
-                                torch.empty((cap, cfg.b, cfg.b), dtype=torch.float64, device=dev))
-                hbuf[i][key] = (torch.empty(cap, dtype=torch.int32).pin_memory(),
-                                torch.empty(cap, dtype=torch.int32).pin_memory(),
-                                torch.empty((cap, cfg.b, cfg.b), dtype=torch.float64).pin_memory())
-            return dbuf[i][key], hbuf[i][key]
+                h = hout[i][key] = (torch.empty(cap, dtype=torch.int32).pin_memory(),
+                                    torch.empty(cap, dtype=torch.int32).pin_memory(),
+                                    torch.empty((cap, cfg.b, cfg.b), dtype=torch.float64).pin_memory())
+            return h
 
-        # device input buffers, double-buffered: step i+1's H2D is issued as soon as
-        # step i's build has consumed its own buffer (prefetch under step i's compute)
-        din = [tuple(torch.empty_like(h, device=dev) for h in h_in) for _ in range(2)]
-        in_done, in_free = [None, None], [None, None]
-
-        def issue_h2d(slot):
-            with torch.cuda.stream(h2d):
-                if in_free[slot] is not None:
-                    h2d.wait_event(in_free[slot])
-                for dt_, ht_ in zip(din[slot], h_in):
-                    dt_.copy_(ht_, non_blocking=True)
-                in_done[slot] = h2d.record_event()
-
-        def e2e_step(i, last):
-            slot = i % 2
-            if in_done[slot] is None:
-                issue_h2d(slot)
-            stream.wait_event(in_done[slot])
-            in_done[slot] = None
-            S = build(din[slot])
-            in_free[slot] = stream.record_event()
-            if not last:
-                issue_h2d(1 - slot)
+        def e2e_step(i):
+            S = build(h_in)                           # host pointers: the library's H2D
             if args.channel == "single":
                 r = sp.spamm_ns_sqrt_single(ctx, S, tau, iters, tau_s=tau_s, t_stop=t_stop, scaled=scaled)
             else:
                 r = sp.spamm_ns_sqrt(ctx, S, tau, iters, tau_s=tau_s, mu=cfg.mu, t_stop=t_stop, scaled=scaled)
             S.free()
-            if done[slot] is not None:
-                stream.wait_event(done[slot])        # that slot's previous D2H has finished
             nbytes = 0
-            pairs = []
             for key in ("Y", "Z"):
-                nblk = r[key].nblocks
-                db, hb = bufs(slot, key, nblk)
-                sp.spamm_export_blocks(ctx, r[key], db)
-                pairs.append((db, hb, nblk))
+                nblk = sp.spamm_export_blocks_async(ctx, r[key], hbufs(i % 2, key, r[key].nblocks))
                 nbytes += nblk * (8 + 8 * cfg.b * cfg.b)
-            r["Y"].free()
-            r["Z"].free()
-            copy.wait_stream(stream)
-            with torch.cuda.stream(copy):
-                for db, hb, nblk in pairs:
-                    for dt_, ht_ in zip(db, hb):
-                        ht_[:nblk].copy_(dt_[:nblk], non_blocking=True)
-            done[slot] = copy.record_event()
+                r[key].free()
             flops = sum(p["flops"] for k in r["stats"] for p in k)
             return flops, nbytes
 
         for i in range(2):                            # allocate the buffers (untimed)
-            e2e_step(i, last=i == 1)
+            e2e_step(i)
+        sp.spamm_copies_wait(ctx)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
@@ -476,9 +465,9 @@ def run_ours(args):
         ef = 0.0
         d2h = 0
         for i in range(args.steps):
-            f, d2h = e2e_step(i, last=i == args.steps - 1)
+            f, d2h = e2e_step(i)
             ef += f
-        stream.wait_stream(copy)
+        sp.spamm_copies_join(ctx)
         e3.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -487,8 +476,33 @@ def run_ours(args):
                "h2d_bytes_per_step": int(D.sum_over_ranks(in_bytes, dev)),
                "d2h_bytes_per_step": int(D.sum_over_ranks(d2h, dev)),
                "ms_per_step": ems / args.steps,
-               "pipelining": "H2D (prefetched one step ahead) / D2H on copy streams, overlapped with "
-                             "the neighbouring steps' compute; every byte of both inside the timed region"}
+               "path": "C ABI host pointers: spamm_build_tree_blocks(pinned host input; the library's "
+                       "H2D on its stream) + spamm_export_blocks_async(pinned host output; D2H on the "
+                       "library's copy stream, overlapping the next step) + spamm_copies_join"}
+
+    # ---- seconds per NS iteration k (BJ:2), from one extra untimed run driven step by
+    # step (spamm_ns_step, CUDA events on the library stream around each k)
+    per_k = None
+    if args.channel == "dual" and not scaled:
+        S = build(d_in)
+        c = sp.spamm_power_scale(ctx, S, 100)
+        Y, Z = sp.spamm_ns_y0(ctx, S, c, cfg.mu), sp.spamm_identity(ctx, cfg.n, cfg.b)
+        S.free()
+        per_k = []
+        for _ in range(iters):
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0.record(stream)
+            Yn, Zn, t, _ = sp.spamm_ns_step(ctx, Y, Z, tau, tau_s)
+            k1.record(stream)
+            k1.synchronize()
+            per_k.append(k0.elapsed_time(k1) / 1e3)
+            Y.free()
+            Z.free()
+            Y, Z = Yn, Zn
+            if t_stop > 0 and abs(t) <= t_stop:
+                break
+        Y.free()
+        Z.free()
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
@@ -496,10 +510,11 @@ def run_ours(args):
         S = build(d_in)
         c = sp.spamm_power_scale(ctx, S, 100)
         S.free()
-        dt, fl, cores = oracle_sample(cfg, payload, tau, args.ref_iters, c, tau_s)
+        dt, fl, cores, per_k, build_s = oracle_sample(cfg, payload, tau, args.ref_iters, c, tau_s)
         cpu = {"value": fl / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{args.config} input: oracle quadtree build + Y0 + first {args.ref_iters} "
-                         f"of {iters} NS iterations ({fl:.3g} culled-leaf flop in {dt:.1f} s)"}
+                         f"of {iters} NS iterations ({fl:.3g} culled-leaf flop in {dt:.1f} s)",
+               "cpu": cpu_model(), "s_per_k": per_k, "build_s": build_s}
 
     blocks_mb = D.sum_over_ranks(in_bytes, dev) / 1e6
     if rank == 0:
@@ -511,6 +526,9 @@ def run_ours(args):
             "config": run_config(args, cfg, ws, blocks_mb * 1e6),
             "iters_run": int(r["iters"]),
             "s_per_ns_iteration": prof["loop_ms"] / args.steps / max(int(r["iters"]), 1) / 1e3,
+            "s_per_k": per_k,
+            "s_per_k_source": "one extra untimed run driven by spamm_ns_step (host-driven, no graph/"
+                              "chaining), CUDA events around each k",
             "setup_ms_per_step": prof["setup_ms"] / args.steps,
             "tasks_per_step": tasks_all / args.steps,
             "t_final": float(r["t"][-1]) if len(r["t"]) else None,

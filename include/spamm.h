@@ -306,6 +306,18 @@ spamm_status spamm_scale(spamm_ctx ctx, spamm_mat m, double alpha, int32_t divid
  * *n = number of stored blocks (pool order).  Pass cap = 0 to query *n. */
 spamm_status spamm_export_blocks(spamm_ctx ctx, spamm_mat m, int32_t *bi, int32_t *bj,
                                  double *blocks, int64_t cap, int64_t *n);
+/* Asynchronous spamm_export_blocks to HOST buffers (pinned for real overlap): the
+ * row-major staging runs on the context stream into a library-owned device slot
+ * (SPAMM_XSLOTS = 4 of them, reused round-robin, each grown on demand), the
+ * device->host copy on the context's own copy stream, so it overlaps whatever the
+ * context stream runs next.  m may be freed right after the call.  The host buffers
+ * are complete after spamm_copies_wait (host) or, in stream order, after
+ * spamm_copies_join (the context stream waits for every export issued so far).
+ * Errors: EINVAL (device output pointers, NULL), ENOMEM (staging). */
+spamm_status spamm_export_blocks_async(spamm_ctx ctx, spamm_mat m, int32_t *bi, int32_t *bj,
+                                       double *blocks, int64_t cap, int64_t *n);
+spamm_status spamm_copies_join(spamm_ctx ctx);
+spamm_status spamm_copies_wait(spamm_ctx ctx);
 
 /* ------------------------------------------------- measurement utilities */
 /* Device-side phase timing with CUDA events on the context stream (bench.py

@@ -32,6 +32,7 @@ __all__ = [
     "Comm", "spamm_comm_nccl_unique_id", "spamm_comm_nccl_create", "spamm_comm_local_group",
     "spamm_comm_destroy", "spamm_ctx_set_comm", "spamm_mat_rows", "spamm_row_task_counts",
     "VolumeSink", "spamm_ctx_set_volume_sink",
+    "spamm_export_blocks_async", "spamm_copies_join", "spamm_copies_wait",
 ]
 
 STATUS = {0: "SPAMM_OK", 1: "SPAMM_EINVAL", 2: "SPAMM_ESHAPE", 3: "SPAMM_ENOMEM",
@@ -139,6 +140,9 @@ def load():
         "spamm_mat_rows": (i32, [vp, P(i32), P(i32)]),
         "spamm_row_task_counts": (i32, [vp, vp, vp, dbl, vp]),
         "spamm_ctx_set_volume_sink": (i32, [vp, vp]),
+        "spamm_export_blocks_async": (i32, [vp, vp, vp, vp, vp, i64, P(i64)]),
+        "spamm_copies_join": (i32, [vp]),
+        "spamm_copies_wait": (i32, [vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -599,6 +603,25 @@ def spamm_export_blocks(ctx: Ctx, m: Mat, out=None):
                                          C.byref(n)))
     ctx.sync_out()
     return bi[:k], bj[:k], blocks[:k]
+
+
+def spamm_export_blocks_async(ctx: Ctx, m: Mat, out):
+    """Asynchronous export into preallocated HOST buffers out = (bi, bj, blocks) (pinned
+    torch tensors or numpy arrays); valid after spamm_copies_wait / spamm_copies_join.
+    Returns the number of blocks."""
+    bi, bj, blocks = out
+    n = C.c_int64()
+    ctx.check(load().spamm_export_blocks_async(ctx.h, m.h, _ptr(bi), _ptr(bj), _ptr(blocks), len(bi),
+                                               C.byref(n)))
+    return n.value
+
+
+def spamm_copies_join(ctx: Ctx):
+    ctx.check(load().spamm_copies_join(ctx.h))
+
+
+def spamm_copies_wait(ctx: Ctx):
+    ctx.check(load().spamm_copies_wait(ctx.h))
 
 
 def spamm_profile_enable(ctx: Ctx, enable: bool = True):

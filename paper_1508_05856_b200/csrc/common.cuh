@@ -79,6 +79,7 @@ struct spamm_ctx_s {
     // comes from the context's pool / allocator)
     spamm_volume_sink *vsink = nullptr;   // per-product recorder (f4), nullable
     struct NsGraph *nsg = nullptr;        // cached graph-replayed NS step (spamm.cu)
+    void *xs = nullptr;                   // asynchronous export: copy stream + staging (prof.cu)
     bool capturing = false;               // inside a CUDA graph capture (no prof events)
     std::atomic<int64_t> live_mats{0};
     std::atomic<bool> destroy_pending{false};
@@ -372,6 +373,8 @@ int prof_begin(spamm_ctx ctx, int phase);
 void prof_end(spamm_ctx ctx, int idx);
 void prof_gemm_work(spamm_ctx ctx, int64_t tasks, int64_t segs, int b);
 void prof_destroy(spamm_ctx ctx);
+#define SPAMM_XSLOTS 4
+void xstate_free(spamm_ctx ctx);   // the asynchronous-export state (copies drained first)
 
 // power.cu
 spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host);

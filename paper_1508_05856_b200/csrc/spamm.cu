@@ -91,6 +91,7 @@ extern "C" void spamm_ctx_destroy(spamm_ctx ctx)
 void ctx_teardown(spamm_ctx ctx)
 {
     cudaStreamSynchronize(ctx->stream);
+    xstate_free(ctx);
     dist_free(ctx);
     for (int i = 0; i < 3; i++) {
         if (!ctx->cw[i]) continue;
