@@ -319,6 +319,23 @@ spamm_status spamm_export_blocks_async(spamm_ctx ctx, spamm_mat m, int32_t *bi, 
 spamm_status spamm_copies_join(spamm_ctx ctx);
 spamm_status spamm_copies_wait(spamm_ctx ctx);
 
+/* Asynchronous upload of a block-list input from HOST memory (pinned for overlap),
+ * the prefetch half of spamm_build_tree_blocks: the host->device copy is issued at
+ * once on the library's upload stream, into one of SPAMM_ISLOTS = 2 context-owned
+ * staging slots (round-robin; a slot is refilled only after the build that read it),
+ * with NO ordering against the context stream, so it overlaps whatever the context is
+ * computing.  spamm_build_tree_staged(ctx, n, staged, &m) then builds the quadtree
+ * on the context stream once the copy has landed (same result as
+ * spamm_build_tree_blocks on the same arrays) and consumes the handle; the host
+ * arrays must stay unchanged until then.  At most SPAMM_ISLOTS uploads may be
+ * outstanding (an older handle is rejected with EINVAL).  spamm_staged_free drops an
+ * unused handle.  Errors: EINVAL (device pointers, b), ENOMEM (staging). */
+typedef struct spamm_staged_s *spamm_staged;
+spamm_status spamm_stage_blocks(spamm_ctx ctx, int64_t nblocks, int32_t b, const int32_t *bi,
+                                const int32_t *bj, const double *blocks, spamm_staged *out);
+spamm_status spamm_build_tree_staged(spamm_ctx ctx, int64_t n, spamm_staged staged, spamm_mat *out);
+void spamm_staged_free(spamm_staged staged);
+
 /* ------------------------------------------------- measurement utilities */
 /* Device-side phase timing with CUDA events on the context stream (bench.py
  * uses it for the roofline of the dominant kernel).  Phases: */

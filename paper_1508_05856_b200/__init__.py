@@ -33,6 +33,7 @@ __all__ = [
     "spamm_comm_destroy", "spamm_ctx_set_comm", "spamm_mat_rows", "spamm_row_task_counts",
     "VolumeSink", "spamm_ctx_set_volume_sink",
     "spamm_export_blocks_async", "spamm_copies_join", "spamm_copies_wait",
+    "spamm_stage_blocks", "spamm_build_tree_staged", "spamm_staged_free",
 ]
 
 STATUS = {0: "SPAMM_OK", 1: "SPAMM_EINVAL", 2: "SPAMM_ESHAPE", 3: "SPAMM_ENOMEM",
@@ -143,6 +144,9 @@ def load():
         "spamm_export_blocks_async": (i32, [vp, vp, vp, vp, vp, i64, P(i64)]),
         "spamm_copies_join": (i32, [vp]),
         "spamm_copies_wait": (i32, [vp]),
+        "spamm_stage_blocks": (i32, [vp, i64, i32, vp, vp, vp, P(vp)]),
+        "spamm_build_tree_staged": (i32, [vp, i64, vp, P(vp)]),
+        "spamm_staged_free": (None, [vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -616,6 +620,33 @@ def spamm_export_blocks_async(ctx: Ctx, m: Mat, out):
     return n.value
 
 
+class Staged:
+    """Handle of an upload in flight (spamm_stage_blocks); keeps the host arrays alive."""
+
+    def __init__(self, ctx, h, keep):
+        self.ctx, self.h, self.keep = ctx, h, keep
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load().spamm_staged_free(self.h)
+            self.h = None
+
+
+def spamm_stage_blocks(ctx: Ctx, b: int, bi, bj, blocks) -> Staged:
+    """Start the upload of a HOST block list (pinned torch tensors or numpy arrays)."""
+    h = C.c_void_p()
+    ctx.check(load().spamm_stage_blocks(ctx.h, len(bi), b, _ptr(bi), _ptr(bj), _ptr(blocks), C.byref(h)))
+    return Staged(ctx, h, (bi, bj, blocks))
+
+
+def spamm_build_tree_staged(ctx: Ctx, n: int, staged: Staged) -> Mat:
+    """Build from a staged upload (consumes the handle)."""
+    h = C.c_void_p()
+    sh, staged.h = staged.h, None
+    ctx.check(load().spamm_build_tree_staged(ctx.h, n, sh, C.byref(h)))
+    return Mat(ctx, h)
+
+
 def spamm_copies_join(ctx: Ctx):
     ctx.check(load().spamm_copies_join(ctx.h))
 
@@ -685,3 +716,10 @@ def spamm_ctx_set_volume_sink(ctx: Ctx, sink: VolumeSink | None):
     """Attach (or detach with None) a per-product volume recorder to ctx."""
     ctx.check(load().spamm_ctx_set_volume_sink(ctx.h, C.byref(sink.s) if sink is not None else None))
     ctx._vsink = sink   # the library holds raw pointers into it
+
+
+def spamm_staged_free(staged: Staged):
+    """Drop an upload handle that will not be built."""
+    if getattr(staged, "h", None):
+        load().spamm_staged_free(staged.h)
+        staged.h = None

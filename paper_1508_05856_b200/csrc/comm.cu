@@ -28,6 +28,7 @@ struct NcclApi {
     std::string why;
     ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitRankConfig)(ncclComm_t *, int, ncclUniqueId, int, ncclConfig_t *) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -66,6 +67,7 @@ NcclApi *nccl_api()
               sym(h, "ncclSend", a.Send) && sym(h, "ncclRecv", a.Recv) &&
               sym(h, "ncclGroupStart", a.GroupStart) && sym(h, "ncclGroupEnd", a.GroupEnd) &&
               sym(h, "ncclGetErrorString", a.GetErrorString);
+    sym(h, "ncclCommInitRankConfig", a.CommInitRankConfig);   // optional
     if (!ok) {
         a.why = "libnccl.so.2 lacks a required symbol";
         return nullptr;
@@ -251,7 +253,19 @@ extern "C" spamm_status spamm_comm_nccl_create(const void *id128, int32_t rank, 
     c->api = api;
     c->rank = rank;
     c->world = world;
-    if (api->CommInitRank(&c->comm, world, id, rank) != ncclSuccess) {
+    // The halo exchange runs while the local-segment GEMM holds the SMs (spamm.cu
+    // overlapped_gemm leaves exchange_ctas() SMs free): cap NCCL's CTAs to that many so
+    // its kernels fit the reserved SMs instead of waiting for the GEMM to drain.
+    ncclResult_t ir;
+    if (api->CommInitRankConfig) {
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.maxCTAs = exchange_ctas();
+        cfg.minCTAs = 1;
+        ir = api->CommInitRankConfig(&c->comm, world, id, rank, &cfg);
+    } else {
+        ir = api->CommInitRank(&c->comm, world, id, rank);
+    }
+    if (ir != ncclSuccess) {
         c->comm = nullptr;
         delete c;
         return SPAMM_ENCCL;

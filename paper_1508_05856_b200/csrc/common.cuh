@@ -81,6 +81,7 @@ struct spamm_ctx_s {
     struct NsGraph *nsg = nullptr;        // cached graph-replayed NS step (spamm.cu)
     void *xs = nullptr;                   // asynchronous export: copy stream + staging (prof.cu)
     bool capturing = false;               // inside a CUDA graph capture (no prof events)
+    int gemm_grid_cap = 0;                // > 0: at most this many leaf-GEMM CTAs (overlap window)
     std::atomic<int64_t> live_mats{0};
     std::atomic<bool> destroy_pending{false};
 };
@@ -262,6 +263,19 @@ spamm_status check_cuda(spamm_ctx ctx, cudaError_t e, const char *what);
 
 static inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// SMs left to the halo exchange while the local-segment GEMM runs (row partition,
+// world > 1); NCCL communicators are created with maxCTAs = this (SPAMM_EXCHANGE_CTAS,
+// default 8)
+static inline int exchange_ctas()
+{
+    static const int v = [] {
+        const char *e = getenv("SPAMM_EXCHANGE_CTAS");
+        const int x = e && *e ? atoi(e) : 8;
+        return x < 1 ? 1 : x > 64 ? 64 : x;
+    }();
+    return v;
+}
+
 // Per-device, thread-safe one-time kernel configuration (function attributes are
 // per device; contexts may be driven from several host threads).  f() is
 // idempotent, so two threads racing on the first call both running it is harmless.
@@ -374,7 +388,8 @@ void prof_end(spamm_ctx ctx, int idx);
 void prof_gemm_work(spamm_ctx ctx, int64_t tasks, int64_t segs, int b);
 void prof_destroy(spamm_ctx ctx);
 #define SPAMM_XSLOTS 4
-void xstate_free(spamm_ctx ctx);   // the asynchronous-export state (copies drained first)
+#define SPAMM_ISLOTS 2
+void xstate_free(spamm_ctx ctx);   // the asynchronous host-I/O state (hostio.cu; copies drained first)
 
 // power.cu
 spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host);

@@ -396,6 +396,7 @@ static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
     const int occ = occ_cache.load();
     int grid = ctx->sm_count * occ;
     if (!g.nseg_dev && grid > g.nseg) grid = g.nseg;
+    if (ctx->gemm_grid_cap > 0 && grid > ctx->gemm_grid_cap) grid = ctx->gemm_grid_cap;
     kern<<<grid, NT, smem, ctx->stream>>>(g);
     CKL(ctx);
     return SPAMM_OK;

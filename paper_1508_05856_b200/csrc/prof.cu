@@ -200,107 +200,3 @@ extern "C" spamm_status spamm_export_blocks(spamm_ctx ctx, spamm_mat m, int32_t 
     return SPAMM_OK;
 }
 
-// ------------------------------------------------------- asynchronous export
-// Staging slots owned by the context: the un-swizzle runs on the context stream into
-// slot q, the device->host copy on the context's copy stream (a separate copy engine
-// queue) after an event, so it overlaps the context stream's next work.  A slot is
-// reused only after its previous copy's event (the context stream waits on it).
-struct XSlot {
-    void *dev = nullptr;
-    size_t bytes = 0;
-    cudaEvent_t done = nullptr;
-};
-struct XState {
-    cudaStream_t copy = nullptr;
-    cudaEvent_t ready = nullptr, last = nullptr;
-    XSlot slot[SPAMM_XSLOTS];
-    int next = 0;
-};
-
-static spamm_status xstate(spamm_ctx ctx, XState **out)
-{
-    if (!ctx->xs) {
-        XState *x = new XState();
-        ctx->xs = x;
-        CK(cudaStreamCreateWithFlags(&x->copy, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&x->ready, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&x->last, cudaEventDisableTiming));
-        for (auto &q : x->slot) CK(cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming));
-    }
-    *out = (XState *)ctx->xs;
-    return SPAMM_OK;
-}
-
-void xstate_free(spamm_ctx ctx)
-{
-    XState *x = (XState *)ctx->xs;
-    if (!x) return;
-    if (x->copy) cudaStreamSynchronize(x->copy);
-    for (auto &q : x->slot) {
-        dev_free(ctx, q.dev, q.bytes);
-        if (q.done) cudaEventDestroy(q.done);
-    }
-    if (x->ready) cudaEventDestroy(x->ready);
-    if (x->last) cudaEventDestroy(x->last);
-    if (x->copy) cudaStreamDestroy(x->copy);
-    delete x;
-    ctx->xs = nullptr;
-}
-
-extern "C" spamm_status spamm_export_blocks_async(spamm_ctx ctx, spamm_mat m, int32_t *bi, int32_t *bj,
-                                                  double *blocks, int64_t cap, int64_t *n)
-{
-    if (!ctx || !m || !n) return set_err(ctx, SPAMM_EINVAL, "bad argument");
-    *n = m->nblk;
-    const int64_t k = m->nblk < cap ? m->nblk : cap;
-    if (k <= 0) return SPAMM_OK;
-    if (!bi || !bj || !blocks) return set_err(ctx, SPAMM_EINVAL, "NULL output");
-    if (is_device_ptr(bi) || is_device_ptr(bj) || is_device_ptr(blocks))
-        return set_err(ctx, SPAMM_EINVAL, "spamm_export_blocks_async writes host buffers");
-    XState *x = nullptr;
-    ST(xstate(ctx, &x));
-    XSlot &q = x->slot[x->next];
-    x->next = (x->next + 1) % SPAMM_XSLOTS;
-    const int64_t b2 = (int64_t)m->b * m->b;
-    const size_t need = sizeof(double) * k * b2 + 2 * sizeof(int32_t) * k + 512;
-    CK(cudaStreamWaitEvent(ctx->stream, q.done, 0));   // the slot's previous copy is over
-    if (q.bytes < need) {
-        dev_free(ctx, q.dev, q.bytes);
-        q.bytes = need + need / 4;
-        q.dev = dev_alloc(ctx, q.bytes);
-        if (!q.dev) {
-            q.bytes = 0;
-            return set_err(ctx, SPAMM_ENOMEM, "export staging (%lld blocks)", (long long)k);
-        }
-    }
-    double *dbl = (double *)q.dev;
-    int32_t *dbi = (int32_t *)(dbl + k * b2), *dbj = dbi + k;
-    k_coords_out<<<cdiv(k, 256), 256, 0, ctx->stream>>>(m->coord, k, dbi, dbj);
-    CKL(ctx);
-    k_unswizzle<<<(int)k, 256, 0, ctx->stream>>>(m->pool, m->b, dbl);
-    CKL(ctx);
-    CK(cudaEventRecord(x->ready, ctx->stream));
-    CK(cudaStreamWaitEvent(x->copy, x->ready, 0));
-    CK(cudaMemcpyAsync(blocks, dbl, sizeof(double) * k * b2, cudaMemcpyDeviceToHost, x->copy));
-    CK(cudaMemcpyAsync(bi, dbi, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, x->copy));
-    CK(cudaMemcpyAsync(bj, dbj, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, x->copy));
-    CK(cudaEventRecord(q.done, x->copy));
-    CK(cudaEventRecord(x->last, x->copy));
-    return SPAMM_OK;
-}
-
-extern "C" spamm_status spamm_copies_join(spamm_ctx ctx)
-{
-    if (!ctx) return SPAMM_EINVAL;
-    if (!ctx->xs) return SPAMM_OK;
-    CK(cudaStreamWaitEvent(ctx->stream, ((XState *)ctx->xs)->last, 0));
-    return SPAMM_OK;
-}
-
-extern "C" spamm_status spamm_copies_wait(spamm_ctx ctx)
-{
-    if (!ctx) return SPAMM_EINVAL;
-    if (!ctx->xs) return SPAMM_OK;
-    CK(cudaEventSynchronize(((XState *)ctx->xs)->last));
-    return SPAMM_OK;
-}

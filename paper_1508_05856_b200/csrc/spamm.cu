@@ -7,6 +7,7 @@
 //       partials), diagonal fix-up, t_k; Y' = Y (x)_tau_s H; Z' = H (x)_tau Z
 //       (Eq. cannonical P:383-389 in the north_star form, reading L8)
 //   spamm_ns_sqrt  : setup (c, Y0 = s/c, Z0 = I) + iters steps + unscale.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -263,7 +264,11 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
         order = lpt;
     }
     int pg = prof_begin(ctx, SPAMM_PH_GEMM);
+    // the local segments leave exchange_ctas() SMs to the exchange's NCCL kernels (a
+    // persistent GEMM CTA fills an SM's shared memory and most of its registers)
+    ctx->gemm_grid_cap = std::max(1, ctx->sm_count - exchange_ctas());
     spamm_status st = gemm_run(ctx, cw, A, B, nullptr, m, epi, trace_part, order, nloc, 0);
+    ctx->gemm_grid_cap = 0;
     prof_end(ctx, pg);
     // halo exchange with every allocation, kernel and collective on the comm stream
     double *halo = nullptr;
@@ -902,7 +907,8 @@ static spamm_status ns_graph_run(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, double
         rec_stats(rec[k], L, b, st);
         if (o.t_history) o.t_history[k] = rec[k].t;
         if (o.per_product) memcpy(o.per_product + 3 * k, st, sizeof(st));
-        for (int p = 0; p < 3; p++) prof_gemm_work(ctx, st[p].tasks, st[p].segments, b);
+        // (no prof_gemm_work: the graph's GEMMs carry no phase events, so the GEMM
+        // roofline of a profiled run covers the host-driven products only)
     }
     const int q = steps & 1;
     g->Yb[q]->nblk = rec[steps - 1].cnt[1][CNT_NSEG];

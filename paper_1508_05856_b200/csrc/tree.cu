@@ -356,11 +356,14 @@ static spamm_status build_common(spamm_ctx ctx, BlockSrc src, int64_t count, int
     int ntiles = cdiv(count, 512);
     int32_t *flags = dalloc<int32_t>(ctx, ntiles + 1);
     V1 *agg = dalloc<V1>(ctx, ntiles), *pre = dalloc<V1>(ctx, ntiles);
-    if (!n2 || !slot_of || !flags || !agg || !pre) return set_err(ctx, SPAMM_ENOMEM, "build workspace");
     spamm_status st = SPAMM_OK;
     int64_t nblk = 0;
     spamm_mat m = nullptr;
     do {
+        if (!n2 || !slot_of || !flags || !agg || !pre) {
+            st = set_err(ctx, SPAMM_ENOMEM, "build workspace");
+            break;
+        }
         if (count > 0) {
             k_block_norm2<<<cdiv(count * 32, 256), 256, 0, ctx->stream>>>(src, count, n2);
             ctx->launches++;
