@@ -86,10 +86,9 @@ __global__ void k_cull_reset(int32_t *cnt, int ncnt, int32_t *flags, int64_t nfl
     for (int64_t i = i0; i < nflags; i += stride) flags[i] = 0;
 }
 
-__global__ void __launch_bounds__(1024) k_cull_init(CullArgs g, int l0, int4 *rec, int32_t *cnt)
+// the init level for a CTA of 1024 threads (k_cull_init and k_cull_small)
+__device__ __forceinline__ void cull_init_body(const CullArgs &g, int l0, int4 *rec, int32_t *cnt)
 {
-    pdl_wait();
-    pdl_trigger();
     __shared__ int sw[32];
     __shared__ int gpre[(1 << (2 * INIT_L0)) + 1];   // exclusive prefix at each group (I,J) start
     const int S = 1 << l0;
@@ -143,6 +142,48 @@ __global__ void __launch_bounds__(1024) k_cull_init(CullArgs g, int l0, int4 *re
     }
 }
 
+__global__ void __launch_bounds__(1024) k_cull_init(CullArgs g, int l0, int4 *rec, int32_t *cnt)
+{
+    pdl_wait();
+    pdl_trigger();
+    cull_init_body(g, l0, rec, cnt);
+}
+
+// 8-bit child mask of parent record r at level l (bit 2q + dk, q = (di<<1|dj)):
+//   pa = n2A_{l+1}[4*Morton(I,K) + (di<<1|dk)],  pb = n2B_{l+1}[4*Morton(K,J) + (dk<<1|dj)]
+__device__ __forceinline__ uint32_t cull_parent_mask(const CullArgs &g, int l, int4 r, const double *an,
+                                                     const double *bn, double T)
+{
+    uint32_t code = r.x;
+    int K = r.y, I = morton_i(code), J = morton_j(code);
+    const double2 *pa2 = reinterpret_cast<const double2 *>(an + 4 * (int64_t)a_code(g, I, K));
+    const double2 *pb2 = reinterpret_cast<const double2 *>(bn + 4 * (int64_t)morton(K, J));
+    double2 a01 = __ldg(pa2), a23 = __ldg(pa2 + 1), b01 = __ldg(pb2), b23 = __ldg(pb2 + 1);
+    // [di][dk]; for A^T the stored child (dk, di) of node (K, I)
+    double pa[2][2] = {{a01.x, a01.y}, {a23.x, a23.y}};
+    if (g.transA) {
+        pa[0][1] = a23.x;
+        pa[1][0] = a01.y;
+    }
+    double pb[2][2] = {{b01.x, b01.y}, {b23.x, b23.y}};  // [dk][dj]
+    uint32_t mm = 0;
+#pragma unroll
+    for (int di = 0; di < 2; di++) {
+        if (!rows_meet(g, 2 * I + di, l + 1)) continue;
+#pragma unroll
+        for (int dj = 0; dj < 2; dj++)
+#pragma unroll
+            for (int dk = 0; dk < 2; dk++)
+                if (keep(pa[di][dk], pb[dk][dj], T)) mm |= 1u << (2 * ((di << 1) | dj) + dk);
+    }
+    return mm;
+}
+
+__device__ __forceinline__ int4 mask_counts(uint32_t mm)
+{
+    return make_int4(__popc(mm & 3u), __popc((mm >> 2) & 3u), __popc((mm >> 4) & 3u), __popc((mm >> 6) & 3u));
+}
+
 // ------------------------------------------------------- level mask + scan
 // Parent task t at level l -> 8 children at level l+1.  child (di,dk,dj):
 //   pa = n2A_{l+1}[4*Morton(I,K) + (di<<1|dk)],  pb = n2B_{l+1}[4*Morton(K,J) + (dk<<1|dj)]
@@ -176,32 +217,9 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
             c[i] = make_int4(0, 0, 0, 0);
             m[i] = 0;
             if (t < n) {
-                int4 r = rec[t];
-                uint32_t code = r.x;
-                int K = r.y, I = morton_i(code), J = morton_j(code);
-                const double2 *pa2 = reinterpret_cast<const double2 *>(an + 4 * (int64_t)a_code(g, I, K));
-                const double2 *pb2 = reinterpret_cast<const double2 *>(bn + 4 * (int64_t)morton(K, J));
-                double2 a01 = __ldg(pa2), a23 = __ldg(pa2 + 1), b01 = __ldg(pb2), b23 = __ldg(pb2 + 1);
-                // [di][dk]; for A^T the stored child (dk, di) of node (K, I)
-                double pa[2][2] = {{a01.x, a01.y}, {a23.x, a23.y}};
-                if (g.transA) {
-                    pa[0][1] = a23.x;
-                    pa[1][0] = a01.y;
-                }
-                double pb[2][2] = {{b01.x, b01.y}, {b23.x, b23.y}};  // [dk][dj]
-                uint32_t mm = 0;
-#pragma unroll
-                for (int di = 0; di < 2; di++) {
-                    if (!rows_meet(g, 2 * I + di, l + 1)) continue;
-#pragma unroll
-                    for (int dj = 0; dj < 2; dj++)
-#pragma unroll
-                        for (int dk = 0; dk < 2; dk++)
-                            if (keep(pa[di][dk], pb[dk][dj], T)) mm |= 1u << (2 * ((di << 1) | dj) + dk);
-                }
+                const uint32_t mm = cull_parent_mask(g, l, rec[t], an, bn, T);
                 m[i] = mm;
-                c[i] = make_int4(__popc(mm & 3u), __popc((mm >> 2) & 3u), __popc((mm >> 4) & 3u),
-                                 __popc((mm >> 6) & 3u));
+                c[i] = mask_counts(mm);
                 csum = vadd(csum, c[i]);
             }
         }
@@ -240,19 +258,15 @@ __global__ void __launch_bounds__(CT) k_cull_scan(CullArgs g, int l, const int4 
 __device__ __forceinline__ int comp(int4 v, int q) { return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w; }
 
 // ------------------------------------------------------------- scatter
+// children of parent t, emitted per quadrant q in (K, dk) order (order-preserving)
 template <bool FINAL>
-__global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const int4 *rec,
-                                                      const uint8_t *mask, const int4 *pre,
-                                                      int4 *rec_out, int32_t *tA, int32_t *tB,
-                                                      int32_t *tK, const int32_t *cnt)
+__device__ __forceinline__ void cull_scatter_one(const CullArgs &g, const int4 *rec, const uint8_t *mask,
+                                                 const int4 *pre, int t, int4 *rec_out, int32_t *tA, int32_t *tB,
+                                                 int32_t *tK)
 {
-    pdl_wait();
-    pdl_trigger();
-    if (cnt[CNT_OVERFLOW]) return;   // see k_cull_scan
-    const int n = clamp_n(cnt, l, g.cap);
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    do {
         uint32_t m = mask[t];
-        if (!m) continue;
+        if (!m) break;
         int4 r = rec[t];
         int4 P = pre[t], Ps = pre[r.z], Pe = pre[r.w];
         int base = Ps.x + Ps.y + Ps.z + Ps.w;  // children of all earlier groups
@@ -286,7 +300,21 @@ __global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const i
             }
             base += cq;
         }
-    }
+    } while (0);
+}
+
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_cull_scatter(CullArgs g, int l, const int4 *rec,
+                                                      const uint8_t *mask, const int4 *pre,
+                                                      int4 *rec_out, int32_t *tA, int32_t *tB,
+                                                      int32_t *tK, const int32_t *cnt)
+{
+    pdl_wait();
+    pdl_trigger();
+    if (cnt[CNT_OVERFLOW]) return;   // see k_cull_scan
+    const int n = clamp_n(cnt, l, g.cap);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        cull_scatter_one<FINAL>(g, rec, mask, pre, t, rec_out, tA, tB, tK);
 }
 
 // Final records -> segments when the init level is already the leaf level.
@@ -357,6 +385,127 @@ __global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, in
     if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) cnt[CNT_NSEG] = 0;
 }
 
+// ------------------------------------------------------- single-CTA query
+// Small problems (the level sizes of C1/C2 are ~10^2-10^4 triples) are latency-bound:
+// the multi-kernel chain costs ~9 launches per product.  k_cull_small runs the SAME
+// algorithm -- init level, then per level the child masks, the int4 exclusive scan of
+// per-quadrant counts (sequential tiles of one CTA instead of a decoupled look-back
+// across CTAs), the order-preserving scatter, and the segment compaction -- in one
+// 1024-thread CTA with block barriers between phases.  Every array it writes equals
+// the chain's bit for bit (same records, prefixes, tasks, segments; same overflow
+// rule), so the products do not depend on which form ran.
+constexpr int SMALL_T = 1024;
+
+__global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4 *rec0, int4 *rec1, uint8_t *mask,
+                                                        int4 *pre, int32_t *tA, int32_t *tB, int32_t *tK,
+                                                        int64_t cap_segs, int32_t *seg_code, int32_t *seg_start,
+                                                        int32_t *seg_len, int32_t *cnt)
+{
+    __shared__ int4 sw4[SMALL_T / 32];
+    __shared__ V1 sw1[SMALL_T / 32];
+    pdl_wait();
+    pdl_trigger();
+    for (int i = threadIdx.x; i < 64; i += SMALL_T) cnt[i] = 0;
+    __syncthreads();
+    int4 *rec[2] = {rec0, rec1};
+    int cur = 0;
+    cull_init_body(g, l0, rec[cur], cnt);
+    __syncthreads();
+    const double T = cull_T(g);
+    for (int l = l0; l < g.L; l++) {
+        if (cnt[CNT_OVERFLOW]) return;
+        const int n = clamp_n(cnt, l, g.cap);
+        const double *an = g.a_n2 + pyr_off(l + 1), *bn = g.b_n2 + pyr_off(l + 1);
+        // masks + per-quadrant counts, exclusive int4 scan in task order
+        int4 carry = make_int4(0, 0, 0, 0);
+        for (int t0 = 0; t0 < n; t0 += SMALL_T * CI) {
+            const int tb = t0 + threadIdx.x * CI;
+            int4 c[CI];
+            uint32_t m[CI];
+            int4 csum = make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int i = 0; i < CI; i++) {
+                const int t = tb + i;
+                m[i] = t < n ? cull_parent_mask(g, l, rec[cur][t], an, bn, T) : 0u;
+                c[i] = mask_counts(m[i]);
+                csum = vadd(csum, c[i]);
+            }
+            int4 tot;
+            int4 p = vadd(carry, block_excl_scan<int4, SMALL_T>(csum, &tot, sw4));
+#pragma unroll
+            for (int i = 0; i < CI; i++) {
+                const int t = tb + i;
+                if (t < n) {
+                    pre[t] = p;
+                    mask[t] = (uint8_t)m[i];
+                }
+                p = vadd(p, c[i]);
+            }
+            carry = vadd(carry, tot);
+        }
+        if (threadIdx.x == 0) {
+            pre[n] = carry;
+            const int total = carry.x + carry.y + carry.z + carry.w;
+            cnt[l + 1] = total;
+            if (total > g.cap) cnt[CNT_OVERFLOW] = 1;
+        }
+        __syncthreads();
+        if (cnt[CNT_OVERFLOW]) return;
+        if (l + 1 == g.L) {
+            for (int t = threadIdx.x; t < n; t += SMALL_T)
+                cull_scatter_one<true>(g, rec[cur], mask, pre, t, rec[cur ^ 1], tA, tB, tK);
+        } else {
+            for (int t = threadIdx.x; t < n; t += SMALL_T)
+                cull_scatter_one<false>(g, rec[cur], mask, pre, t, rec[cur ^ 1], nullptr, nullptr, nullptr);
+        }
+        cur ^= 1;
+        __syncthreads();
+    }
+    if (cnt[CNT_OVERFLOW]) return;
+    const int n = clamp_n(cnt, g.L, g.cap);
+    if (l0 == g.L) {   // the init level is the leaf level: tasks straight from the records
+        for (int t = threadIdx.x; t < n; t += SMALL_T) {
+            const int4 r = rec[cur][t];
+            const int i = morton_i(r.x), j = morton_j(r.x), k = r.y;
+            tA[t] = g.a_slot[a_code(g, i, k)];
+            tB[t] = g.b_slot[morton(k, j)];
+            tK[t] = k;
+        }
+    }
+    // segment heads (record r starts its group: r.z == t) -> {code, start, len}
+    int carry = 0;
+    for (int t0 = 0; t0 < n; t0 += SMALL_T * CI) {
+        const int tb = t0 + threadIdx.x * CI;
+        int4 r[CI];
+        int hs = 0;
+#pragma unroll
+        for (int i = 0; i < CI; i++) {
+            const int t = tb + i;
+            r[i] = t < n ? rec[cur][t] : make_int4(0, 0, -1, 0);
+            hs += (t < n && r[i].z == t) ? 1 : 0;
+        }
+        V1 tot;
+        int sidx = carry + block_excl_scan<V1, SMALL_T>(V1{hs}, &tot, sw1).x;
+#pragma unroll
+        for (int i = 0; i < CI; i++) {
+            const int t = tb + i;
+            if (t < n && r[i].z == t) {
+                if (sidx < cap_segs) {
+                    seg_code[sidx] = r[i].x;
+                    seg_start[sidx] = t;
+                    seg_len[sidx] = r[i].w - r[i].z;
+                }
+                sidx++;
+            }
+        }
+        carry += tot.x;
+    }
+    if (threadIdx.x == 0) {
+        cnt[CNT_NSEG] = carry;
+        if (carry > cap_segs) cnt[CNT_OVERFLOW] = 1;
+    }
+}
+
 // ------------------------------------------------------------- host side
 void cull_free(spamm_ctx ctx, Cull *cw)
 {
@@ -412,6 +561,21 @@ static spamm_status cull_alloc(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap
     return SPAMM_OK;
 }
 
+// The single-CTA query for small problems: nb <= 128 (C1, C2), decided from the shape
+// alone so a captured graph and the host-driven path always agree.
+// SPAMM_CULL_SMALL=0 disables it (A/B checks).
+static bool cull_small_ok(spamm_ctx ctx, const Cull *cw, spamm_mat A)
+{
+    static const int mode = [] {
+        const char *e = getenv("SPAMM_CULL_SMALL");
+        return e && *e ? atoi(e) : 1;
+    }();
+    if (!mode) return false;
+    if (A->nb <= 128) return true;
+    (void)ctx;
+    return false;
+}
+
 // Enqueue the whole query (no host sync).
 static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0,
                                  int r1, int transA)
@@ -423,6 +587,13 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     cw->b = A->b;
     CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap, L, r0, r1, transA};
     cudaStream_t s = ctx->stream;
+    if (cull_small_ok(ctx, cw, A)) {
+        cw->final_buf = (L - l0) & 1;
+        CK(launch_k(ctx, k_cull_small, 1, SMALL_T, 0, g, l0, cw->rec[0], cw->rec[1], cw->mask, cw->pre, cw->tA, cw->tB,
+                    cw->tK, cw->cap_segs, cw->seg_code, cw->seg_start, cw->seg_len, cw->counters));
+        CKL(ctx);
+        return SPAMM_OK;
+    }
     const int64_t nflags = (int64_t)(SPAMM_MAX_L + 2) * cw->tiles;
     const int pdl = A->dist ? 0 : 1;   // row partition: the predecessor may be a collective
     if (pdl) {

@@ -649,6 +649,16 @@ static int spmv_sym_mode()
     return m;
 }
 
+// SPAMM_GRAPH=0 also turns off the graph-replayed power step
+static bool graph_power_mode()
+{
+    static const bool on = [] {
+        const char *e = getenv("SPAMM_GRAPH");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
 {
     const int nb = s->nb;
@@ -710,8 +720,7 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     // row partition: local block rows of w = s v, then all ranks gather the full w and
     // form the norm partials from it (each row is computed by one rank with the
     // single-device arithmetic: bitwise G-invariant)
-    auto mv = [&](const double *x, double *y) -> spamm_status {
-        int32_t *tk = tickets + nmv++;
+    auto mv = [&](const double *x, double *y, int32_t *tk) -> spamm_status {
         if (tma) {
             switch (s->b) {
             case 16: {
@@ -751,8 +760,9 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
         }
         return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
     };
-    for (int it = 0; it < K; it++) {
-        ST(mv(v, w));
+    // one power step: w = s v, then v = w / ||w|| (its ticket zeroed first)
+    auto power_step = [&](int32_t *tk) -> spamm_status {
+        ST(mv(v, w, tk));
         if (tma) {   // the fix-up's (or, row partition, k_row_sumsq's) per-block-row partials
             const int g = (int)std::min<int64_t>(NRM_CTAS, nb);
             if (s->dist) k_norm_apply<<<g, 256, 0, st>>>(w, n, nrm_part, nb, v);
@@ -766,8 +776,46 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
             else CK(launch_pdl(k_normalize, 1, 1024, 0, st, (const double *)w, n, v));
         }
         ctx->launches++;
+        return SPAMM_OK;
+    };
+    // Single device, K >= 8: the step (same kernels, same order) is captured once as a
+    // CUDA graph and replayed K times, so the K launch pairs cost one graph launch each
+    // (C2 setup: ~200 stream launches) -- c is bitwise the same.
+    cudaGraphExec_t gexec = nullptr;
+    int64_t per_step = 0;
+    if (!s->dist && K >= 8 && graph_power_mode()) {
+        const int64_t l0 = ctx->launches;
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        ctx->capturing = true;
+        spamm_status r = SPAMM_OK;
+        if (cudaMemsetAsync(tickets, 0, sizeof(int32_t), st) != cudaSuccess) r = set_err(ctx, SPAMM_ECUDA, "memset");
+        if (!r) r = power_step(tickets);
+        ctx->capturing = false;
+        cudaError_t e = cudaStreamEndCapture(st, &graph);
+        per_step = ctx->launches - l0;
+        ctx->launches = l0;
+        if (!r && e == cudaSuccess) e = cudaGraphInstantiate(&gexec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (r || e != cudaSuccess) {   // not capturable here: the plain launch loop below
+            cudaGetLastError();
+            gexec = nullptr;
+        }
     }
-    ST(mv(v, w));
+    for (int it = 0; it < K; it++) {
+        if (gexec) {
+            cudaError_t e = cudaGraphLaunch(gexec, st);
+            if (e != cudaSuccess) {
+                cudaGraphExecDestroy(gexec);
+                return check_cuda(ctx, e, "power-step graph launch");
+            }
+            ctx->launches += per_step;
+        } else {
+            ST(power_step(tickets + nmv++));
+        }
+    }
+    if (gexec) cudaGraphExecDestroy(gexec);   // safe while the launches are in flight
+    ST(mv(v, w, tickets + K));
     k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
     CKL(ctx);
     double h = 0;
