@@ -439,15 +439,13 @@ def run_ours(args):
             return h
 
         def upload():
-            # block-list inputs: the library's asynchronous upload (prefetch half of the
-            # build); dense inputs go through spamm_build_tree's host path in the step
-            return sp.spamm_stage_blocks(ctx, cfg.b, *h_in) if kind != "dense" else None
+            # the library's asynchronous upload (prefetch half of the build)
+            if kind == "dense":
+                return sp.spamm_stage_dense(ctx, h_in[0])
+            return sp.spamm_stage_blocks(ctx, cfg.b, *h_in)
 
         def e2e_step(i, staged, last):
-            if staged is not None:
-                S = sp.spamm_build_tree_staged(ctx, cfg.n, staged)   # waits for its H2D
-            else:
-                S = build(h_in)                                      # host pointer: H2D in the call
+            S = sp.spamm_build_tree_staged(ctx, cfg.n, cfg.b, staged)   # waits for its H2D
             nxt = None if last else upload()          # next input's H2D overlaps this step
             if args.channel == "single":
                 r = sp.spamm_ns_sqrt_single(ctx, S, tau, iters, tau_s=tau_s, t_stop=t_stop, scaled=scaled)
@@ -487,9 +485,9 @@ def run_ours(args):
                "h2d_bytes_per_step": int(D.sum_over_ranks(in_bytes, dev)),
                "d2h_bytes_per_step": int(D.sum_over_ranks(d2h, dev)),
                "ms_per_step": ems / args.steps,
-               "path": "C ABI host pointers: spamm_stage_blocks (pinned host input; H2D on the library's "
-                       "upload stream, issued for step i+1 while step i computes) + spamm_build_tree_staged, "
-                       "or spamm_build_tree(pinned host dense input) for KMS; spamm_export_blocks_async "
+               "path": "C ABI host pointers: spamm_stage_blocks / spamm_stage_dense (pinned host input; H2D "
+                       "on the library's upload stream, issued for step i+1 while step i computes) + "
+                       "spamm_build_tree_staged; spamm_export_blocks_async "
                        "(pinned host output; D2H on the library's copy stream, overlapping the next step) "
                        "+ spamm_copies_join"}
 

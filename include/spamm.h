@@ -333,7 +333,11 @@ spamm_status spamm_copies_wait(spamm_ctx ctx);
 typedef struct spamm_staged_s *spamm_staged;
 spamm_status spamm_stage_blocks(spamm_ctx ctx, int64_t nblocks, int32_t b, const int32_t *bi,
                                 const int32_t *bj, const double *blocks, spamm_staged *out);
-spamm_status spamm_build_tree_staged(spamm_ctx ctx, int64_t n, spamm_staged staged, spamm_mat *out);
+/* the same for a dense n x n row-major HOST input with leading dimension ld (the
+ * prefetch half of spamm_build_tree) */
+spamm_status spamm_stage_dense(spamm_ctx ctx, const double *dense, int64_t n, int64_t ld, spamm_staged *out);
+/* b must equal the block-list upload's; for a dense upload n must equal its n */
+spamm_status spamm_build_tree_staged(spamm_ctx ctx, int64_t n, int32_t b, spamm_staged staged, spamm_mat *out);
 void spamm_staged_free(spamm_staged staged);
 
 /* ------------------------------------------------- measurement utilities */

@@ -33,7 +33,7 @@ __all__ = [
     "spamm_comm_destroy", "spamm_ctx_set_comm", "spamm_mat_rows", "spamm_row_task_counts",
     "VolumeSink", "spamm_ctx_set_volume_sink",
     "spamm_export_blocks_async", "spamm_copies_join", "spamm_copies_wait",
-    "spamm_stage_blocks", "spamm_build_tree_staged", "spamm_staged_free",
+    "spamm_stage_blocks", "spamm_stage_dense", "spamm_build_tree_staged", "spamm_staged_free",
 ]
 
 STATUS = {0: "SPAMM_OK", 1: "SPAMM_EINVAL", 2: "SPAMM_ESHAPE", 3: "SPAMM_ENOMEM",
@@ -145,7 +145,8 @@ def load():
         "spamm_copies_join": (i32, [vp]),
         "spamm_copies_wait": (i32, [vp]),
         "spamm_stage_blocks": (i32, [vp, i64, i32, vp, vp, vp, P(vp)]),
-        "spamm_build_tree_staged": (i32, [vp, i64, vp, P(vp)]),
+        "spamm_stage_dense": (i32, [vp, vp, i64, i64, P(vp)]),
+        "spamm_build_tree_staged": (i32, [vp, i64, i32, vp, P(vp)]),
         "spamm_staged_free": (None, [vp]),
     }
     for name, (res, args) in sigs.items():
@@ -639,11 +640,18 @@ def spamm_stage_blocks(ctx: Ctx, b: int, bi, bj, blocks) -> Staged:
     return Staged(ctx, h, (bi, bj, blocks))
 
 
-def spamm_build_tree_staged(ctx: Ctx, n: int, staged: Staged) -> Mat:
+def spamm_stage_dense(ctx: Ctx, dense) -> Staged:
+    """Start the upload of a HOST dense n x n row-major matrix (pinned tensor / numpy)."""
+    h = C.c_void_p()
+    ctx.check(load().spamm_stage_dense(ctx.h, _ptr(dense), dense.shape[0], dense.shape[1], C.byref(h)))
+    return Staged(ctx, h, (dense,))
+
+
+def spamm_build_tree_staged(ctx: Ctx, n: int, b: int, staged: Staged) -> Mat:
     """Build from a staged upload (consumes the handle)."""
     h = C.c_void_p()
     sh, staged.h = staged.h, None
-    ctx.check(load().spamm_build_tree_staged(ctx.h, n, sh, C.byref(h)))
+    ctx.check(load().spamm_build_tree_staged(ctx.h, n, b, sh, C.byref(h)))
     return Mat(ctx, h)
 
 

@@ -28,22 +28,31 @@ def headers():
         os.path.join(HERE, "..", "include", "spamm.h")]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(f) <= t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
+LIB_DEBUG = os.path.join(HERE, "libspamm_b200_debug.so")
+
+
+def build_debug(force: bool = False, verbose: bool = False) -> str:
+    """The SPAMM_DEBUG variant (device-side bounds asserts, common.cuh SPAMM_ASSERT);
+    select it with SPAMM_LIB=<path> for a checked test run."""
+    return build(force, verbose, lib=LIB_DEBUG, extra=["-DSPAMM_DEBUG"])
+
+
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, extra=()) -> str:
+    if not force and up_to_date(lib):
+        return lib
     # one nvcc per translation unit, in parallel, then one link
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     objdir = os.path.join(HERE, "build", f"obj{os.getpid()}")
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in sources()]
-    cmds = [[NVCC, *NVCC_FLAGS, "-c", "-o", o, s] for s, o in zip(sources(), objs)]
+    cmds = [[NVCC, *NVCC_FLAGS, *extra, "-c", "-o", o, s] for s, o in zip(sources(), objs)]
     if verbose:
         for c in cmds:
             print(" ".join(c))
@@ -53,12 +62,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if any(rcs):
         raise subprocess.CalledProcessError(max(rcs), "nvcc (see the errors above)")
     subprocess.check_call([NVCC, *LINK_FLAGS, "-o", tmp, *objs])
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     shutil.rmtree(objdir, ignore_errors=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
     import sys
-    build(force="-f" in sys.argv, verbose=True)
-    print(LIB)
+    if "--debug" in sys.argv:
+        print(build_debug(force="-f" in sys.argv, verbose=True))
+    else:
+        print(build(force="-f" in sys.argv, verbose=True))

@@ -125,6 +125,28 @@ __host__ __device__ static inline int64_t pyr_size(int L)
     return L == 0 ? 4 : pyr_off(L) + (int64_t(1) << (2 * L));
 }
 
+// ------------------------------------------------------------ debug asserts
+// Built with -DSPAMM_DEBUG (paper_1508_05856_b200/_build.py build_debug -> the
+// libspamm_b200_debug.so that SPAMM_LIB can select): device-side bounds checks on
+// every index that addresses a pool, a task list or a slot map; a failure prints the
+// condition and traps (the launch fails with an error the host reports).  Compiled out
+// of the product library.
+#ifdef SPAMM_DEBUG
+#include <cstdio>
+#define SPAMM_ASSERT(c)                                                                             \
+    do {                                                                                          \
+        if (!(c)) {                                                                               \
+            printf("SPAMM_ASSERT(%s) failed at %s:%d block %d thread %d\n", #c, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                            \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define SPAMM_ASSERT(c) \
+    do {                \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------------ Morton
 __host__ __device__ static inline uint32_t spread_bits(uint32_t x)
 {

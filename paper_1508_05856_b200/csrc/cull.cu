@@ -292,6 +292,9 @@ __device__ __forceinline__ void cull_scatter_one(const CullArgs &g, const int4 *
                                 tA[pos] = g.a_slot[a_code(g, i, ck)];
                                 tB[pos] = g.b_slot[morton(ck, j)];
                                 tK[pos] = ck;
+                                // a surviving triple has non-zero norms: both blocks are stored
+                                // (row partition: a remote B block is -1 until the halo patch)
+                                SPAMM_ASSERT(tA[pos] >= 0 && (tB[pos] >= 0 || g.r1 - g.r0 < (1 << g.L)));
                             }
                         }
                         pos++;

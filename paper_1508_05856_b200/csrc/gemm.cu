@@ -46,6 +46,9 @@ struct GemmArgs {
     double alpha;      // EPI_STORE: C = alpha (A (x) B) (the final unscale of the NS run, fused)
     const int32_t *nseg_dev;   // non-null: the segment count is read here (device-driven
                                // steps: the cull's count, no host round trip)
+    // capacities, checked by the SPAMM_DEBUG build only
+    int64_t a_cap, b_cap, halo_cap, c_cap, task_cap, seg_cap;
+    int nb;
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b)
@@ -117,9 +120,12 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
                 else if (g.seg_order) seg = g.seg_order[seg];
                 int code = 0;
                 if (seg >= 0) {
+                    SPAMM_ASSERT(seg < g.seg_cap);
                     start = g.seg_start[seg];
                     len = g.seg_len[seg];
                     code = g.seg_code[seg];
+                    SPAMM_ASSERT(len > 0 && start >= 0 && start + len <= g.task_cap);
+                    SPAMM_ASSERT((int64_t)code < (int64_t)g.nb * g.nb);
                 }
                 mbar_wait(&qempty[q], qphase ^ 1);
                 segq[q] = make_int4(seg, len, code, 0);
@@ -141,6 +147,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
                 for (int j = 0; j < cnt; j++) {
                     const int a = __shfl_sync(0xffffffffu, sa, j);
                     const int b = __shfl_sync(0xffffffffu, sb, j);
+                    SPAMM_ASSERT(a >= 0 && a < g.a_cap);
+                    SPAMM_ASSERT(b >= 0 ? b < g.b_cap : (-b - 1) < g.halo_cap);
                     if (lane == 0) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         mbar_expect_tx(&full[stage], 2 * TILE_BYTES);
@@ -227,6 +235,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
                     pacc[mf][nf][1] = y1;
                 }
         }
+        SPAMM_ASSERT(pseg >= 0 && pseg < g.c_cap);
         double *dst = g.c_pool + (int64_t)pseg * TILE;
 #pragma unroll
         for (int mf = 0; mf < MF; mf++) {
@@ -421,7 +430,8 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
     GemmArgs g{A->pool, B->pool, b_halo, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
                (int)nseg, seg_order, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
                cw->counters + CNT_GEMM_TICKET + ticket, cw->alpha,
-               device_count ? cw->counters + CNT_NSEG : nullptr};
+               device_count ? cw->counters + CNT_NSEG : nullptr,
+               A->cap, B->cap, b_halo ? (int64_t)1 << 40 : 0, C->cap, cw->cap, cw->cap_segs, A->nb};
     if (transA) {
         if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 1>(ctx, A->b, g);
         if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 1>(ctx, A->b, g);
@@ -493,7 +503,7 @@ spamm_status lpt_order(spamm_ctx ctx, const int32_t *seg_len, const int32_t *in,
 // nseg.. in ascending i (single-CTA scan, deterministic), then filled in parallel.
 template <int THREADS>
 __global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int r0, int r1, int64_t base,
-                              int32_t *newslot, int64_t *count_out, const int32_t *base_dev)
+                              int32_t *newslot, int64_t *count_out, const int32_t *base_dev, int64_t cap)
 {
     pdl_wait();
     pdl_trigger();
@@ -508,6 +518,7 @@ __global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int r0,
         V1 ex = block_excl_scan<V1, THREADS>(v, &tot, sw);
         if (i < nb) {
             int32_t s = v.x ? (int32_t)(base + run + ex.x) : -1;
+            SPAMM_ASSERT(s < 0 || s < cap);
             newslot[i] = s;
             if (v.x) {
                 slot_map[code] = s;
@@ -542,7 +553,7 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
     int32_t *newslot = dalloc<int32_t>(ctx, m->nb);
     if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
     CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, m->slot, m->coord, m->nb, m->r0, m->r1, base, newslot,
-                ctx->iscratch, (const int32_t *)nullptr));
+                ctx->iscratch, (const int32_t *)nullptr, m->cap));
     CKL(ctx);
     CK(launch_k(ctx, k_diag_fill, m->nb, 256, 0, (const int32_t *)newslot, m->pool, m->b, value,
                 m->norm2 + pyr_off(m->L)));
@@ -559,7 +570,7 @@ spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double v
     int32_t *newslot = dalloc<int32_t>(ctx, H->nb);
     if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
     CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, nseg, newslot, dcount,
-                (const int32_t *)nullptr));
+                (const int32_t *)nullptr, H->cap));
     CKL(ctx);
     CK(launch_k(ctx, k_diag_fill, H->nb, 256, 0, (const int32_t *)newslot, H->pool, H->b, value,
                 H->norm2 + pyr_off(H->L)));
@@ -573,7 +584,7 @@ spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev,
                             int64_t *dcount)
 {
     CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, (int64_t)0, newslot,
-                dcount, nseg_dev));
+                dcount, nseg_dev, H->cap));
     CKL(ctx);
     CK(launch_k(ctx, k_diag_fill, H->nb, 256, 0, (const int32_t *)newslot, H->pool, H->b, value,
                 H->norm2 + pyr_off(H->L)));

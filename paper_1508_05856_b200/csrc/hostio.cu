@@ -141,9 +141,31 @@ extern "C" spamm_status spamm_copies_wait(spamm_ctx ctx)
 // ------------------------------------------------------------------ uploads
 struct spamm_staged_s {
     int slot;
-    int64_t gen, nblocks;
+    int64_t gen, nblocks;   // block list: nblocks; dense: -1
     int b;
+    int64_t n;              // dense: n x n, row-major (ld = n in the slot)
 };
+
+// slot qi refilled with `bytes` from the upload stream (grown when needed)
+static spamm_status slot_fill(spamm_ctx ctx, XState *x, int qi, size_t need)
+{
+    ISlot &q = x->in[qi];
+    if (q.bytes < need) {
+        // growth (rare): the slot's previous upload and build must be over first
+        CK(cudaEventSynchronize(q.loaded));
+        CK(cudaEventSynchronize(q.consumed));
+        dev_free(ctx, q.dev, q.bytes);
+        q.bytes = need + need / 8;
+        q.dev = dev_alloc(ctx, q.bytes);
+        if (!q.dev) {
+            q.bytes = 0;
+            return set_err(ctx, SPAMM_ENOMEM, "upload staging (%lld bytes)", (long long)need);
+        }
+        CK(cudaStreamSynchronize(ctx->stream));   // the allocation is usable on any stream
+    }
+    CK(cudaStreamWaitEvent(x->up, q.consumed, 0));   // the slot's previous build has read it
+    return SPAMM_OK;
+}
 
 extern "C" spamm_status spamm_stage_blocks(spamm_ctx ctx, int64_t nblocks, int32_t b, const int32_t *bi,
                                            const int32_t *bj, const double *blocks, spamm_staged *out)
@@ -160,23 +182,9 @@ extern "C" spamm_status spamm_stage_blocks(spamm_ctx ctx, int64_t nblocks, int32
     ISlot &q = x->in[qi];
     x->in_next = (x->in_next + 1) % SPAMM_ISLOTS;
     const int64_t b2 = (int64_t)b * b;
-    const size_t need = sizeof(double) * nblocks * b2 + 2 * sizeof(int32_t) * nblocks + 1024;
-    if (q.bytes < need) {
-        // growth (rare): the slot's previous upload and build must be over first
-        CK(cudaEventSynchronize(q.loaded));
-        CK(cudaEventSynchronize(q.consumed));
-        dev_free(ctx, q.dev, q.bytes);
-        q.bytes = need + need / 8;
-        q.dev = dev_alloc(ctx, q.bytes);
-        if (!q.dev) {
-            q.bytes = 0;
-            return set_err(ctx, SPAMM_ENOMEM, "upload staging (%lld blocks)", (long long)nblocks);
-        }
-        CK(cudaStreamSynchronize(ctx->stream));   // the allocation is usable on any stream
-    }
+    ST(slot_fill(ctx, x, qi, sizeof(double) * nblocks * b2 + 2 * sizeof(int32_t) * nblocks + 1024));
     double *dbl = (double *)q.dev;
     int32_t *dbi = (int32_t *)(dbl + nblocks * b2), *dbj = dbi + nblocks;
-    CK(cudaStreamWaitEvent(x->up, q.consumed, 0));   // the slot's previous build has read it
     if (nblocks > 0) {
         CK(cudaMemcpyAsync(dbl, blocks, sizeof(double) * nblocks * b2, cudaMemcpyHostToDevice, x->up));
         CK(cudaMemcpyAsync(dbi, bi, sizeof(int32_t) * nblocks, cudaMemcpyHostToDevice, x->up));
@@ -184,11 +192,32 @@ extern "C" spamm_status spamm_stage_blocks(spamm_ctx ctx, int64_t nblocks, int32
     }
     CK(cudaEventRecord(q.loaded, x->up));
     q.gen++;
-    *out = new spamm_staged_s{qi, q.gen, nblocks, b};
+    *out = new spamm_staged_s{qi, q.gen, nblocks, b, 0};
     return SPAMM_OK;
 }
 
-extern "C" spamm_status spamm_build_tree_staged(spamm_ctx ctx, int64_t n, spamm_staged staged, spamm_mat *out)
+extern "C" spamm_status spamm_stage_dense(spamm_ctx ctx, const double *dense, int64_t n, int64_t ld,
+                                          spamm_staged *out)
+{
+    if (!ctx || !out || !dense || n <= 0 || ld < n) return set_err(ctx, SPAMM_EINVAL, "bad argument");
+    *out = nullptr;
+    if (is_device_ptr(dense)) return set_err(ctx, SPAMM_EINVAL, "spamm_stage_dense reads host memory");
+    XState *x = nullptr;
+    ST(xstate(ctx, &x));
+    const int qi = x->in_next;
+    ISlot &q = x->in[qi];
+    x->in_next = (x->in_next + 1) % SPAMM_ISLOTS;
+    ST(slot_fill(ctx, x, qi, sizeof(double) * n * n + 1024));
+    CK(cudaMemcpy2DAsync(q.dev, sizeof(double) * n, dense, sizeof(double) * ld, sizeof(double) * n, n,
+                         cudaMemcpyHostToDevice, x->up));
+    CK(cudaEventRecord(q.loaded, x->up));
+    q.gen++;
+    *out = new spamm_staged_s{qi, q.gen, -1, 0, n};
+    return SPAMM_OK;
+}
+
+extern "C" spamm_status spamm_build_tree_staged(spamm_ctx ctx, int64_t n, int32_t b, spamm_staged staged,
+                                                spamm_mat *out)
 {
     if (!ctx || !staged || !out) return set_err(ctx, SPAMM_EINVAL, "bad argument");
     XState *x = (XState *)ctx->xs;
@@ -198,12 +227,19 @@ extern "C" spamm_status spamm_build_tree_staged(spamm_ctx ctx, int64_t n, spamm_
         return set_err(ctx, SPAMM_EINVAL, "staged upload overwritten (more than %d uploads outstanding)",
                        SPAMM_ISLOTS);
     }
-    const int64_t nb = staged->nblocks, b2 = (int64_t)staged->b * staged->b;
-    const double *dbl = (const double *)q.dev;
-    const int32_t *dbi = (const int32_t *)(dbl + nb * b2), *dbj = dbi + nb;
     spamm_status st = SPAMM_OK;
-    if (cudaStreamWaitEvent(ctx->stream, q.loaded, 0) != cudaSuccess) st = set_err(ctx, SPAMM_ECUDA, "upload wait");
-    if (!st) st = spamm_build_tree_blocks(ctx, n, staged->b, nb, dbi, dbj, dbl, out);
+    if (staged->nblocks >= 0 && staged->b != b) st = set_err(ctx, SPAMM_EINVAL, "b differs from the upload's");
+    if (staged->nblocks < 0 && staged->n != n) st = set_err(ctx, SPAMM_ESHAPE, "n differs from the upload's");
+    if (!st && cudaStreamWaitEvent(ctx->stream, q.loaded, 0) != cudaSuccess)
+        st = set_err(ctx, SPAMM_ECUDA, "upload wait");
+    if (!st && staged->nblocks < 0) {
+        st = spamm_build_tree(ctx, (const double *)q.dev, n, n, b, out);
+    } else if (!st) {
+        const int64_t nbk = staged->nblocks, b2 = (int64_t)b * b;
+        const double *dbl = (const double *)q.dev;
+        const int32_t *dbi = (const int32_t *)(dbl + nbk * b2), *dbj = dbi + nbk;
+        st = spamm_build_tree_blocks(ctx, n, b, nbk, dbi, dbj, dbl, out);
+    }
     cudaEventRecord(q.consumed, ctx->stream);   // the slot may be refilled after the build
     delete staged;
     return st;

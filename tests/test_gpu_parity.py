@@ -484,3 +484,37 @@ def test_volume_sink_whole_run_matches_oracle(ctx):
             assert P.triples(g) == P.triples(tasks[q]), (k, q)
             d = np.max(np.abs(np.stack([g[:, 0] - g[:, 2], g[:, 0] - g[:, 1], g[:, 2] - g[:, 1]])), axis=0)
             assert np.array_equal(sink.hist[3 * k + q], np.bincount(np.minimum(d, nb - 1), minlength=nb))
+
+
+def test_async_host_io_equals_sync(ctx):
+    """The C ABI's asynchronous host I/O (upload on the library's upload stream, export on
+    its copy stream) gives exactly the synchronous calls' results: a staged block list and
+    a staged dense input build the same quadtrees, spamm_export_blocks_async writes the same
+    blocks as spamm_export_blocks, and a third outstanding upload invalidates the first."""
+    c = si.CONFIGS["C3"]
+    _, (bi, bj, blocks) = si.make_input(c, n=4096)
+    hb = [torch.from_numpy(x).pin_memory() for x in (bi, bj, blocks)]
+    A = sp().spamm_build_tree_blocks(ctx, 4096, 64, *hb)
+    A2 = sp().spamm_build_tree_staged(ctx, 4096, 64, sp().spamm_stage_blocks(ctx, 64, *hb))
+    s = si.kms(1024, 0.8)
+    D = sp().spamm_build_tree(ctx, s, 32)
+    D2 = sp().spamm_build_tree_staged(ctx, 1024, 32, sp().spamm_stage_dense(ctx, torch.from_numpy(s).pin_memory()))
+    for M, M2 in ((A, A2), (D, D2)):
+        g1, g2 = sp().spamm_export_blocks(ctx, M), sp().spamm_export_blocks(ctx, M2)
+        for x, y in zip(g1, g2):
+            assert np.array_equal(x, y)
+        L = (M.n // M.b).bit_length() - 1
+        assert np.array_equal(sp().spamm_level_norms2(ctx, M, L), sp().spamm_level_norms2(ctx, M2, L))
+        k = M.nblocks
+        out = (torch.empty(k, dtype=torch.int32).pin_memory(), torch.empty(k, dtype=torch.int32).pin_memory(),
+               torch.empty((k, M.b, M.b), dtype=torch.float64).pin_memory())
+        assert sp().spamm_export_blocks_async(ctx, M, out) == k
+        sp().spamm_copies_wait(ctx)
+        for x, y in zip(g1, out):
+            assert np.array_equal(x, y.numpy())
+    h1 = sp().spamm_stage_blocks(ctx, 64, *hb)
+    sp().spamm_stage_blocks(ctx, 64, *hb)
+    sp().spamm_stage_blocks(ctx, 64, *hb)          # SPAMM_ISLOTS = 2: h1's slot is refilled
+    with pytest.raises(sp().SpammError) as e:
+        sp().spamm_build_tree_staged(ctx, 4096, 64, h1)
+    assert e.value.code == 1
