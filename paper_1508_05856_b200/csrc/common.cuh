@@ -367,8 +367,18 @@ spamm_status cull_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double 
                       int transA = 0);
 spamm_status cull_start(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
                         int transA = 0);
+// arrays the query's first kernel clears (device-driven steps): slot maps -> -1,
+// pyramids -> 0 of up to 3 output matrices, and z[0..nz) -> 0
+struct CullClear {
+    int32_t *slot[3];
+    double *n2[3];
+    int64_t nslot, nn2;
+    double *z;
+    int64_t nz;
+};
 // enqueue only (fixed workspace, capacity-sized grids): for CUDA graph capture
-spamm_status cull_enqueue_fixed(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau);
+spamm_status cull_enqueue_fixed(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau,
+                                const CullClear *clear = nullptr);
 // (re)allocate a workspace for at least cap tasks per level and cap_segs segments
 spamm_status cull_reserve(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap_segs);
 spamm_status cull_complete(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0, int r1,
@@ -391,6 +401,9 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
 // caller-provided scratch (newslot [nb]); no allocation, no host round trip
 spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, double value, int32_t *newslot,
                             int64_t *dcount);
+// device-driven step, small nb: diagonal fix-up (1.5 I) + H's pyramid + t_k in one CTA
+spamm_status h_finish_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, int32_t *newslot,
+                          const double *trace_part, double *t_out);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
 // as diag_fixup without the host round trip: the count of appended blocks lands in
 // *dcount (device); the caller fetches it and sets H->nblk = nseg + count

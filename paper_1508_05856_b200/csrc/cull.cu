@@ -77,13 +77,29 @@ __device__ __forceinline__ int clamp_n(const int32_t *cnt, int l, int64_t cap)
 constexpr int INIT_L0 = 4;
 // zero the counters and the look-back tile flags of all levels (a kernel rather than
 // two memsets, so the whole query is one programmatic-dependent-launch chain)
-__global__ void k_cull_reset(int32_t *cnt, int ncnt, int32_t *flags, int64_t nflags)
+// output patterns cleared by the query's first kernel (device-driven step: the slot maps
+// of up to 3 matrices set to -1, their pyramids and one extra array zeroed), replacing
+// memset nodes on the step's critical path
+__device__ __forceinline__ void cull_clear(const CullClear &c, int64_t i0, int64_t stride)
+{
+    for (int m = 0; m < 3; m++) {
+        if (c.slot[m])
+            for (int64_t i = i0; i < c.nslot; i += stride) c.slot[m][i] = -1;
+        if (c.n2[m])
+            for (int64_t i = i0; i < c.nn2; i += stride) c.n2[m][i] = 0.0;
+    }
+    if (c.z)
+        for (int64_t i = i0; i < c.nz; i += stride) c.z[i] = 0.0;
+}
+
+__global__ void k_cull_reset(int32_t *cnt, int ncnt, int32_t *flags, int64_t nflags, CullClear clr)
 {
     pdl_wait();
     pdl_trigger();
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = i0; i < ncnt; i += stride) cnt[i] = 0;
     for (int64_t i = i0; i < nflags; i += stride) flags[i] = 0;
+    cull_clear(clr, i0, stride);
 }
 
 // the init level for a CTA of 1024 threads (k_cull_init and k_cull_small)
@@ -402,13 +418,14 @@ constexpr int SMALL_T = 1024;
 __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4 *rec0, int4 *rec1, uint8_t *mask,
                                                         int4 *pre, int32_t *tA, int32_t *tB, int32_t *tK,
                                                         int64_t cap_segs, int32_t *seg_code, int32_t *seg_start,
-                                                        int32_t *seg_len, int32_t *cnt)
+                                                        int32_t *seg_len, int32_t *cnt, CullClear clr)
 {
     __shared__ int4 sw4[SMALL_T / 32];
     __shared__ V1 sw1[SMALL_T / 32];
     pdl_wait();
     pdl_trigger();
     for (int i = threadIdx.x; i < 64; i += SMALL_T) cnt[i] = 0;
+    cull_clear(clr, threadIdx.x, SMALL_T);
     __syncthreads();
     int4 *rec[2] = {rec0, rec1};
     int cur = 0;
@@ -581,8 +598,9 @@ static bool cull_small_ok(spamm_ctx ctx, const Cull *cw, spamm_mat A)
 
 // Enqueue the whole query (no host sync).
 static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0,
-                                 int r1, int transA)
+                                 int r1, int transA, const CullClear *clear = nullptr)
 {
+    const CullClear clr = clear ? *clear : CullClear{};
     const int L = A->L;
     const int l0 = L < INIT_L0 ? L : INIT_L0;
     cw->L = L;
@@ -593,17 +611,19 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     if (cull_small_ok(ctx, cw, A)) {
         cw->final_buf = (L - l0) & 1;
         CK(launch_k(ctx, k_cull_small, 1, SMALL_T, 0, g, l0, cw->rec[0], cw->rec[1], cw->mask, cw->pre, cw->tA, cw->tB,
-                    cw->tK, cw->cap_segs, cw->seg_code, cw->seg_start, cw->seg_len, cw->counters));
+                    cw->tK, cw->cap_segs, cw->seg_code, cw->seg_start, cw->seg_len, cw->counters, clr));
         CKL(ctx);
         return SPAMM_OK;
     }
     const int64_t nflags = (int64_t)(SPAMM_MAX_L + 2) * cw->tiles;
     const int pdl = A->dist ? 0 : 1;   // row partition: the predecessor may be a collective
     if (pdl) {
-        CK(launch_pdl(k_cull_reset, (int)std::min<int64_t>(cdiv(nflags, 256), 4 * ctx->sm_count), 256, 0, s,
-                      cw->counters, 64, cw->tile_flag, nflags));
+        const int64_t work = std::max<int64_t>(nflags, std::max(clr.nslot, clr.nn2));
+        CK(launch_pdl(k_cull_reset, (int)std::min<int64_t>(cdiv(work, 256), 4 * ctx->sm_count), 256, 0, s,
+                      cw->counters, 64, cw->tile_flag, nflags, clr));
         CKL(ctx);
     } else {
+        if (clear) return set_err(ctx, SPAMM_EINVAL, "pattern clearing needs the single-device query");
         CK(cudaMemsetAsync(cw->counters, 0, sizeof(int32_t) * 64, s));
         CK(cudaMemsetAsync(cw->tile_flag, 0, sizeof(int32_t) * nflags, s));
     }
@@ -654,9 +674,10 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     return SPAMM_OK;
 }
 
-spamm_status cull_enqueue_fixed(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau)
+spamm_status cull_enqueue_fixed(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau,
+                                const CullClear *clear)
 {
-    return cull_enqueue(ctx, cw, A, B, tau, 0, A->nb, 0);
+    return cull_enqueue(ctx, cw, A, B, tau, 0, A->nb, 0, clear);
 }
 
 spamm_status cull_reserve(spamm_ctx ctx, Cull *cw, int64_t cap, int64_t cap_segs)

@@ -803,12 +803,13 @@ static bool graph_power_mode()
     return on;
 }
 
-// SPAMM_POWER_FUSED=0 keeps the launch loop for small n too
+// SPAMM_POWER_FUSED=1 selects the one-launch power iteration for small n (measured
+// slower than the launch loop so far: off by default)
 static bool fused_power_mode()
 {
     static const bool on = [] {
         const char *e = getenv("SPAMM_POWER_FUSED");
-        return !(e && *e == '0');
+        return e && *e == '1';
     }();
     return on;
 }
