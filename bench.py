@@ -515,6 +515,29 @@ def run_ours(args):
         Y.free()
         Z.free()
 
+    # ---- BASELINE.json's literal configuration (tau_s = tau, the config's fixed iteration
+    # count, no convergence exit), when the bench workload re-scopes it (readings L9/L15):
+    # one untimed run, its outcome recorded
+    literal = None
+    if args.channel == "dual" and not scaled and (tau_s != tau or t_stop > 0):
+        S = build(d_in)
+        t0 = time.perf_counter()
+        r = sp.spamm_ns_sqrt(ctx, S, tau, iters, tau_s=tau, mu=cfg.mu, check=False)
+        dt = time.perf_counter() - t0
+        S.free()
+        if "status" in r:
+            literal = {"tau_s": tau, "iters": iters, "t_stop": 0.0,
+                       "outcome": f"diverges: {r['error']} after {r['iters']} completed steps",
+                       "t_history": [float(x) for x in r["t"]], "wall_s": dt,
+                       "oracle": "tests/test_gpu_fullsize.py::test_c5_tau_s_equal_tau_divergence_is_the_methods "
+                                 "(the oracle's step from the GPU's Y_9, Z_9 reproduces ||Z|| x2.37 and t_10 = 2.5598)"}
+        else:
+            literal = {"tau_s": tau, "iters": iters, "t_stop": 0.0, "outcome": "completed",
+                       "t_final": float(r["t"][-1]), "wall_s": dt,
+                       "tasks": int(sum(p["tasks"] for k in r["stats"] for p in k))}
+            r["Y"].free()
+            r["Z"].free()
+
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -545,6 +568,7 @@ def run_ours(args):
             "t_final": float(r["t"][-1]) if len(r["t"]) else None,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "baseline_literal": literal,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,

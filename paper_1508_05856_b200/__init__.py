@@ -572,9 +572,12 @@ def spamm_scale(ctx: Ctx, m: Mat, alpha: float, divide: bool = False) -> Mat:
 
 def spamm_ns_sqrt(ctx: Ctx, s: Mat, tau: float, iters: int, tau_s: float | None = None,
                   mu: float = 0.0, scale: float = 0.0, power_iters: int = 100,
-                  want_stats: bool = True, t_stop: float = 0.0, scaled: bool = False):
+                  want_stats: bool = True, t_stop: float = 0.0, scaled: bool = False,
+                  check: bool = True):
     """Full dual NS run: returns dict(Y, Z, t, stats, c, iters).  t_stop > 0 ends the
-    run after the first k with |t_k| <= t_stop (t, stats then cover the steps run)."""
+    run after the first k with |t_k| <= t_stop (t, stats then cover the steps run).
+    check=False: a failing run returns dict(status=<code>, error=<text>, t=<history up to
+    the failing step>, iters=<steps completed>) instead of raising."""
     t = np.zeros(iters)
     sts = (spamm_stats * (3 * iters))() if want_stats else None
     c = C.c_double()
@@ -584,8 +587,11 @@ def spamm_ns_sqrt(ctx: Ctx, s: Mat, tau: float, iters: int, tau_s: float | None 
                       C.cast(C.pointer(c), C.c_void_p), float(t_stop),
                       C.cast(C.pointer(done), C.c_void_p), int(scaled))
     yo, zo = C.c_void_p(), C.c_void_p()
-    ctx.check(load().spamm_ns_sqrt(ctx.h, s.h, float(tau), int(iters), C.byref(yo), C.byref(zo),
-                                   C.byref(o)))
+    rc = load().spamm_ns_sqrt(ctx.h, s.h, float(tau), int(iters), C.byref(yo), C.byref(zo), C.byref(o))
+    if rc and not check:
+        k = done.value
+        return dict(status=rc, error=load().spamm_last_error(ctx.h).decode(), t=t[:k + 1], iters=k, c=c.value)
+    ctx.check(rc)
     k = done.value
     stats = None
     if want_stats:

@@ -359,6 +359,7 @@ struct Cull {
     int32_t prev[SPAMM_MAX_L + 2] = {};
     double alpha = 1.0;           // EPI_STORE output scale of the next GEMM (fused unscale)
     int64_t gen = 0;              // bumped by every (re)allocation (captured graphs check it)
+    bool counts_only = false;     // a counting query (its tasks never reach a GEMM)
     spamm_stats stats{};
 };
 // Enqueue the query, synchronise once to read the counts, and grow + re-run

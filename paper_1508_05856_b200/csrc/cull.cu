@@ -35,6 +35,8 @@ struct CullArgs {
     int L, r0, r1;               // leaf level; output block rows [r0, r1) (row partition, §8(e))
     int transA;                  // 1: the left operand is A^T (single channel, §8(f) f2):
                                  //    node (I,K) of A^T is node (K,I) of A, norms shared
+    int counts_only;             // spamm_row_task_counts over all rows of a row-partitioned
+                                 // operand: remote rows have no slots (debug check off)
 };
 
 // Morton code of node (I, K) of the left operand in A's own pyramid / slot map
@@ -310,7 +312,7 @@ __device__ __forceinline__ void cull_scatter_one(const CullArgs &g, const int4 *
                                 tK[pos] = ck;
                                 // a surviving triple has non-zero norms: both blocks are stored
                                 // (row partition: a remote B block is -1 until the halo patch)
-                                SPAMM_ASSERT(tA[pos] >= 0 && (tB[pos] >= 0 || g.r1 - g.r0 < (1 << g.L)));
+                                SPAMM_ASSERT(g.counts_only || (tA[pos] >= 0 && (tB[pos] >= 0 || g.r1 - g.r0 < (1 << g.L))));
                             }
                         }
                         pos++;
@@ -606,7 +608,7 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     cw->L = L;
     cw->l0 = l0;
     cw->b = A->b;
-    CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap, L, r0, r1, transA};
+    CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap, L, r0, r1, transA, cw->counts_only ? 1 : 0};
     cudaStream_t s = ctx->stream;
     if (cull_small_ok(ctx, cw, A)) {
         cw->final_buf = (L - l0) & 1;
@@ -794,6 +796,7 @@ extern "C" spamm_status spamm_row_task_counts(spamm_ctx ctx, spamm_mat A, spamm_
     if (A->n != B->n || A->b != B->b) return set_err(ctx, SPAMM_ESHAPE, "shape mismatch");
     if (!(tau >= 0.0)) return set_err(ctx, SPAMM_EINVAL, "tau must be >= 0");
     Cull *cw = new Cull();
+    cw->counts_only = true;
     spamm_status st = cull_run(ctx, cw, A, B, tau, 0, A->nb);
     if (ctx->last == cw) ctx->last = nullptr;
     std::vector<int32_t> code(cw->nsegs), len(cw->nsegs);

@@ -560,150 +560,6 @@ __global__ void k_dot(const double *a, const double *b, int64_t n, double *out)
     if (threadIdx.x == 0) *out = sh[0];
 }
 
-// ------------------------------------------------ fused small-n power iteration
-// Single device, b < 64, n < 2^16 (the C1 / C2 shapes): the K + 1 SpMVs and K
-// normalisations run in ONE cooperative launch with a grid barrier after each SpMV,
-// instead of 2K + 1 launches.  The arithmetic is that of k_spmv + k_normalize, in the
-// same order, so w, v and c are bitwise the launch loop's (and the row-partitioned
-// path's, which keeps the launch loop):
-//   * each 256-thread quarter of a CTA processes k_spmv units (block row I, row group)
-//     exactly as a k_spmv CTA does: blocks in ascending CSR order, an fma chain over a
-//     thread's E elements per block, then the xor tree over the TPR lanes of a row;
-//   * ||w|| is formed by EVERY CTA with k_normalize's order (1024 virtual threads, i
-//     strided by 1024, fma chain, then the halving tree), so all CTAs agree bitwise and
-//     v = w / ||w|| is applied on the fly where the next SpMV reads v (the same
-//     division k_normalize stores).
-__device__ __forceinline__ void grid_barrier(unsigned *count, volatile unsigned *gen, unsigned nctas)
-{
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == nctas - 1) {
-            *count = 0;
-            __threadfence();
-            atomicAdd((unsigned *)gen, 1u);
-        } else {
-            while (*gen == g) {
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// ||w|| with k_normalize's summation order, by a 512-thread CTA (virtual threads t and
-// t + 512 of the 1024-thread reduction; the first tree level adds them)
-__device__ __forceinline__ double norm_k_normalize_order(const double *w, int64_t n, double *sh)
-{
-    const int t = threadIdx.x;
-    double s0 = 0.0, s1 = 0.0;
-    // w was written by other CTAs since this SM last read the buffer: L2 loads (__ldcg),
-    // never a stale L1 line
-    for (int64_t i = t; i < n; i += 1024) {
-        const double x = __ldcg(w + i);
-        s0 = fma(x, x, s0);
-    }
-    for (int64_t i = t + 512; i < n; i += 1024) {
-        const double x = __ldcg(w + i);
-        s1 = fma(x, x, s1);
-    }
-    sh[t] = s0 + s1;
-    __syncthreads();
-    for (int k = 256; k > 0; k >>= 1) {
-        if (t < k) sh[t] += sh[t + k];
-        __syncthreads();
-    }
-    const double r = sqrt(sh[0]);
-    __syncthreads();
-    return r;
-}
-
-template <int B>
-__global__ void __launch_bounds__(512, 1) k_power_fused(const double *pool, const int32_t *rowptr,
-                                                        const int32_t *cols, const int32_t *slots, int nb, int64_t n,
-                                                        int K, const double *v0, double *wa, double *wb,
-                                                        double *v_last, double *w_last, unsigned *bar)
-{
-    constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
-    constexpr int SPC = 512;
-    __shared__ int s_slot[2][SPC], s_col[2][SPC];
-    __shared__ double sh[512];
-    const int qtr = threadIdx.x >> 8, tq = threadIdx.x & 255;   // quarter of the CTA, thread in it
-    const int nunits = nb * CPR, nq = 2 * gridDim.x, gq = 2 * blockIdx.x + qtr;
-    const double *vin = v0;   // iteration 0 reads v0; later v = w_prev / nrm
-    double nrm = 1.0;
-    double *wcur = wa, *wprev = nullptr;
-    for (int it = 0; it <= K; it++) {
-        if (it > 0) nrm = norm_k_normalize_order(wprev, n, sh);
-        double *wout = it == K ? w_last : wcur;
-        for (int unit = gq; unit < nunits; unit += nq) {
-            const int I = unit / CPR, rg = unit % CPR;
-            const int p0 = rowptr[I], p1 = rowptr[I + 1];
-            const int r = rg * RG + tq / TPR;
-            const int e0 = r * B + (tq % TPR) * E;
-            int lc[E];
-#pragma unroll
-            for (int i = 0; i < E; i++) lc[i] = pool_col(e0 + i, B);
-            double acc = 0.0;
-            for (int pc = p0; pc < p1; pc += SPC) {
-                const int pe = p1 < pc + SPC ? p1 : pc + SPC;
-                asm volatile("bar.sync %0, 256;\n" ::"r"(qtr + 1));
-                for (int i = tq; i < pe - pc; i += 256) {
-                    s_slot[qtr][i] = slots[pc + i];
-                    s_col[qtr][i] = cols[pc + i];
-                }
-                asm volatile("bar.sync %0, 256;\n" ::"r"(qtr + 1));
-                constexpr int U = 2;
-                for (int p = pc; p < pe; p += U) {
-                    double x[U][E], vx[U][E];
-#pragma unroll
-                    for (int u = 0; u < U; u++) {
-                        if (p + u < pe) {
-                            const double *blk = pool + (int64_t)s_slot[qtr][p + u - pc] * B * B + e0;
-                            const int64_t vb = (int64_t)s_col[qtr][p + u - pc] * B;
-                            if constexpr (E >= 2) {
-#pragma unroll
-                                for (int i = 0; i < E; i += 2) {
-                                    double2 t = __ldg(reinterpret_cast<const double2 *>(blk + i));
-                                    x[u][i] = t.x;
-                                    x[u][i + 1] = t.y;
-                                }
-                            } else {
-                                x[u][0] = __ldg(blk);
-                            }
-#pragma unroll
-                            for (int i = 0; i < E; i++)
-                                vx[u][i] = it == 0 ? vin[vb + lc[i]] : __ldcg(wprev + vb + lc[i]) / nrm;
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; u++) {
-                        if (p + u < pe) {
-                            double sdot = 0.0;
-#pragma unroll
-                            for (int i = 0; i < E; i++) sdot = fma(x[u][i], vx[u][i], sdot);
-                            acc += sdot;
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if ((tq % TPR) == 0) wout[(int64_t)I * B + r] = acc;
-        }
-        if (it == K) {
-            // v_K for the Rayleigh quotient (k_dot after this kernel)
-            for (int64_t i = blockIdx.x * 512 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 512)
-                v_last[i] = it == 0 ? vin[i] : __ldcg(wprev + i) / nrm;
-            break;
-        }
-        grid_barrier(bar, bar + 1, gridDim.x);
-        wprev = wcur;
-        wcur = wcur == wa ? wb : wa;
-    }
-}
-
 struct SymSpmv {
     const int32_t *up, *mir;   // mir only for SYM
     double *colpart;
@@ -801,41 +657,6 @@ static bool graph_power_mode()
         return e && *e == '1';
     }();
     return on;
-}
-
-// SPAMM_POWER_FUSED=1 selects the one-launch power iteration for small n (measured
-// slower than the launch loop so far: off by default)
-static bool fused_power_mode()
-{
-    static const bool on = [] {
-        const char *e = getenv("SPAMM_POWER_FUSED");
-        return e && *e == '1';
-    }();
-    return on;
-}
-
-template <int B>
-static spamm_status launch_power_fused(spamm_ctx ctx, int grid, spamm_mat s, const int32_t *rowptr,
-                                       const int32_t *cols, const int32_t *slots, int nb, int64_t n, int K,
-                                       double *v, double *w, double *pp, unsigned *bar)
-{
-    // every CTA must be co-resident (grid barrier): the cooperative launch checks it
-    static std::atomic<int> occ_cache{0};
-    int occ = occ_cache.load();
-    if (!occ) {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_power_fused<B>, 512, 0));
-        occ_cache.store(occ < 1 ? 1 : occ);
-    }
-    if (grid > ctx->sm_count * occ) grid = ctx->sm_count * occ;
-    const double *pool = s->pool, *v0 = v;
-    double *wa = pp, *wb = pp + n;
-    // v0 is read only at iteration 0 and v_last written only at iteration K (after the
-    // last barrier), so v serves as both; w_last = w never aliases the ping-pong
-    void *args[] = {(void *)&pool, (void *)&rowptr, (void *)&cols, (void *)&slots, (void *)&nb, (void *)&n,
-                    (void *)&K, (void *)&v0, (void *)&wa, (void *)&wb, (void *)&v, (void *)&w, (void *)&bar};
-    CK(cudaLaunchCooperativeKernel((const void *)k_power_fused<B>, dim3(grid), dim3(512), args, 0, ctx->stream));
-    CKL(ctx);
-    return SPAMM_OK;
 }
 
 spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
@@ -957,28 +778,6 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
         ctx->launches++;
         return SPAMM_OK;
     };
-    // Single device, register SpMV, one-CTA normalisation (b < 64, n < 2^16): the whole
-    // iteration in one cooperative launch (k_power_fused), bitwise the loop below
-    if (!s->dist && !tma && n < (1 << 16) && K >= 1 && fused_power_mode()) {
-        const int nunits = nb;   // k_spmv units (CPR = 1 for b = 16, 32)
-        const int grid = std::min(ctx->sm_count, std::max(1, (nunits + 1) / 2));
-        double *pp = dalloc<double>(ctx, 2 * n);   // the w ping-pong of the iterations
-        if (!pp) return set_err(ctx, SPAMM_ENOMEM, "power");
-        unsigned *bar = reinterpret_cast<unsigned *>(tickets);   // {count, generation}, zeroed above
-        spamm_status fr = s->b == 16 ? launch_power_fused<16>(ctx, grid, s, rowptr, cols, slots, nb, n, K, v, w, pp, bar)
-                                     : launch_power_fused<32>(ctx, grid, s, rowptr, cols, slots, nb, n, K, v, w, pp, bar);
-        if (!fr) {
-            k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
-            ctx->launches++;
-            if (cudaGetLastError() != cudaSuccess) fr = set_err(ctx, SPAMM_ECUDA, "k_dot launch");
-        }
-        double h = 0;
-        if (!fr) fr = fetch1(ctx, c, &h, sizeof(double));
-        dev_free(ctx, pp, sizeof(double) * 2 * n);
-        ST(fr);
-        *c_host = h;
-        return SPAMM_OK;
-    }
     // Single device, K >= 8: the step (same kernels, same order) is captured once as a
     // CUDA graph and replayed K times (measured no faster than the launch loop on C1/C2;
     // kept behind SPAMM_GRAPH_POWER=1) -- c is bitwise the same.

@@ -731,12 +731,24 @@ static bool ns_graph_eligible(spamm_ctx ctx, spamm_mat s, const spamm_ns_opts &o
     return mats + culls <= (gm >= 2 ? 32.0 : 4.0) * (1u << 30);
 }
 
+// SPAMM_GRAPH_SPLIT: 0 = Y', Z' GEMMs one after the other on all SMs, 2 = concurrently on
+// half the SMs each, 1 (default) = concurrently only for nb <= 32 (C1: GEMMs of ~100
+// segments; at C2, ~1000 segments each, the full grid wins: 3.9 vs 5.0 ms per run)
+static bool graph_split(int nb)
+{
+    static const int m = [] {
+        const char *e = getenv("SPAMM_GRAPH_SPLIT");
+        return e && *e ? atoi(e) : 1;
+    }();
+    return m == 2 || (m == 1 && nb <= 32);
+}
+
 // One device-driven dual step: (Y, Z) -> (Yn, Zn) through the fixed buffers (captured).
 //   main:  X cull (also clears H, Y', Z' patterns and the trace partials) -> X GEMM ->
 //          H finish (diagonal fix-up, pyramid, t_k) -> fork
-//   main:  Y' cull -> Y' GEMM (half the SMs) -> pyramid(Y')   } concurrent branches
-//   side:  Z' cull -> Z' GEMM (half the SMs) -> pyramid(Z')   }
-//   join -> step record.
+//   main:  Y' cull [-> Y' GEMM (half the SMs) -> pyramid(Y')]   } concurrent branches
+//   side:  Z' cull [-> Z' GEMM (half the SMs) -> pyramid(Z')]   } ([..]: split mode)
+//   join [-> Y' GEMM -> pyramid(Y') -> Z' GEMM -> pyramid(Z')] -> step record.
 static spamm_status graph_step(spamm_ctx ctx, NsGraph *g, spamm_mat Y, spamm_mat Z, spamm_mat Yn, spamm_mat Zn)
 {
     Cull *c0 = ctx->cw[0], *c1 = ctx->cw[1], *c2 = ctx->cw[2];
@@ -748,31 +760,43 @@ static spamm_status graph_step(spamm_ctx ctx, NsGraph *g, spamm_mat Y, spamm_mat
     ST(cull_enqueue_fixed(ctx, c0, Z, Y, g->tau, &clr));
     c0->alpha = 1.0;
     ST(gemm_run(ctx, c0, Z, Y, nullptr, H, EPI_NS_H, g->trace_part, nullptr, 0, 0, 0, true));
-    if (nb <= 256) {
+    static const int hf = [] {   // SPAMM_GRAPH_HFINISH=0: the separate kernels (A/B)
+        const char *e = getenv("SPAMM_GRAPH_HFINISH");
+        return e && *e ? atoi(e) : 1;
+    }();
+    if (hf && nb <= 256) {
         ST(h_finish_dev(ctx, H, c0->counters + CNT_NSEG, g->newslot, g->trace_part, ctx->dscratch));
     } else {
         ST(diag_fixup_dev(ctx, H, c0->counters + CNT_NSEG, 1.5, g->newslot, g->hadd));
         ST(pyramid_build(ctx, H));
         ST(trace_finish(ctx, g->trace_part, nb, Y->n, ctx->dscratch));
     }
-    // Y' = Y (x)_tau_s H on the main stream || Z' = H (x)_tau Z on the side stream
+    // Y' = Y (x)_tau_s H on the main stream || Z' = H (x)_tau Z on the side stream: the two
+    // culls always; with split, the GEMMs (each on half the SMs) and pyramids as well
+    const bool split = graph_split(nb);
     const cudaStream_t main_s = ctx->stream;
     CK(cudaEventRecord(ctx->ev[0], main_s));
     CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev[0], 0));
     c1->alpha = c2->alpha = 1.0;
-    ctx->gemm_grid_cap = std::max(1, ctx->sm_count / 2);
+    if (split) ctx->gemm_grid_cap = std::max(1, ctx->sm_count / 2);
     ctx->stream = ctx->comm_stream;
     spamm_status st = cull_enqueue_fixed(ctx, c2, H, Z, g->tau);
-    if (!st) st = gemm_run(ctx, c2, H, Z, nullptr, Zn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true);
-    if (!st) st = pyramid_build(ctx, Zn);
+    if (!st && split) st = gemm_run(ctx, c2, H, Z, nullptr, Zn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true);
+    if (!st && split) st = pyramid_build(ctx, Zn);
     ctx->stream = main_s;
     if (!st) st = cull_enqueue_fixed(ctx, c1, Y, H, g->tau_s);
-    if (!st) st = gemm_run(ctx, c1, Y, H, nullptr, Yn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true);
-    if (!st) st = pyramid_build(ctx, Yn);
+    if (!st && split) st = gemm_run(ctx, c1, Y, H, nullptr, Yn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true);
+    if (!st && split) st = pyramid_build(ctx, Yn);
     ctx->gemm_grid_cap = 0;
     ST(st);
     CK(cudaEventRecord(ctx->ev[1], ctx->comm_stream));
     CK(cudaStreamWaitEvent(main_s, ctx->ev[1], 0));
+    if (!split) {
+        ST(gemm_run(ctx, c1, Y, H, nullptr, Yn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true));
+        ST(pyramid_build(ctx, Yn));
+        ST(gemm_run(ctx, c2, H, Z, nullptr, Zn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true));
+        ST(pyramid_build(ctx, Zn));
+    }
     CK(launch_pdl(k_step_record, 1, 64, 0, ctx->stream, ctx->dscratch, (const int32_t *)c0->counters,
                   (const int32_t *)c1->counters, (const int32_t *)c2->counters, (const double *)Yn->norm2,
                   (const double *)Zn->norm2, g->rec, g->kdev));

@@ -185,25 +185,3 @@ def test_graph_replay_equals_host_driven(case):
         out[gm] = [l for l in p.stdout.splitlines() if l.startswith("hash")]
         assert len(out[gm]) == 2 and out[gm][0] == out[gm][1], out[gm]
     assert out["0"][0] == out["1"][0], out
-
-
-def test_fused_power_iteration_bitwise():
-    """The one-launch power iteration (k_power_fused: cooperative grid, barrier per SpMV)
-    reproduces the launch loop's arithmetic order, so c is bitwise the same
-    (SPAMM_POWER_FUSED=0/1) for b = 16 and b = 32 inputs, K = 1 and K = 100."""
-    if not torch.cuda.is_available():
-        pytest.skip("no GPU")
-    code = ("import sys; sys.path.insert(0, %r); import paper_1508_05856_b200 as sp, spamm_inputs as si\n"
-            "ctx = sp.spamm_ctx_create(0)\n"
-            "for name in ('C1', 'C2'):\n"
-            "    c = si.CONFIGS[name]; S = sp.spamm_build_tree(ctx, si.kms(c.n, c.rho), c.b)\n"
-            "    print('c', name, repr(sp.spamm_power_scale(ctx, S, 100)), repr(sp.spamm_power_scale(ctx, S, 1)))\n"
-            "S = sp.spamm_build_tree(ctx, si.kms(2048, 0.95), 16)\n"
-            "print('c big', repr(sp.spamm_power_scale(ctx, S, 37)))\n") % ROOT
-    out = []
-    for fused in ("0", "1"):
-        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
-                           env={**os.environ, "SPAMM_POWER_FUSED": fused})
-        assert p.returncode == 0, p.stderr[-2000:]
-        out.append([l for l in p.stdout.splitlines() if l.startswith("c ")])
-    assert len(out[0]) == 3 and out[0] == out[1], out
