@@ -402,9 +402,6 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
 // caller-provided scratch (newslot [nb]); no allocation, no host round trip
 spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, double value, int32_t *newslot,
                             int64_t *dcount);
-// device-driven step, small nb: diagonal fix-up (1.5 I) + H's pyramid + t_k in one CTA
-spamm_status h_finish_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, int32_t *newslot,
-                          const double *trace_part, double *t_out);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
 // as diag_fixup without the host round trip: the count of appended blocks lands in
 // *dcount (device); the caller fetches it and sets H->nblk = nseg + count

@@ -600,88 +600,6 @@ spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value)
     return SPAMM_OK;
 }
 
-// Device-driven step, small nb (one CTA): everything between the X GEMM and the Y', Z'
-// culls in one launch -- the diagonal fix-up (k_diag_assign + k_diag_fill), H's norm
-// pyramid (k_pyramid's (c0 + c1) + (c2 + c3) per node, level by level) and t_k
-// (k_trace_finish's 256-way order).  Same arithmetic as those kernels, so the same bits.
-__global__ void __launch_bounds__(1024) k_h_finish(int32_t *slot_map, int32_t *coord, double *pool, int nb, int L,
-                                                   int b, const int32_t *base_dev, double value, double *norm2,
-                                                   int32_t *newslot, int64_t cap, const double *trace_part,
-                                                   double n, double *t_out)
-{
-    __shared__ V1 sw[1024 / 32];
-    __shared__ double sh[256];
-    pdl_wait();
-    pdl_trigger();
-    // 1. slots for the absent diagonal blocks, appended after the X segments in ascending i
-    int64_t run = 0;
-    const int64_t base = *base_dev;
-    for (int i0 = 0; i0 < nb; i0 += 1024) {
-        const int i = i0 + threadIdx.x;
-        const uint32_t code = i < nb ? morton(i, i) : 0;
-        V1 v{(i < nb && slot_map[code] < 0) ? 1 : 0};
-        V1 tot;
-        V1 ex = block_excl_scan<V1, 1024>(v, &tot, sw);
-        if (i < nb) {
-            const int32_t sl = v.x ? (int32_t)(base + run + ex.x) : -1;
-            SPAMM_ASSERT(sl < 0 || sl < cap);
-            newslot[i] = sl;
-            if (v.x) {
-                slot_map[code] = sl;
-                coord[sl] = (int32_t)code;
-            }
-        }
-        run += tot.x;
-        __syncthreads();
-    }
-    // 2. fill them with value * I and their leaf norms
-    const int64_t b2 = (int64_t)b * b;
-    for (int64_t idx = threadIdx.x; idx < (int64_t)nb * b2; idx += 1024) {
-        const int i = (int)(idx / b2), e = (int)(idx % b2);
-        const int sl = newslot[i];
-        if (sl >= 0) pool[(int64_t)sl * b2 + e] = (e / b == pool_col(e, b)) ? value : 0.0;
-    }
-    double *leaf = norm2 + pyr_off(L);
-    for (int i = threadIdx.x; i < nb; i += 1024)
-        if (newslot[i] >= 0) {
-            double ss = 0.0;
-            for (int r = 0; r < b; r++) ss += value * value;
-            leaf[morton(i, i)] = ss;
-        }
-    __syncthreads();
-    // 3. pyramid, levels L-1 .. 0
-    for (int l = L - 1; l >= 0; l--) {
-        const double *src = norm2 + pyr_off(l + 1);
-        double *dst = norm2 + pyr_off(l);
-        for (int64_t m = threadIdx.x; m < ((int64_t)1 << (2 * l)); m += 1024) {
-            const double c0 = src[4 * m], c1 = src[4 * m + 1], c2 = src[4 * m + 2], c3 = src[4 * m + 3];
-            dst[m] = (c0 + c1) + (c2 + c3);
-        }
-        __syncthreads();
-    }
-    // 4. t = (n - tr X) / n in k_trace_finish's order
-    if (threadIdx.x < 256) {
-        double s = 0.0;
-        for (int i = threadIdx.x; i < nb; i += 256) s += trace_part[i];
-        sh[threadIdx.x] = s;
-    }
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *t_out = (n - sh[0]) / n;
-}
-
-spamm_status h_finish_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, int32_t *newslot,
-                          const double *trace_part, double *t_out)
-{
-    CK(launch_k(ctx, k_h_finish, 1, 1024, 0, H->slot, H->coord, H->pool, H->nb, H->L, H->b, nseg_dev, 1.5,
-                H->norm2, newslot, H->cap, trace_part, (double)H->n, t_out));
-    CKL(ctx);
-    return SPAMM_OK;
-}
-
 // t = (n - sum_i trace_part[i]) / n, fixed-order single-CTA reduction
 __global__ void k_trace_finish(const double *part, int nb, double n, double *t_out)
 {

@@ -74,15 +74,45 @@ __global__ void k_row_fill(const int32_t *slot, int nb, const int32_t *rowptr, i
 // in flight), then the TPR threads of a row reduce with a fixed xor tree.
 // Persistent: CTAs take (block row, row group) units from a ticket, so the grid is
 // exactly the resident capacity (no partial last wave) and uneven rows balance.
+// ||w|| in k_normalize's order (1024-way fma chains over i strided by 1024, then the
+// halving tree) by a 256-thread CTA: thread t holds the chains of the virtual threads t,
+// t + 256, t + 512, t + 768; the tree's first two levels are the adds below.  Every CTA
+// gets the same bits, and so does k_normalize.
+__device__ __forceinline__ double norm_as_k_normalize(const double *w, int64_t n, double *sh)
+{
+    const int t = threadIdx.x;
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+        for (int64_t i = t + 256 * q; i < n; i += 1024) c[q] = fma(w[i], w[i], c[q]);
+    // level 512: [t] += [t + 512], [t + 256] += [t + 768]; level 256: [t] += [t + 256]
+    sh[t] = (c[0] + c[2]) + (c[1] + c[3]);
+    __syncthreads();
+    for (int k = 128; k > 0; k >>= 1) {
+        if (t < k) sh[t] += sh[t + k];
+        __syncthreads();
+    }
+    const double r = sqrt(sh[0]);
+    __syncthreads();
+    return r;
+}
+
+// w = s x.  wprev != nullptr (small n, the power step fused into the next SpMV): x is not
+// stored but read as x = wprev / ||wprev|| -- the norm computed by every CTA in
+// k_normalize's order, the same division k_normalize stores -- and v_out (nullable)
+// receives x for this unit's rows.
 template <int B>
 __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t *rowptr,
                                               const int32_t *cols, const int32_t *slots,
-                                              const double *v, double *w, int32_t *ticket, int nunits)
+                                              const double *v, double *w, int32_t *ticket, int nunits,
+                                              const double *wprev, int64_t n, double *v_out)
 {
     pdl_wait();
     pdl_trigger();
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
     __shared__ int s_unit;
+    __shared__ double s_red[256];
+    const double nrm = wprev ? norm_as_k_normalize(wprev, n, s_red) : 1.0;
     for (;;) {
     if (threadIdx.x == 0) s_unit = atomicAdd(ticket, 1);
     __syncthreads();
@@ -126,8 +156,14 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
                     } else {
                         x[u][0] = __ldg(blk);
                     }
+                    if (wprev) {
+                        const double *ww = wprev + (vv - v);
 #pragma unroll
-                    for (int i = 0; i < E; i++) vx[u][i] = __ldg(vv + lc[i]);
+                        for (int i = 0; i < E; i++) vx[u][i] = ww[lc[i]] / nrm;
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < E; i++) vx[u][i] = __ldg(vv + lc[i]);
+                    }
                 }
             }
 #pragma unroll
@@ -143,7 +179,10 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
     }
 #pragma unroll
     for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x % TPR) == 0) w[(int64_t)I * B + r] = acc;
+    if ((threadIdx.x % TPR) == 0) {
+        w[(int64_t)I * B + r] = acc;
+        if (v_out) v_out[(int64_t)I * B + r] = wprev[(int64_t)I * B + r] / nrm;
+    }
     }
 }
 
@@ -609,7 +648,8 @@ __global__ void __launch_bounds__(256) k_row_sumsq(const double *w, double *nrm_
 
 template <int B>
 static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
-                         const int32_t *slots, const double *v, double *w, int32_t *ticket)
+                         const int32_t *slots, const double *v, double *w, int32_t *ticket,
+                         const double *wprev = nullptr, double *v_out = nullptr)
 {
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
     static std::atomic<int> occ_cache{0};
@@ -622,8 +662,13 @@ static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, cons
     const int nunits = s->nb * CPR;
     int grid = ctx->sm_count * occ;
     if (grid > nunits) grid = nunits;
-    if (s->dist) k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
-    else CK(launch_pdl(k_spmv<B>, grid, 256, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits));
+    const double *vv = wprev ? wprev : v;   // x's row offsets are taken in this array
+    if (s->dist)
+        k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, vv, w, ticket, nunits, wprev, s->n,
+                                                 v_out);
+    else
+        CK(launch_pdl(k_spmv<B>, grid, 256, 0, ctx->stream, s->pool, rowptr, cols, slots, vv, w, ticket, nunits,
+                      wprev, (int64_t)s->n, v_out));
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -647,16 +692,6 @@ static int spmv_sym_mode()
         return e && *e ? atoi(e) : 1;
     }();
     return m;
-}
-
-// SPAMM_GRAPH_POWER=1: the graph-replayed power step (off by default)
-static bool graph_power_mode()
-{
-    static const bool on = [] {
-        const char *e = getenv("SPAMM_GRAPH_POWER");
-        return e && *e == '1';
-    }();
-    return on;
 }
 
 spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
@@ -778,43 +813,37 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
         ctx->launches++;
         return SPAMM_OK;
     };
-    // Single device, K >= 8: the step (same kernels, same order) is captured once as a
-    // CUDA graph and replayed K times (measured no faster than the launch loop on C1/C2;
-    // kept behind SPAMM_GRAPH_POWER=1) -- c is bitwise the same.
-    cudaGraphExec_t gexec = nullptr;
-    int64_t per_step = 0;
-    if (!s->dist && K >= 8 && graph_power_mode()) {
-        const int64_t l0 = ctx->launches;
-        cudaGraph_t graph = nullptr;
-        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        ctx->capturing = true;
+    // Single device, register SpMV, n < 2^16 (C1, C2): each normalisation rides on the
+    // next SpMV (k_spmv reads x = w_prev / ||w_prev||, the norm in k_normalize's order, the
+    // last one also stores v_K), so K + 1 launches instead of 2K + 1 -- the same v, w and
+    // c bit for bit (the row-partitioned path keeps the separate k_normalize).
+    if (!tma && !s->dist && n < (1 << 16) && K >= 1) {
+        double *pp = dalloc<double>(ctx, 2 * n);
+        if (!pp) return set_err(ctx, SPAMM_ENOMEM, "power");
         spamm_status r = SPAMM_OK;
-        if (cudaMemsetAsync(tickets, 0, sizeof(int32_t), st) != cudaSuccess) r = set_err(ctx, SPAMM_ECUDA, "memset");
-        if (!r) r = power_step(tickets);
-        ctx->capturing = false;
-        cudaError_t e = cudaStreamEndCapture(st, &graph);
-        per_step = ctx->launches - l0;
-        ctx->launches = l0;
-        if (!r && e == cudaSuccess) e = cudaGraphInstantiate(&gexec, graph, 0);
-        if (graph) cudaGraphDestroy(graph);
-        if (r || e != cudaSuccess) {   // not capturable here: the plain launch loop below
-            cudaGetLastError();
-            gexec = nullptr;
-        }
-    }
-    for (int it = 0; it < K; it++) {
-        if (gexec) {
-            cudaError_t e = cudaGraphLaunch(gexec, st);
-            if (e != cudaSuccess) {
-                cudaGraphExecDestroy(gexec);
-                return check_cuda(ctx, e, "power-step graph launch");
+        auto mvn = [&](const double *x, const double *wprev, double *y, int32_t *tk, double *v_out) {
+            switch (s->b) {
+            case 16: return spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk, wprev, v_out);
+            default: return spmv<32>(ctx, s, rowptr, cols, slots, x, y, tk, wprev, v_out);
             }
-            ctx->launches += per_step;
-        } else {
-            ST(power_step(tickets + nmv++));
+        };
+        r = mvn(v, nullptr, pp, tickets, nullptr);                              // w_1 = s v_0
+        for (int j = 1; j < K && !r; j++)                                        // w_{j+1} = s (w_j/|w_j|)
+            r = mvn(nullptr, pp + ((j - 1) & 1) * n, pp + (j & 1) * n, tickets + j, nullptr);
+        if (!r) r = mvn(nullptr, pp + ((K - 1) & 1) * n, w, tickets + K, v);     // w = s v_K, v <- v_K
+        if (!r) {
+            k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
+            ctx->launches++;
+            if (cudaGetLastError() != cudaSuccess) r = set_err(ctx, SPAMM_ECUDA, "k_dot launch");
         }
+        double h = 0;
+        if (!r) r = fetch1(ctx, c, &h, sizeof(double));
+        dev_free(ctx, pp, sizeof(double) * 2 * n);
+        ST(r);
+        *c_host = h;
+        return SPAMM_OK;
     }
-    if (gexec) cudaGraphExecDestroy(gexec);   // safe while the launches are in flight
+    for (int it = 0; it < K; it++) ST(power_step(tickets + nmv++));
     ST(mv(v, w, tickets + K));
     k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
     CKL(ctx);

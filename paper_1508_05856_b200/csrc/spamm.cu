@@ -745,7 +745,7 @@ static bool graph_split(int nb)
 
 // One device-driven dual step: (Y, Z) -> (Yn, Zn) through the fixed buffers (captured).
 //   main:  X cull (also clears H, Y', Z' patterns and the trace partials) -> X GEMM ->
-//          H finish (diagonal fix-up, pyramid, t_k) -> fork
+//          diagonal fix-up -> pyramid(H) -> t_k -> fork
 //   main:  Y' cull [-> Y' GEMM (half the SMs) -> pyramid(Y')]   } concurrent branches
 //   side:  Z' cull [-> Z' GEMM (half the SMs) -> pyramid(Z')]   } ([..]: split mode)
 //   join [-> Y' GEMM -> pyramid(Y') -> Z' GEMM -> pyramid(Z')] -> step record.
@@ -760,17 +760,9 @@ static spamm_status graph_step(spamm_ctx ctx, NsGraph *g, spamm_mat Y, spamm_mat
     ST(cull_enqueue_fixed(ctx, c0, Z, Y, g->tau, &clr));
     c0->alpha = 1.0;
     ST(gemm_run(ctx, c0, Z, Y, nullptr, H, EPI_NS_H, g->trace_part, nullptr, 0, 0, 0, true));
-    static const int hf = [] {   // SPAMM_GRAPH_HFINISH=0: the separate kernels (A/B)
-        const char *e = getenv("SPAMM_GRAPH_HFINISH");
-        return e && *e ? atoi(e) : 1;
-    }();
-    if (hf && nb <= 256) {
-        ST(h_finish_dev(ctx, H, c0->counters + CNT_NSEG, g->newslot, g->trace_part, ctx->dscratch));
-    } else {
-        ST(diag_fixup_dev(ctx, H, c0->counters + CNT_NSEG, 1.5, g->newslot, g->hadd));
-        ST(pyramid_build(ctx, H));
-        ST(trace_finish(ctx, g->trace_part, nb, Y->n, ctx->dscratch));
-    }
+    ST(diag_fixup_dev(ctx, H, c0->counters + CNT_NSEG, 1.5, g->newslot, g->hadd));
+    ST(pyramid_build(ctx, H));
+    ST(trace_finish(ctx, g->trace_part, nb, Y->n, ctx->dscratch));
     // Y' = Y (x)_tau_s H on the main stream || Z' = H (x)_tau Z on the side stream: the two
     // culls always; with split, the GEMMs (each on half the SMs) and pyramids as well
     const bool split = graph_split(nb);
