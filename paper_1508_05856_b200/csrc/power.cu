@@ -74,45 +74,15 @@ __global__ void k_row_fill(const int32_t *slot, int nb, const int32_t *rowptr, i
 // in flight), then the TPR threads of a row reduce with a fixed xor tree.
 // Persistent: CTAs take (block row, row group) units from a ticket, so the grid is
 // exactly the resident capacity (no partial last wave) and uneven rows balance.
-// ||w|| in k_normalize's order (1024-way fma chains over i strided by 1024, then the
-// halving tree) by a 256-thread CTA: thread t holds the chains of the virtual threads t,
-// t + 256, t + 512, t + 768; the tree's first two levels are the adds below.  Every CTA
-// gets the same bits, and so does k_normalize.
-__device__ __forceinline__ double norm_as_k_normalize(const double *w, int64_t n, double *sh)
-{
-    const int t = threadIdx.x;
-    double c[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-        for (int64_t i = t + 256 * q; i < n; i += 1024) c[q] = fma(w[i], w[i], c[q]);
-    // level 512: [t] += [t + 512], [t + 256] += [t + 768]; level 256: [t] += [t + 256]
-    sh[t] = (c[0] + c[2]) + (c[1] + c[3]);
-    __syncthreads();
-    for (int k = 128; k > 0; k >>= 1) {
-        if (t < k) sh[t] += sh[t + k];
-        __syncthreads();
-    }
-    const double r = sqrt(sh[0]);
-    __syncthreads();
-    return r;
-}
-
-// w = s x.  wprev != nullptr (small n, the power step fused into the next SpMV): x is not
-// stored but read as x = wprev / ||wprev|| -- the norm computed by every CTA in
-// k_normalize's order, the same division k_normalize stores -- and v_out (nullable)
-// receives x for this unit's rows.
 template <int B>
 __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t *rowptr,
                                               const int32_t *cols, const int32_t *slots,
-                                              const double *v, double *w, int32_t *ticket, int nunits,
-                                              const double *wprev, int64_t n, double *v_out)
+                                              const double *v, double *w, int32_t *ticket, int nunits)
 {
     pdl_wait();
     pdl_trigger();
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
     __shared__ int s_unit;
-    __shared__ double s_red[256];
-    const double nrm = wprev ? norm_as_k_normalize(wprev, n, s_red) : 1.0;
     for (;;) {
     if (threadIdx.x == 0) s_unit = atomicAdd(ticket, 1);
     __syncthreads();
@@ -127,7 +97,9 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
 #pragma unroll
     for (int i = 0; i < E; i++) lc[i] = pool_col(e0 + i, B);
     double acc = 0.0;
-    constexpr int U = 4;      // blocks in flight per thread
+    // blocks in flight per thread: ~32-64 KB of loads in flight per CTA, what an SM needs
+    // to stream s near the HBM rate (the order of the sum over blocks does not depend on U)
+    constexpr int U = B == 16 ? 16 : 8;
     constexpr int SPC = 512;  // block-row entries staged in shared memory per pass
     __shared__ int s_slot[SPC], s_col[SPC];
     for (int pc = p0; pc < p1; pc += SPC) {
@@ -156,14 +128,8 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
                     } else {
                         x[u][0] = __ldg(blk);
                     }
-                    if (wprev) {
-                        const double *ww = wprev + (vv - v);
 #pragma unroll
-                        for (int i = 0; i < E; i++) vx[u][i] = ww[lc[i]] / nrm;
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < E; i++) vx[u][i] = __ldg(vv + lc[i]);
-                    }
+                    for (int i = 0; i < E; i++) vx[u][i] = __ldg(vv + lc[i]);
                 }
             }
 #pragma unroll
@@ -179,10 +145,7 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
     }
 #pragma unroll
     for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x % TPR) == 0) {
-        w[(int64_t)I * B + r] = acc;
-        if (v_out) v_out[(int64_t)I * B + r] = wprev[(int64_t)I * B + r] / nrm;
-    }
+    if ((threadIdx.x % TPR) == 0) w[(int64_t)I * B + r] = acc;
     }
 }
 
@@ -648,8 +611,7 @@ __global__ void __launch_bounds__(256) k_row_sumsq(const double *w, double *nrm_
 
 template <int B>
 static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
-                         const int32_t *slots, const double *v, double *w, int32_t *ticket,
-                         const double *wprev = nullptr, double *v_out = nullptr)
+                         const int32_t *slots, const double *v, double *w, int32_t *ticket)
 {
     constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
     static std::atomic<int> occ_cache{0};
@@ -662,13 +624,8 @@ static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, cons
     const int nunits = s->nb * CPR;
     int grid = ctx->sm_count * occ;
     if (grid > nunits) grid = nunits;
-    const double *vv = wprev ? wprev : v;   // x's row offsets are taken in this array
-    if (s->dist)
-        k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, vv, w, ticket, nunits, wprev, s->n,
-                                                 v_out);
-    else
-        CK(launch_pdl(k_spmv<B>, grid, 256, 0, ctx->stream, s->pool, rowptr, cols, slots, vv, w, ticket, nunits,
-                      wprev, (int64_t)s->n, v_out));
+    if (s->dist) k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
+    else CK(launch_pdl(k_spmv<B>, grid, 256, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits));
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -813,36 +770,6 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
         ctx->launches++;
         return SPAMM_OK;
     };
-    // Single device, register SpMV, n < 2^16 (C1, C2): each normalisation rides on the
-    // next SpMV (k_spmv reads x = w_prev / ||w_prev||, the norm in k_normalize's order, the
-    // last one also stores v_K), so K + 1 launches instead of 2K + 1 -- the same v, w and
-    // c bit for bit (the row-partitioned path keeps the separate k_normalize).
-    if (!tma && !s->dist && n < (1 << 16) && K >= 1) {
-        double *pp = dalloc<double>(ctx, 2 * n);
-        if (!pp) return set_err(ctx, SPAMM_ENOMEM, "power");
-        spamm_status r = SPAMM_OK;
-        auto mvn = [&](const double *x, const double *wprev, double *y, int32_t *tk, double *v_out) {
-            switch (s->b) {
-            case 16: return spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk, wprev, v_out);
-            default: return spmv<32>(ctx, s, rowptr, cols, slots, x, y, tk, wprev, v_out);
-            }
-        };
-        r = mvn(v, nullptr, pp, tickets, nullptr);                              // w_1 = s v_0
-        for (int j = 1; j < K && !r; j++)                                        // w_{j+1} = s (w_j/|w_j|)
-            r = mvn(nullptr, pp + ((j - 1) & 1) * n, pp + (j & 1) * n, tickets + j, nullptr);
-        if (!r) r = mvn(nullptr, pp + ((K - 1) & 1) * n, w, tickets + K, v);     // w = s v_K, v <- v_K
-        if (!r) {
-            k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
-            ctx->launches++;
-            if (cudaGetLastError() != cudaSuccess) r = set_err(ctx, SPAMM_ECUDA, "k_dot launch");
-        }
-        double h = 0;
-        if (!r) r = fetch1(ctx, c, &h, sizeof(double));
-        dev_free(ctx, pp, sizeof(double) * 2 * n);
-        ST(r);
-        *c_host = h;
-        return SPAMM_OK;
-    }
     for (int it = 0; it < K; it++) ST(power_step(tickets + nmv++));
     ST(mv(v, w, tickets + K));
     k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
