@@ -247,13 +247,14 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
                     make_double2(pacc[mf][nf][0], pacc[mf][nf][1]);
             }
         }
-        // xor-tree levels 16, 8, 4, 2, 1: level i in slice min(i, NKC - 1)
+        // xor-tree levels 16, 8, 4, 2, 1: level i in slice min(i, NKC - 1); the trace
+        // partials only on diagonal blocks (warp-uniform branch: ~1 segment in 100 at C5)
 #pragma unroll
         for (int i = 0; i < 5; i++) {
             if ((i < NKC - 1 ? i : NKC - 1) != kc) continue;
             const int o = 16 >> i;
             pss += __shfl_xor_sync(0xffffffffu, pss, o);
-            if (!STORE) ptr += __shfl_xor_sync(0xffffffffu, ptr, o);
+            if (!STORE && diag) ptr += __shfl_xor_sync(0xffffffffu, ptr, o);
         }
     };
     // after the last slice: deposit the warp's partials; the last warp of the CTA to

@@ -66,3 +66,20 @@ for name, (A, B) in (("Z*Y", (Z, Y)), ("Y*Z", (Y, Z))):
     print(f"{a.config} k={a.k} {name}: tasks {st['tasks']} segments {st['segments']} "
           f"({st['tasks'] / max(st['segments'], 1):.2f} per segment) {best:.3f} ms "
           f"{st['flops'] / best / 1e9:.2f} TFLOP/s", flush=True)
+# one whole NS step (X with the fused H epilogue, Y', Z'): GEMM time per product from the
+# library's phase events, best of --reps
+best = None
+for _ in range(a.reps):
+    sp.spamm_profile_enable(ctx, True)
+    Yn, Zn, t, st = sp.spamm_ns_step(ctx, Y, Z, tau, tau_s)
+    torch.cuda.synchronize()
+    prof = sp.spamm_profile_read(ctx)
+    sp.spamm_profile_enable(ctx, False)
+    Yn.free()
+    Zn.free()
+    if best is None or prof["gemm_ms"] < best[0]["gemm_ms"]:
+        best = (prof, st)
+prof, st = best
+fl = sum(p["flops"] for p in st)
+print(f"{a.config} k={a.k} NS step: tasks {[p['tasks'] for p in st]} GEMM {prof['gemm_ms']:.3f} ms "
+      f"({prof['gemm_count']} launches) {fl / prof['gemm_ms'] / 1e9:.2f} TFLOP/s", flush=True)
