@@ -21,12 +21,8 @@
 // whole query is enqueued with no host round trip.
 #include <algorithm>
 
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 #include "scan.cuh"
-
-namespace cg = cooperative_groups;
 
 constexpr int CT = 512;  // threads per CTA of the scan kernels
 constexpr int CI = 4;    // consecutive items per thread: a scan tile is CT*CI items
@@ -421,42 +417,6 @@ __global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, in
 // rule), so the products do not depend on which form ran.
 constexpr int SMALL_T = 1024;
 
-// CL > 1: the query runs on a thread-block cluster of CL CTAs instead of one CTA.  Each
-// level's parents are split into CL contiguous chunks; a chunk's exclusive prefix is its
-// CTA's scan plus the totals of the lower-ranked CTAs, read from their shared memory
-// (DSMEM) after a cluster barrier -- integer sums, so every prefix equals the one-CTA
-// scan's.  Three cluster barriers per level (totals, prefixes, scatter).
-template <int CL>
-__device__ __forceinline__ void csync()
-{
-    if constexpr (CL > 1) cg::this_cluster().sync();
-    else __syncthreads();
-}
-
-template <int CL>
-__device__ __forceinline__ unsigned crank()
-{
-    if constexpr (CL > 1) return cg::this_cluster().block_rank();
-    else return 0;
-}
-
-// sum of the cluster's per-CTA totals: ranks below `below`, and all of them
-template <int CL, typename T>
-__device__ __forceinline__ void cluster_offsets(T *s_tot, unsigned below, T *off, T *all)
-{
-    T o = vzero(*s_tot), a = vzero(*s_tot);
-    for (unsigned r = 0; r < (unsigned)CL; r++) {
-        T v;
-        if constexpr (CL > 1) v = *cg::this_cluster().map_shared_rank(s_tot, r);
-        else v = *s_tot;
-        if (r < below) o = vadd(o, v);
-        a = vadd(a, v);
-    }
-    *off = o;
-    *all = a;
-}
-
-template <int CL>
 __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4 *rec0, int4 *rec1, uint8_t *mask,
                                                         int4 *pre, int32_t *tA, int32_t *tB, int32_t *tK,
                                                         int64_t cap_segs, int32_t *seg_code, int32_t *seg_start,
@@ -464,58 +424,32 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
 {
     __shared__ int4 sw4[SMALL_T / 32];
     __shared__ V1 sw1[SMALL_T / 32];
-    __shared__ int4 s_tot;
-    __shared__ V1 s_htot;
-    __shared__ int4 s_off, s_all;
-    __shared__ V1 s_hoff, s_hall;
     pdl_wait();
     pdl_trigger();
-    const unsigned cr = crank<CL>();
-    if (cr == 0)
-        for (int i = threadIdx.x; i < 64; i += SMALL_T) cnt[i] = 0;
-    cull_clear(clr, cr * SMALL_T + threadIdx.x, (int64_t)CL * SMALL_T);
+    for (int i = threadIdx.x; i < 64; i += SMALL_T) cnt[i] = 0;
+    cull_clear(clr, threadIdx.x, SMALL_T);
     __syncthreads();
     int4 *rec[2] = {rec0, rec1};
     int cur = 0;
-    if (cr == 0) cull_init_body(g, l0, rec[cur], cnt);
-    csync<CL>();
+    cull_init_body(g, l0, rec[cur], cnt);
+    __syncthreads();
     const double T = cull_T(g);
     for (int l = l0; l < g.L; l++) {
         if (cnt[CNT_OVERFLOW]) return;
         const int n = clamp_n(cnt, l, g.cap);
-        const int chunk = (n + CL - 1) / CL;
-        const int b0 = min(n, (int)cr * chunk), b1 = min(n, b0 + chunk);
         const double *an = g.a_n2 + pyr_off(l + 1), *bn = g.b_n2 + pyr_off(l + 1);
-        // pass 1: child masks of this CTA's parents, their per-quadrant count total
-        int4 mine = make_int4(0, 0, 0, 0);
-        for (int t0 = b0; t0 < b1; t0 += SMALL_T * CI) {
-            const int tb = t0 + threadIdx.x * CI;
-            int4 csum = make_int4(0, 0, 0, 0);
-#pragma unroll
-            for (int i = 0; i < CI; i++) {
-                const int t = tb + i;
-                const uint32_t m = t < b1 ? cull_parent_mask(g, l, rec[cur][t], an, bn, T) : 0u;
-                if (t < b1) mask[t] = (uint8_t)m;
-                csum = vadd(csum, mask_counts(m));
-            }
-            int4 tot;
-            block_excl_scan<int4, SMALL_T>(csum, &tot, sw4);
-            mine = vadd(mine, tot);
-        }
-        if (threadIdx.x == 0) s_tot = mine;
-        csync<CL>();
-        if (threadIdx.x == 0) cluster_offsets<CL>(&s_tot, cr, &s_off, &s_all);
-        __syncthreads();
-        // pass 2: exclusive prefixes in task order (the cluster offset + this CTA's scan)
-        int4 carry = s_off;
-        for (int t0 = b0; t0 < b1; t0 += SMALL_T * CI) {
+        // masks + per-quadrant counts, exclusive int4 scan in task order
+        int4 carry = make_int4(0, 0, 0, 0);
+        for (int t0 = 0; t0 < n; t0 += SMALL_T * CI) {
             const int tb = t0 + threadIdx.x * CI;
             int4 c[CI];
+            uint32_t m[CI];
             int4 csum = make_int4(0, 0, 0, 0);
 #pragma unroll
             for (int i = 0; i < CI; i++) {
                 const int t = tb + i;
-                c[i] = mask_counts(t < b1 ? (uint32_t)mask[t] : 0u);
+                m[i] = t < n ? cull_parent_mask(g, l, rec[cur][t], an, bn, T) : 0u;
+                c[i] = mask_counts(m[i]);
                 csum = vadd(csum, c[i]);
             }
             int4 tot;
@@ -523,36 +457,36 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
 #pragma unroll
             for (int i = 0; i < CI; i++) {
                 const int t = tb + i;
-                if (t < b1) pre[t] = p;
+                if (t < n) {
+                    pre[t] = p;
+                    mask[t] = (uint8_t)m[i];
+                }
                 p = vadd(p, c[i]);
             }
             carry = vadd(carry, tot);
         }
-        if (cr == 0 && threadIdx.x == 0) {
-            const int4 all = s_all;
-            pre[n] = all;
-            const int total = all.x + all.y + all.z + all.w;
+        if (threadIdx.x == 0) {
+            pre[n] = carry;
+            const int total = carry.x + carry.y + carry.z + carry.w;
             cnt[l + 1] = total;
             if (total > g.cap) cnt[CNT_OVERFLOW] = 1;
         }
-        csync<CL>();
+        __syncthreads();
         if (cnt[CNT_OVERFLOW]) return;
         if (l + 1 == g.L) {
-            for (int t = b0 + threadIdx.x; t < b1; t += SMALL_T)
+            for (int t = threadIdx.x; t < n; t += SMALL_T)
                 cull_scatter_one<true>(g, rec[cur], mask, pre, t, rec[cur ^ 1], tA, tB, tK);
         } else {
-            for (int t = b0 + threadIdx.x; t < b1; t += SMALL_T)
+            for (int t = threadIdx.x; t < n; t += SMALL_T)
                 cull_scatter_one<false>(g, rec[cur], mask, pre, t, rec[cur ^ 1], nullptr, nullptr, nullptr);
         }
         cur ^= 1;
-        csync<CL>();
+        __syncthreads();
     }
     if (cnt[CNT_OVERFLOW]) return;
     const int n = clamp_n(cnt, g.L, g.cap);
-    const int chunk = (n + CL - 1) / CL;
-    const int b0 = min(n, (int)cr * chunk), b1 = min(n, b0 + chunk);
     if (l0 == g.L) {   // the init level is the leaf level: tasks straight from the records
-        for (int t = b0 + threadIdx.x; t < b1; t += SMALL_T) {
+        for (int t = threadIdx.x; t < n; t += SMALL_T) {
             const int4 r = rec[cur][t];
             const int i = morton_i(r.x), j = morton_j(r.x), k = r.y;
             tA[t] = g.a_slot[a_code(g, i, k)];
@@ -561,33 +495,23 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
         }
     }
     // segment heads (record r starts its group: r.z == t) -> {code, start, len}
-    int mine = 0;
-    for (int t = b0 + threadIdx.x; t < b1; t += SMALL_T) mine += rec[cur][t].z == t ? 1 : 0;
-    {
-        V1 tot;
-        block_excl_scan<V1, SMALL_T>(V1{mine}, &tot, sw1);
-        if (threadIdx.x == 0) s_htot = tot;
-    }
-    csync<CL>();
-    if (threadIdx.x == 0) cluster_offsets<CL>(&s_htot, cr, &s_hoff, &s_hall);
-    __syncthreads();
-    int carry = s_hoff.x;
-    for (int t0 = b0; t0 < b1; t0 += SMALL_T * CI) {
+    int carry = 0;
+    for (int t0 = 0; t0 < n; t0 += SMALL_T * CI) {
         const int tb = t0 + threadIdx.x * CI;
         int4 r[CI];
         int hs = 0;
 #pragma unroll
         for (int i = 0; i < CI; i++) {
             const int t = tb + i;
-            r[i] = t < b1 ? rec[cur][t] : make_int4(0, 0, -1, 0);
-            hs += (t < b1 && r[i].z == t) ? 1 : 0;
+            r[i] = t < n ? rec[cur][t] : make_int4(0, 0, -1, 0);
+            hs += (t < n && r[i].z == t) ? 1 : 0;
         }
         V1 tot;
         int sidx = carry + block_excl_scan<V1, SMALL_T>(V1{hs}, &tot, sw1).x;
 #pragma unroll
         for (int i = 0; i < CI; i++) {
             const int t = tb + i;
-            if (t < b1 && r[i].z == t) {
+            if (t < n && r[i].z == t) {
                 if (sidx < cap_segs) {
                     seg_code[sidx] = r[i].x;
                     seg_start[sidx] = t;
@@ -598,12 +522,10 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
         }
         carry += tot.x;
     }
-    if (cr == 0 && threadIdx.x == 0) {
-        const int all = s_hall.x;
-        cnt[CNT_NSEG] = all;
-        if (all > cap_segs) cnt[CNT_OVERFLOW] = 1;
+    if (threadIdx.x == 0) {
+        cnt[CNT_NSEG] = carry;
+        if (carry > cap_segs) cnt[CNT_OVERFLOW] = 1;
     }
-    csync<CL>();   // no CTA leaves while a peer may still read its shared memory
 }
 
 // ------------------------------------------------------------- host side
@@ -676,17 +598,6 @@ static bool cull_small_ok(spamm_ctx ctx, const Cull *cw, spamm_mat A)
     return false;
 }
 
-// nb >= 64: the small query on a cluster of CULL_CL CTAs (SPAMM_CULL_CLUSTER=0: one CTA)
-constexpr int CULL_CL = 8;
-static bool cull_cluster_mode()
-{
-    static const bool on = [] {
-        const char *e = getenv("SPAMM_CULL_CLUSTER");
-        return !(e && *e == '0');
-    }();
-    return on;
-}
-
 // Enqueue the whole query (no host sync).
 static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0,
                                  int r1, int transA, const CullClear *clear = nullptr)
@@ -701,28 +612,8 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     cudaStream_t s = ctx->stream;
     if (cull_small_ok(ctx, cw, A)) {
         cw->final_buf = (L - l0) & 1;
-        if (A->nb >= 64 && cull_cluster_mode()) {
-            // a cluster of CULL_CL CTAs (DSMEM prefix exchange), PDL as for the chain
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(CULL_CL);
-            cfg.blockDim = dim3(SMALL_T);
-            cfg.stream = s;
-            cudaLaunchAttribute at[2];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = CULL_CL;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[1].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = (ctx->comm == nullptr && pdl_enabled()) ? 2 : 1;
-            CK(cudaLaunchKernelEx(&cfg, k_cull_small<CULL_CL>, g, l0, cw->rec[0], cw->rec[1], cw->mask, cw->pre, cw->tA,
-                                  cw->tB, cw->tK, (int64_t)cw->cap_segs, cw->seg_code, cw->seg_start, cw->seg_len,
-                                  cw->counters, clr));
-        } else {
-            CK(launch_k(ctx, k_cull_small<1>, 1, SMALL_T, 0, g, l0, cw->rec[0], cw->rec[1], cw->mask, cw->pre, cw->tA,
-                        cw->tB, cw->tK, cw->cap_segs, cw->seg_code, cw->seg_start, cw->seg_len, cw->counters, clr));
-        }
+        CK(launch_k(ctx, k_cull_small, 1, SMALL_T, 0, g, l0, cw->rec[0], cw->rec[1], cw->mask, cw->pre, cw->tA, cw->tB,
+                    cw->tK, cw->cap_segs, cw->seg_code, cw->seg_start, cw->seg_len, cw->counters, clr));
         CKL(ctx);
         return SPAMM_OK;
     }
