@@ -401,11 +401,14 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
 // diag_fixup with the base slot read from the device (the X cull's segment count) and
 // caller-provided scratch (newslot [nb]); no allocation, no host round trip
 spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, double value, int32_t *newslot,
-                            int64_t *dcount);
+                            int64_t *dcount, const double *trace_part = nullptr, double *t_out = nullptr);
 spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value);
 // as diag_fixup without the host round trip: the count of appended blocks lands in
 // *dcount (device); the caller fetches it and sets H->nblk = nseg + count
-spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value, int64_t *dcount);
+// trace_part (nullable): the fill launch also forms t_k = (n - sum trace_part)/n -> *t_out
+// (trace_finish's arithmetic; single device)
+spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value, int64_t *dcount,
+                              const double *trace_part = nullptr, double *t_out = nullptr);
 // out[0..n) = the segments of `in` (nullable => 0..n-1), longest first (a schedule only)
 spamm_status lpt_order(spamm_ctx ctx, const int32_t *seg_len, const int32_t *in, int64_t n, int32_t *out);
 // scaled / stabilised NS map in place over X: coef <- {alpha, eps, sqrt(alpha)/2}(t)

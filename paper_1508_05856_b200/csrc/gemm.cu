@@ -532,12 +532,31 @@ __global__ void k_diag_assign(int32_t *slot_map, int32_t *coord, int nb, int r0,
     if (threadIdx.x == 0) *count_out = run;
 }
 
-__global__ void k_diag_fill(const int32_t *newslot, double *pool, int b, double value,
-                            double *leaf_n2)
+// trace_part != nullptr: CTA 0 also forms t = (n - sum_i trace_part[i]) / n exactly as
+// k_trace_finish does (256 threads, i strided by 256, then the halving tree) -- one launch
+// fewer per NS step (the trace partials are complete once the X GEMM is)
+__device__ __forceinline__ void trace_256(const double *part, int nb, double n, double *t_out)
+{
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 256) s += part[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *t_out = (n - sh[0]) / n;
+}
+
+__global__ void __launch_bounds__(256) k_diag_fill(const int32_t *newslot, double *pool, int b, double value,
+                                                   double *leaf_n2, const double *trace_part, int nb, double n,
+                                                   double *t_out)
 {
     pdl_wait();
     pdl_trigger();
     int i = blockIdx.x;
+    if (trace_part && i == 0) trace_256(trace_part, nb, n, t_out);
     int s = newslot[i];
     if (s < 0) return;
     double *d = pool + (int64_t)s * b * b;
@@ -557,7 +576,7 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
                 ctx->iscratch, (const int32_t *)nullptr, m->cap));
     CKL(ctx);
     CK(launch_k(ctx, k_diag_fill, m->nb, 256, 0, (const int32_t *)newslot, m->pool, m->b, value,
-                m->norm2 + pyr_off(m->L)));
+                m->norm2 + pyr_off(m->L), (const double *)nullptr, 0, 0.0, (double *)nullptr));
     CKL(ctx);
     int64_t h = 0;
     ST(fetch1(ctx, ctx->iscratch, &h, sizeof(int64_t)));
@@ -566,7 +585,8 @@ spamm_status diag_append(spamm_ctx ctx, spamm_mat m, int64_t base, double value,
     return SPAMM_OK;
 }
 
-spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value, int64_t *dcount)
+spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value, int64_t *dcount,
+                              const double *trace_part, double *t_out)
 {
     int32_t *newslot = dalloc<int32_t>(ctx, H->nb);
     if (!newslot) return set_err(ctx, SPAMM_ENOMEM, "diag fixup");
@@ -574,7 +594,7 @@ spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double v
                 (const int32_t *)nullptr, H->cap));
     CKL(ctx);
     CK(launch_k(ctx, k_diag_fill, H->nb, 256, 0, (const int32_t *)newslot, H->pool, H->b, value,
-                H->norm2 + pyr_off(H->L)));
+                H->norm2 + pyr_off(H->L), trace_part, H->nb, (double)H->n, t_out));
     CKL(ctx);
     dev_free(ctx, newslot, sizeof(int32_t) * H->nb);
     H->nblk = nseg;   // provisional until the caller has fetched *dcount
@@ -582,13 +602,13 @@ spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double v
 }
 
 spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, double value, int32_t *newslot,
-                            int64_t *dcount)
+                            int64_t *dcount, const double *trace_part, double *t_out)
 {
     CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, (int64_t)0, newslot,
                 dcount, nseg_dev, H->cap));
     CKL(ctx);
     CK(launch_k(ctx, k_diag_fill, H->nb, 256, 0, (const int32_t *)newslot, H->pool, H->b, value,
-                H->norm2 + pyr_off(H->L)));
+                H->norm2 + pyr_off(H->L), trace_part, H->nb, (double)H->n, t_out));
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -602,20 +622,11 @@ spamm_status diag_fixup(spamm_ctx ctx, spamm_mat H, int64_t nseg, double value)
 }
 
 // t = (n - sum_i trace_part[i]) / n, fixed-order single-CTA reduction
-__global__ void k_trace_finish(const double *part, int nb, double n, double *t_out)
+__global__ void __launch_bounds__(256) k_trace_finish(const double *part, int nb, double n, double *t_out)
 {
     pdl_wait();
     pdl_trigger();
-    __shared__ double sh[256];
-    double s = 0.0;
-    for (int i = threadIdx.x; i < nb; i += 256) s += part[i];
-    sh[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *t_out = (n - sh[0]) / n;
+    trace_256(part, nb, n, t_out);
 }
 
 spamm_status trace_finish(spamm_ctx ctx, const double *trace_part, int nb, int64_t n, double *t_out)

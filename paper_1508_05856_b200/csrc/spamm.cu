@@ -308,7 +308,7 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
 // trip, their count lands there and the caller sets C->nblk after its next fetch.
 static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int epi,
                             double *trace_part, spamm_mat *C, int transA = 0, double alpha = 1.0,
-                            bool cull_done = false, int64_t *diag_dcount = nullptr)
+                            bool cull_done = false, int64_t *diag_dcount = nullptr, double *t_out = nullptr)
 {
     cw->alpha = alpha;
     if (transA && A->dist)
@@ -366,7 +366,8 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
         m->nblk = cw->nsegs;
         // absent diagonal blocks of X: H_ii = 1.5 I (plain map) or X_ii = 0 (scaled map,
         // mapped with the other blocks once alpha(t_k), eps(t_k) are known)
-        if (epi == EPI_NS_H && diag_dcount) st = diag_fixup_async(ctx, m, cw->nsegs, 1.5, diag_dcount);
+        if (epi == EPI_NS_H && diag_dcount)
+            st = diag_fixup_async(ctx, m, cw->nsegs, 1.5, diag_dcount, t_out ? trace_part : nullptr, t_out);
         else if (epi == EPI_NS_H) st = diag_fixup(ctx, m, cw->nsegs, 1.5);
         if (epi == EPI_NS_X) st = diag_fixup(ctx, m, cw->nsegs, 0.0);
     }
@@ -437,10 +438,11 @@ static spamm_status ns_step_batched(spamm_ctx ctx, spamm_mat Y, spamm_mat Z, dou
     const int nb = Y->nb;
     int64_t *ddiag = ctx->iscratch + 1;
     spamm_mat H = nullptr;
+    // plain map: the trace t_k rides on the diagonal fix-up's launch
     spamm_status st = product(ctx, ctx->cw[0], Z, Y, tau, map ? EPI_NS_X : EPI_NS_H, trace_part, &H, 0, 1.0,
-                              fs && fs->x_ready, map ? nullptr : ddiag);
+                              fs && fs->x_ready, map ? nullptr : ddiag, map ? nullptr : ctx->dscratch);
     const int64_t nseg = ctx->cw[0]->nsegs;
-    if (!st) st = trace_finish(ctx, trace_part, nb, Y->n, ctx->dscratch);
+    if (!st && map) st = trace_finish(ctx, trace_part, nb, Y->n, ctx->dscratch);
     if (!st && map) st = ns_scaled_map(ctx, H, ctx->dscratch, ctx->dscratch + 8);
     if (!st && map) st = norms_finish(ctx, H);
     if (!st && stats) stats[0] = ctx->cw[0]->stats;
@@ -760,9 +762,8 @@ static spamm_status graph_step(spamm_ctx ctx, NsGraph *g, spamm_mat Y, spamm_mat
     ST(cull_enqueue_fixed(ctx, c0, Z, Y, g->tau, &clr));
     c0->alpha = 1.0;
     ST(gemm_run(ctx, c0, Z, Y, nullptr, H, EPI_NS_H, g->trace_part, nullptr, 0, 0, 0, true));
-    ST(diag_fixup_dev(ctx, H, c0->counters + CNT_NSEG, 1.5, g->newslot, g->hadd));
+    ST(diag_fixup_dev(ctx, H, c0->counters + CNT_NSEG, 1.5, g->newslot, g->hadd, g->trace_part, ctx->dscratch));
     ST(pyramid_build(ctx, H));
-    ST(trace_finish(ctx, g->trace_part, nb, Y->n, ctx->dscratch));
     // Y' = Y (x)_tau_s H on the main stream || Z' = H (x)_tau Z on the side stream: the two
     // culls always; with split, the GEMMs (each on half the SMs) and pyramids as well
     const bool split = graph_split(nb);

@@ -49,10 +49,24 @@ static int poison_mode()
     return m;
 }
 
+// The context's own pool (no allocator given): requests of 32 MiB and more are rounded up
+// to 4 size classes per octave (<= 25 % slack).  The NS iterates grow a little every step
+// (fill-in), so an exact-size request never fits a freed block and the pool would map new
+// memory for every product (C3: 335 vs 232 ms per run); with classes, freed iterates serve
+// the next step's requests.
+static size_t pool_class(size_t bytes)
+{
+    if (bytes < ((size_t)32 << 20)) return bytes;
+    int e = 63 - __builtin_clzll((unsigned long long)bytes);
+    const size_t q = (size_t)1 << (e - 2);
+    return (bytes + q - 1) & ~(q - 1);
+}
+
 void *dev_alloc(spamm_ctx ctx, size_t bytes)
 {
     bytes = (bytes + 255) & ~size_t(255);
     void *p = nullptr;
+    if (!ctx->has_alloc) bytes = pool_class(bytes);
     if (ctx->has_alloc) {
         p = ctx->alloc.alloc(bytes, (void *)ctx->stream, ctx->alloc.user);
     } else if ((ctx->pool ? cudaMallocFromPoolAsync(&p, bytes, ctx->pool, ctx->stream)
@@ -287,8 +301,12 @@ __global__ void k_build_scatter(BlockSrc src, int64_t count, const int32_t *slot
 
 // Pyramid: each CTA reduces 4^LV consecutive entries of level `lf` into levels
 // lf-1 .. lf-LV (fixed order (c0+c1)+(c2+c3)).
+// tail > 0: the last CTA to finish (a counter in the root level's padding, norm2[1..3],
+// which is zero between uses) also forms the `tail` levels above lf - levels from the
+// values the other CTAs stored -- one launch instead of two, the same (c0 + c1) + (c2 + c3)
+// per node, so the same bits.
 template <int LV>
-__global__ void k_pyramid(double *norm2, int lf, int levels)
+__global__ void k_pyramid(double *norm2, int lf, int levels, int tail)
 {
     pdl_wait();
     pdl_trigger();
@@ -318,6 +336,29 @@ __global__ void k_pyramid(double *norm2, int lf, int levels)
         }
         __syncthreads();
     }
+    if (tail > 0) {
+        __shared__ unsigned s_last;
+        unsigned long long *done = reinterpret_cast<unsigned long long *>(norm2 + 1);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(done, 1ull) == gridDim.x - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        const int top = lf - levels;
+        for (int l = top - 1; l >= top - tail; l--) {
+            const double *c = norm2 + pyr_off(l + 1);
+            double *dst = norm2 + pyr_off(l);
+            for (int64_t i = threadIdx.x; i < ((int64_t)1 << (2 * l)); i += blockDim.x) {
+                const double c0 = __ldcg(c + 4 * i), c1 = __ldcg(c + 4 * i + 1), c2 = __ldcg(c + 4 * i + 2),
+                             c3 = __ldcg(c + 4 * i + 3);
+                dst[i] = (c0 + c1) + (c2 + c3);
+            }
+            __threadfence_block();
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) *done = 0ull;   // the padding is zero again
+    }
 }
 
 static spamm_status pyramid_kernels(spamm_ctx ctx, spamm_mat m)
@@ -325,17 +366,18 @@ static spamm_status pyramid_kernels(spamm_ctx ctx, spamm_mat m)
     int lf = m->L;
     while (lf > 0) {
         int lv = lf >= 5 ? 5 : lf;
+        const int rest = lf - lv, tail = rest <= 5 ? rest : 0;   // the last CTA finishes <= 5 levels
         int64_t cnt = int64_t(1) << (2 * lf);
         int grid = cdiv(cnt, int64_t(1) << (2 * lv));
         switch (lv) {
-        case 5: CK(launch_k(ctx, k_pyramid<5>, grid, 256, 0, m->norm2, lf, 5)); break;
-        case 4: CK(launch_k(ctx, k_pyramid<4>, grid, 256, 0, m->norm2, lf, 4)); break;
-        case 3: CK(launch_k(ctx, k_pyramid<3>, grid, 64, 0, m->norm2, lf, 3)); break;
-        case 2: CK(launch_k(ctx, k_pyramid<2>, grid, 16, 0, m->norm2, lf, 2)); break;
-        default: CK(launch_k(ctx, k_pyramid<1>, grid, 4, 0, m->norm2, lf, 1)); break;
+        case 5: CK(launch_k(ctx, k_pyramid<5>, grid, 256, 0, m->norm2, lf, 5, tail)); break;
+        case 4: CK(launch_k(ctx, k_pyramid<4>, grid, 256, 0, m->norm2, lf, 4, tail)); break;
+        case 3: CK(launch_k(ctx, k_pyramid<3>, grid, 64, 0, m->norm2, lf, 3, tail)); break;
+        case 2: CK(launch_k(ctx, k_pyramid<2>, grid, 16, 0, m->norm2, lf, 2, tail)); break;
+        default: CK(launch_k(ctx, k_pyramid<1>, grid, 4, 0, m->norm2, lf, 1, tail)); break;
         }
         CKL(ctx);
-        lf -= lv;
+        lf -= lv + tail;
     }
     return SPAMM_OK;
 }
