@@ -417,13 +417,21 @@ __global__ void __launch_bounds__(CT) k_cull_segments(const int4 *rec, int L, in
 // rule), so the products do not depend on which form ran.
 constexpr int SMALL_T = 1024;
 
-__global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4 *rec0, int4 *rec1, uint8_t *mask,
-                                                        int4 *pre, int32_t *tA, int32_t *tB, int32_t *tK,
+// a level of up to SMALL_STAGE parents keeps its prefixes and masks in shared memory, so
+// the scatter's reads of pre[t], pre[r.z], pre[r.w] and mask[t] are not global round trips
+constexpr int SMALL_STAGE = 8191;
+constexpr size_t SMALL_SMEM = (SMALL_STAGE + 1) * sizeof(int4) + (SMALL_STAGE + 1);
+
+__global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4 *rec0, int4 *rec1, uint8_t *mask_g,
+                                                        int4 *pre_g, int32_t *tA, int32_t *tB, int32_t *tK,
                                                         int64_t cap_segs, int32_t *seg_code, int32_t *seg_start,
                                                         int32_t *seg_len, int32_t *cnt, CullClear clr)
 {
     __shared__ int4 sw4[SMALL_T / 32];
     __shared__ V1 sw1[SMALL_T / 32];
+    extern __shared__ __align__(16) unsigned char small_smem[];
+    int4 *const pre_s = reinterpret_cast<int4 *>(small_smem);
+    uint8_t *const mask_s = small_smem + (SMALL_STAGE + 1) * sizeof(int4);
     pdl_wait();
     pdl_trigger();
     for (int i = threadIdx.x; i < 64; i += SMALL_T) cnt[i] = 0;
@@ -438,6 +446,9 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
         if (cnt[CNT_OVERFLOW]) return;
         const int n = clamp_n(cnt, l, g.cap);
         const double *an = g.a_n2 + pyr_off(l + 1), *bn = g.b_n2 + pyr_off(l + 1);
+        const bool staged = n <= SMALL_STAGE;
+        int4 *const pre = staged ? pre_s : pre_g;
+        uint8_t *const mask = staged ? mask_s : mask_g;
         // masks + per-quadrant counts, exclusive int4 scan in task order
         int4 carry = make_int4(0, 0, 0, 0);
         for (int t0 = 0; t0 < n; t0 += SMALL_T * CI) {
@@ -612,8 +623,12 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     cudaStream_t s = ctx->stream;
     if (cull_small_ok(ctx, cw, A)) {
         cw->final_buf = (L - l0) & 1;
-        CK(launch_k(ctx, k_cull_small, 1, SMALL_T, 0, g, l0, cw->rec[0], cw->rec[1], cw->mask, cw->pre, cw->tA, cw->tB,
-                    cw->tK, cw->cap_segs, cw->seg_code, cw->seg_start, cw->seg_len, cw->counters, clr));
+        static std::atomic<uint64_t> configured{0};
+        CK(once_per_device(configured, ctx->device, [&]() {
+            return cudaFuncSetAttribute(k_cull_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM);
+        }));
+        CK(launch_k(ctx, k_cull_small, 1, SMALL_T, SMALL_SMEM, g, l0, cw->rec[0], cw->rec[1], cw->mask, cw->pre, cw->tA,
+                    cw->tB, cw->tK, cw->cap_segs, cw->seg_code, cw->seg_start, cw->seg_len, cw->counters, clr));
         CKL(ctx);
         return SPAMM_OK;
     }
