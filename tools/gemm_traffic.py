@@ -51,7 +51,7 @@ out = dict(kernel=f"k_leaf_gemm<64,...> ({cfg}, NS iteration k={k}: X, Y', Z' la
            note="dram read ~= the compulsory unique operand blocks; write = the output blocks; "
                 "the operand stream is served from L2")
 json.dump(out, open(os.path.join("profiles", f"gemm_traffic_{cfg}.json"), "w"), indent=1)
-json.dump(r, open(os.path.join("profiles", f"r01_gemm_{cfg}_k{k}_full.json"), "w"), indent=1)
+json.dump(r, open(os.path.join("profiles", os.environ.get("SPAMM_ROUND", "r02"), f"gemm_{cfg}_k{k}_full.json"), "w"), indent=1)
 for x in launches:
     print(f"{x['kernel'][:48]:48s} tasks {x['tasks']:8d} {x['time_s'] * 1e3:8.3f} ms {x['tflops']:6.2f} TF "
           f"DMMA active {x['dmma_active_frac']:.3f} DRAM {x['dram_total'] / 1e9:6.2f} GB L2 hit {x['l2_hit_pct']:.1f}%")
