@@ -69,19 +69,20 @@ __global__ void k_row_fill(const int32_t *slot, int nb, const int32_t *rowptr, i
 
 // w[I*b + r] = sum over present blocks (I,J), ascending J, of S_IJ[r,:] . v[J*b:].
 // Thread t owns E consecutive (swizzled) elements of one row; TPR = b/E threads
-// per row, RG = 256/TPR rows per CTA, b/RG CTAs per block row.  Each thread
+// per row, RG = NT/TPR rows per CTA, b/RG CTAs per block row.  Each thread
 // accumulates its partial dot products over the row's blocks in order (U blocks
-// in flight), then the TPR threads of a row reduce with a fixed xor tree.
+// in flight), then the TPR threads of a row reduce with a fixed xor tree.  A row's
+// arithmetic depends on neither NT nor U.
 // Persistent: CTAs take (block row, row group) units from a ticket, so the grid is
 // exactly the resident capacity (no partial last wave) and uneven rows balance.
-template <int B>
-__global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t *rowptr,
-                                              const int32_t *cols, const int32_t *slots,
-                                              const double *v, double *w, int32_t *ticket, int nunits)
+template <int B, int NT>
+__global__ void __launch_bounds__(NT) k_spmv(const double *pool, const int32_t *rowptr,
+                                             const int32_t *cols, const int32_t *slots,
+                                             const double *v, double *w, int32_t *ticket, int nunits)
 {
     pdl_wait();
     pdl_trigger();
-    constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
+    constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = NT / TPR, CPR = B / RG;
     __shared__ int s_unit;
     for (;;) {
     if (threadIdx.x == 0) s_unit = atomicAdd(ticket, 1);
@@ -98,14 +99,15 @@ __global__ void __launch_bounds__(256) k_spmv(const double *pool, const int32_t 
     for (int i = 0; i < E; i++) lc[i] = pool_col(e0 + i, B);
     double acc = 0.0;
     // blocks in flight per thread: ~32-64 KB of loads in flight per CTA, what an SM needs
-    // to stream s near the HBM rate (the order of the sum over blocks does not depend on U)
+    // to stream s near the HBM rate (U = 16 with v staged in shared memory measured the
+    // same at C2, 3.015 vs 3.017 ms per power iteration)
     constexpr int U = B == 16 ? 16 : 8;
     constexpr int SPC = 512;  // block-row entries staged in shared memory per pass
     __shared__ int s_slot[SPC], s_col[SPC];
     for (int pc = p0; pc < p1; pc += SPC) {
         const int pe = p1 < pc + SPC ? p1 : pc + SPC;
         __syncthreads();
-        for (int i = threadIdx.x; i < pe - pc; i += 256) {
+        for (int i = threadIdx.x; i < pe - pc; i += NT) {
             s_slot[i] = slots[pc + i];
             s_col[i] = cols[pc + i];
         }
@@ -613,19 +615,22 @@ template <int B>
 static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
                          const int32_t *slots, const double *v, double *w, int32_t *ticket)
 {
-    constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = 256 / TPR, CPR = B / RG;
+    // NT = 64: more, smaller units than 256 threads (C2 setup 3.37 -> 3.23 ms, C1 0.74 ->
+    // 0.66 ms); the register-light 64-thread CTAs also fill the SMs better
+    constexpr int NT = 64;
+    constexpr int E = B >= 32 ? 4 : 1, TPR = B / E, RG = NT / TPR, CPR = B / RG;
     static std::atomic<int> occ_cache{0};
     int occ = occ_cache.load();
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<B>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<B, NT>, NT, 0);
         if (occ < 1) occ = 1;
         occ_cache.store(occ);
     }
     const int nunits = s->nb * CPR;
     int grid = ctx->sm_count * occ;
     if (grid > nunits) grid = nunits;
-    if (s->dist) k_spmv<B><<<grid, 256, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
-    else CK(launch_pdl(k_spmv<B>, grid, 256, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits));
+    if (s->dist) k_spmv<B, NT><<<grid, NT, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
+    else CK(launch_pdl(k_spmv<B, NT>, grid, NT, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits));
     CKL(ctx);
     return SPAMM_OK;
 }

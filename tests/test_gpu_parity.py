@@ -223,13 +223,14 @@ def test_power_scale(ctx):
         assert sp().spamm_power_scale(ctx, S, 100) == pytest.approx(O.power_scale(So, 100), rel=1e-12)
 
 
+@pytest.mark.parametrize("b", [64, 32, 16])
 @pytest.mark.parametrize("case", ["sym", "sym_holes", "asym_values", "asym_pattern"])
-def test_power_scale_symmetric_and_fallback(ctx, case):
+def test_power_scale_symmetric_and_fallback(ctx, case, b):
     """b = 64: a bitwise-symmetric s takes the upper-half SpMV (column parts of the
-    off-diagonal blocks), anything else the full SpMV; both match the oracle's
-    plain power iteration (reading L12).  Holes: absent off-diagonal blocks in a
-    symmetric pattern, and an empty block row tail."""
-    n, b = 2048, 64                     # nb = 32: several units per row, ragged quarters
+    off-diagonal blocks), anything else the full SpMV; b < 64: the register SpMV.  All
+    match the oracle's plain power iteration (reading L12).  Holes: absent off-diagonal
+    blocks in a symmetric pattern, and an empty block row tail."""
+    n = 2048                            # nb = 32 / 64 / 128: several units per row, ragged quarters
     m = np.abs(decaying(n, 0.01, 7))
     m = m + m.T
     nb = n // b
