@@ -44,6 +44,21 @@ def build_debug(force: bool = False, verbose: bool = False) -> str:
     return build(force, verbose, lib=LIB_DEBUG, extra=["-DSPAMM_DEBUG"])
 
 
+LIB_CLOCKS = os.path.join(HERE, "libspamm_b200_clocks.so")
+
+
+def build_clocks(force: bool = False, verbose: bool = False) -> str:
+    """Diagnostic variant: the leaf GEMM's consumer warps count the cycles they wait for
+    stages and queue entries (tools/gemm_clocks.py; select it with SPAMM_LIB=<path>)."""
+    return build(force, verbose, lib=LIB_CLOCKS, extra=["-DSPAMM_GEMM_CLOCKS"])
+
+
+def build_variant(name: str, defines, force: bool = False) -> str:
+    """An experimental variant (extra -D flags) built to libspamm_b200_<name>.so for A/B
+    timing with SPAMM_LIB."""
+    return build(force, lib=os.path.join(HERE, f"libspamm_b200_{name}.so"), extra=[f"-D{d}" for d in defines])
+
+
 def build(force: bool = False, verbose: bool = False, lib: str = LIB, extra=()) -> str:
     if not force and up_to_date(lib):
         return lib

@@ -51,6 +51,27 @@ struct GemmArgs {
     int nb;
 };
 
+#ifdef SPAMM_GEMM_CLOCKS
+// diagnostic build only (tools/gemm_clocks.py): consumer-warp cycle accounting
+// [0] loop total, [1] waiting for a stage (full), [2] waiting for a queue entry,
+// [3] segment boundaries (map, partials, deposit), [4] tasks, [5] segments, [6] of [3]: the
+// map and partials, [7] of [3]: waiting for the epilogue warp to release the tile
+__device__ unsigned long long g_gemm_clk[8];
+extern "C" int spamm_debug_gemm_clocks(unsigned long long *out, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_gemm_clk, sizeof(g_gemm_clk));
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_gemm_clk, z, sizeof(z));
+    }
+    return (int)cudaDeviceSynchronize();
+}
+#define CLK(...) __VA_ARGS__
+#else
+#define CLK(...)
+#endif
+
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b)
 {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -65,13 +86,42 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
 //     smem queue, and per task waits for a free stage, then TMA-bulk-copies the
 //     A and B tiles (b*b*8 bytes each, pre-swizzled in the pool) into it.
 //   warps 0..CW-1 (consumers): per task wait for the stage, load fragments,
-//     issue DMMAs into register accumulators, release the stage; at the end
-//     of a segment run the fused epilogue.  The producer runs ahead across
-//     segment boundaries, so the next segment's tiles load during an epilogue.
+//     issue DMMAs into register accumulators, release the stage; at the end of a
+//     segment apply the value map (H = 1.5 delta - 0.5 X, alpha), form their share
+//     of ||C_ij||^2 (and tr X_ii) in short FMA chains, deposit values (pool layout)
+//     and partial in the smem epilogue tile and go on to the next segment.
+//   warps CW+1 .. CW+EW (epilogue): copy the deposited tile to the pool with
+//     contiguous 16-byte stores; the first also sums the consumers' partials in a
+//     fixed order (deterministic) and writes the block's metadata.
+// The consumers issue no global stores, shuffle trees or cross-warp hand-offs, so
+// the DMMA pipe keeps running across segment boundaries.  Measured on the C5 k = 8
+// products (4.6 tasks per segment; tools/gemm_clocks.py): the whole epilogue in the
+// consumer warps, interleaved with the next segment's first task, took 4.2 % of their
+// cycles + 0.9 % at the boundary; here the boundary is ~3.8 %.  EW = 2 measured best
+// (NS step GEMM 59.61 ms against 59.98 before, EW = 1: 59.65, EW = 4: 60.02); a single
+// epilogue warp that also did the map and norms fell behind (the FP64 pipe is busy with
+// DMMAs: 10.7 % of the consumers' cycles waiting for the tile), and a TMA bulk store of
+// the tile needs a proxy fence in every consumer thread (5.6 % at the boundary).
 // TA = 1: the left operand is A^T (single channel, §8(f) f2): the A tile is read
 // with the column pattern of the B fragments (A^T[m][k] = A[k][m]).
+template <int B, int CW, int STAGES>
+struct GemmSmem {
+    static constexpr int TILE = B * B;
+    static constexpr int QN = 4;   // segment-queue depth (producer -> consumers)
+    // doubles: STAGES x {A, B} tiles, the epilogue tile, the consumers' per-lane ||.||^2
+    // partials and per-warp trace partials; then the barriers, the queue and the record
+    static constexpr int ETR = (CW + 1) & ~1;   // tr partials, padded to keep 16-byte alignment
+    static constexpr size_t bytes = sizeof(double) * ((2 * STAGES + 1) * TILE + 32 * CW + ETR) +
+                                    sizeof(uint64_t) * (2 * STAGES + 2 * QN + 2) + sizeof(int4) * (QN + 1);
+};
+
+#ifndef SPAMM_EPI_WARPS
+#define SPAMM_EPI_WARPS 2
+#endif
+constexpr int EW = SPAMM_EPI_WARPS;   // epilogue warps
+
 template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
-__global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
+__global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
 {
     static_assert(WM * WN == CW, "warp grid");
     constexpr bool STORE = EPI == EPI_STORE || EPI == EPI_STORE_SCALED;
@@ -80,15 +130,18 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
     constexpr int TILE = B * B;
     constexpr uint32_t TILE_BYTES = TILE * 8;
     extern __shared__ __align__(1024) double smem[];
-    constexpr int QN = 4;  // segment-queue depth (producer -> consumers)
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + 2 * STAGES * TILE);
+    constexpr int QN = GemmSmem<B, CW, STAGES>::QN;
+    double *ebuf = smem + 2 * STAGES * TILE;                  // the epilogue tile (pool layout)
+    double *ess = ebuf + TILE;                                // [CW][32] lanes' ||C_ij||^2 partials
+    double *etr = ess + 32 * CW;                              // [CW] warps' tr partials (diagonal blocks)
+    uint64_t *full = reinterpret_cast<uint64_t *>(etr + GemmSmem<B, CW, STAGES>::ETR);
     uint64_t *empty = full + STAGES;
     uint64_t *qfull = empty + STAGES;
     uint64_t *qempty = qfull + QN;
-    int4 *segq = reinterpret_cast<int4 *>(qempty + QN);     // {seg, len, code, -} per queue entry
-    constexpr int RS = 2 * QN;                                // epilogue reduction slots (> QN)
-    double *red = reinterpret_cast<double *>(segq + QN);      // [RS][2 (ss,tr)][CW]
-    int *rcnt = reinterpret_cast<int *>(red + RS * 2 * CW);   // [RS] warps done per slot
+    uint64_t *efull = qempty + QN;                            // tile deposited (CW arrivals)
+    uint64_t *eempty = efull + 1;                             // tile stored by the epilogue warp
+    int4 *segq = reinterpret_cast<int4 *>(eempty + 1);        // {seg, len, code, -} per queue entry
+    int4 *erec = segq + QN;                                   // {seg, code} of the deposited tile
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pdl_trigger();   // the epilogue-side kernels that follow may stage their launch now
@@ -101,7 +154,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
             mbar_init(&qfull[q], 1);
             mbar_init(&qempty[q], CW);
         }
-        for (int r = 0; r < RS; r++) rcnt[r] = 0;
+        mbar_init(efull, CW);
+        mbar_init(eempty, EW);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -167,6 +221,58 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
         return;
     }
 
+    if (warp > CW) {
+        // ------------------------------------------------------- epilogue
+        // EW warps copy the deposited tile to the pool (16-byte chunks lane + 32 (ew + EW i):
+        // contiguous 512-byte stores per warp instruction); warp 0 of them also sums the
+        // consumers' ||C_ij||^2 partials (lane l: lane l of every consumer warp in warp order,
+        // then a fixed xor tree; tr over the warps) and writes the block's metadata.
+        const int ew = warp - CW - 1;
+        uint32_t eph = 0;
+        const double2 *eb2 = reinterpret_cast<const double2 *>(ebuf);
+        for (;;) {
+            mbar_wait(efull, eph);
+            eph ^= 1;
+            const int4 rec = *erec;
+            if (rec.x < 0) break;
+            const int seg = rec.x;
+            const uint32_t code = (uint32_t)rec.y;
+            SPAMM_ASSERT(seg >= 0 && seg < g.c_cap);
+            double2 *dst = reinterpret_cast<double2 *>(g.c_pool + (int64_t)seg * TILE);
+            constexpr int NCH = TILE / 2 / 32 / EW;   // chunks per lane
+            constexpr int NU = NCH < 8 ? NCH : 8;     // loads in flight
+#pragma unroll 1
+            for (int i0 = 0; i0 < NCH; i0 += NU) {
+                double2 v[NU];
+#pragma unroll
+                for (int j = 0; j < NU; j++) v[j] = eb2[lane + 32 * (ew + EW * (i0 + j))];
+#pragma unroll
+                for (int j = 0; j < NU; j++) dst[lane + 32 * (ew + EW * (i0 + j))] = v[j];
+            }
+            double ss = 0.0, tr = 0.0;
+            const int I = morton_i(code), J = morton_j(code);
+            if (ew == 0) {
+#pragma unroll
+                for (int w = 0; w < CW; w++) ss += ess[32 * w + lane];
+                if (!STORE && I == J)
+                    for (int w = 0; w < CW; w++) tr += etr[w];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(eempty);   // this warp's reads of the tile are done
+            if (ew == 0) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                if (lane == 0) {
+                    g.c_leaf_n2[code] = ss;
+                    g.c_coord[seg] = (int32_t)code;
+                    g.c_slot[code] = seg;
+                    if (!STORE && I == J) g.trace_part[I] = tr;
+                }
+            }
+        }
+        return;
+    }
+
     // ----------------------------------------------------------- consumers
     const int g8 = lane >> 2, t4 = lane & 3;
     const int m0 = (warp / WN) * TM, n0 = (warp % WN) * TN;
@@ -193,105 +299,14 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
         for (int s = 0; s < 4; s++) boff[nf][s] = (4 * t4 + s) * B + ((((col >> 1) ^ ((t4 << 1) | (s & 1)))) << 1) + (col & 1);
     }
 
-    // Deferred epilogue: a segment's accumulators are parked in pacc and its epilogue
-    // (value map, ||C_ij||^2 / tr partials, stores, shuffle reduction) runs in NKC
-    // slices interleaved with the kc chunks of the NEXT segment's first task, so the
-    // two warps of an SMSP keep issuing DMMAs instead of both idling in the epilogue.
-    constexpr int NKC = B / 16;
-    double pacc[MF][NF][2];
-    int pseg = -1, pslot = 0;
-    uint32_t pcode = 0;
-    double pss = 0.0, ptr = 0.0;
-    // slice kc of the pending epilogue (kc = 0 also maps the values and forms the partials)
-    auto epi_slice = [&](int kc) {
-        const int I = morton_i(pcode), J = morton_j(pcode);
-        const bool diag = (I == J);
-        if (kc == 0) {
-            pss = 0.0;
-            ptr = 0.0;
-#pragma unroll
-            for (int mf = 0; mf < MF; mf++)
-#pragma unroll
-                for (int nf = 0; nf < NF; nf++) {
-                    const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
-                    double y0 = pacc[mf][nf][0], y1 = pacc[mf][nf][1];
-                    if (EPI == EPI_STORE_SCALED) {   // the fused final unscale of an NS run
-                        y0 *= g.alpha;
-                        y1 *= g.alpha;
-                    }
-                    if (!STORE) {
-                        if (diag && r == c) ptr += y0;
-                        if (diag && r == c + 1) ptr += y1;
-                    }
-                    if (EPI == EPI_NS_H) {
-                        // H = 1/2 (3 delta - X) written as 1.5 delta - 0.5 x (the 1/2 is exact)
-                        const double d0 = (diag && r == c) ? 1.5 : 0.0, d1 = (diag && r == c + 1) ? 1.5 : 0.0;
-                        y0 = d0 - 0.5 * y0;
-                        y1 = d1 - 0.5 * y1;
-                    }
-                    pss = fma(y0, y0, pss);
-                    pss = fma(y1, y1, pss);
-                    pacc[mf][nf][0] = y0;
-                    pacc[mf][nf][1] = y1;
-                }
-        }
-        SPAMM_ASSERT(pseg >= 0 && pseg < g.c_cap);
-        double *dst = g.c_pool + (int64_t)pseg * TILE;
-#pragma unroll
-        for (int mf = 0; mf < MF; mf++) {
-            if (mf % NKC != kc) continue;
-#pragma unroll
-            for (int nf = 0; nf < NF; nf++) {
-                const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
-                *reinterpret_cast<double2 *>(dst + r * B + ((((c >> 1) ^ swz(r))) << 1)) =
-                    make_double2(pacc[mf][nf][0], pacc[mf][nf][1]);
-            }
-        }
-        // xor-tree levels 16, 8, 4, 2, 1: level i in slice min(i, NKC - 1); the trace
-        // partials only on diagonal blocks (warp-uniform branch: ~1 segment in 100 at C5)
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            if ((i < NKC - 1 ? i : NKC - 1) != kc) continue;
-            const int o = 16 >> i;
-            pss += __shfl_xor_sync(0xffffffffu, pss, o);
-            if (!STORE && diag) ptr += __shfl_xor_sync(0xffffffffu, ptr, o);
-        }
-    };
-    // after the last slice: deposit the warp's partials; the last warp of the CTA to
-    // arrive sums the CW partials in warp order (deterministic) and writes the block's
-    // metadata.  No CTA barrier; warps drift apart by < QN segments (queue entries are
-    // released only when every warp has taken them) and a segment's deposit happens
-    // before its warp takes the segment after next, so RS = 2 QN slots are never
-    // reused early.
-    auto epi_deposit = [&]() {
-        if (lane == 0) {
-            double *rp = red + pslot * 2 * CW;
-            rp[warp] = pss;
-            rp[CW + warp] = ptr;
-            __threadfence_block();
-            if (atomicAdd(&rcnt[pslot], 1) == CW - 1) {
-                __threadfence_block();
-                double s2 = 0.0, t2 = 0.0;
-#pragma unroll
-                for (int w = 0; w < CW; w++) {
-                    s2 += *(volatile double *)&rp[w];
-                    t2 += *(volatile double *)&rp[CW + w];
-                }
-                rcnt[pslot] = 0;
-                const int I = morton_i(pcode), J = morton_j(pcode);
-                g.c_leaf_n2[pcode] = s2;
-                g.c_coord[pseg] = (int32_t)pcode;
-                g.c_slot[pcode] = pseg;
-                if (!STORE && I == J) g.trace_part[I] = t2;
-            }
-        }
-    };
-
     int stage = 0, q = 0;
-    uint32_t phase = 0, qphase = 0;
-    int slot = 0;
+    uint32_t phase = 0, qphase = 0, ephase = 0;
+    CLK(unsigned long long c_full = 0, c_q = 0, c_bnd = 0, n_task = 0, n_seg = 0, c_map = 0, c_ew = 0;
+        const unsigned long long c_start = clock64();)
     for (;;) {
+        CLK(unsigned long long c0 = clock64();)
         mbar_wait(&qfull[q], qphase);
+        CLK(c_q += clock64() - c0;)
         const int4 e = segq[q];
         __syncwarp();
         if (lane == 0) mbar_arrive(&qempty[q]);
@@ -302,23 +317,21 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
         const int seg = e.x;
         if (seg < 0) break;
         const int len = e.y;
-        const uint32_t code = (uint32_t)e.z;
         double acc[MF][NF][2];
 #pragma unroll
         for (int i = 0; i < MF; i++)
 #pragma unroll
             for (int j = 0; j < NF; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-        // one task: wait for its stage, 16-wide k chunks of fragment loads + DMMAs; the
-        // WITH_EPI instance (first task of a segment with an epilogue pending) carries the
-        // epilogue slices in the same straight-line code as the DMMAs
-        auto task = [&](auto with_epi) {
-            constexpr bool WITH_EPI = decltype(with_epi)::value;
+        for (int it = 0; it < len; it++) {
+            // one task: wait for its stage, 16-wide k chunks of fragment loads + DMMAs
+            CLK(unsigned long long c1 = clock64();)
             mbar_wait(&full[stage], phase);
+            CLK(c_full += clock64() - c1; n_task++;)
             const double *As = smem + (2 * stage) * TILE;
             const double *Bs = As + TILE;
 #pragma unroll
-            for (int kc = 0; kc < NKC; kc++) {
+            for (int kc = 0; kc < B / 16; kc++) {
                 // contraction index permuted inside the 16-wide chunk: k = 16kc + 4t + s
                 double a[MF][4], bf[NF][4];
 #pragma unroll
@@ -336,7 +349,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
                 for (int nf = 0; nf < NF; nf++)
 #pragma unroll
                     for (int s = 0; s < 4; s++) bf[nf][s] = Bs[boff[nf][s] + 16 * kc * B];
-                if (kc == NKC - 1) {
+                if (kc == B / 16 - 1) {
                     // Every read of this stage is issued: release it before the last chunk's
                     // DMMAs (which only need registers), so the refill starts a quarter task
                     // earlier and the fence's wait overlaps the previous chunk's DMMAs.  The
@@ -353,45 +366,99 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_leaf_gemm(GemmArgs g)
 #pragma unroll
                         for (int nf = 0; nf < NF; nf++)
                             dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s], bf[nf][s]);
-                if constexpr (WITH_EPI) epi_slice(kc);
             }
-            if constexpr (WITH_EPI) epi_deposit();
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
             }
-        };
-        if (pseg >= 0) task(std::true_type{});
-        else task(std::false_type{});
-        for (int it = 1; it < len; it++) task(std::false_type{});
-        // park this segment's epilogue until the next segment's first task
+        }
+        // the value map and this thread's share of ||C_ij||^2 (and tr X_ii), then deposit
+        // the values (pool layout) and the partials once the epilogue warp has stored the
+        // previous tile, and go on to the next segment
+        CLK(unsigned long long c4 = clock64(); n_seg++;)
+        const uint32_t code = (uint32_t)e.z;
+        const bool diag = morton_i(code) == morton_j(code);
+        double ssp[MF], trp = 0.0;   // one short FMA chain per mf (the FP64 pipe is busy with DMMAs)
 #pragma unroll
-        for (int i = 0; i < MF; i++)
+        for (int mf = 0; mf < MF; mf++) ssp[mf] = 0.0;
 #pragma unroll
-            for (int j = 0; j < NF; j++) {
-                pacc[i][j][0] = acc[i][j][0];
-                pacc[i][j][1] = acc[i][j][1];
+        for (int mf = 0; mf < MF; mf++)
+#pragma unroll
+            for (int nf = 0; nf < NF; nf++) {
+                const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
+                double y0 = acc[mf][nf][0], y1 = acc[mf][nf][1];
+                if (EPI == EPI_STORE_SCALED) {   // the fused final unscale of an NS run
+                    y0 *= g.alpha;
+                    y1 *= g.alpha;
+                }
+                if (!STORE && diag) {
+                    if (r == c) trp += y0;
+                    if (r == c + 1) trp += y1;
+                }
+                if (EPI == EPI_NS_H) {
+                    // H = 1/2 (3 delta - X) written as 1.5 delta - 0.5 x (the 1/2 is exact)
+                    const double d0 = (diag && r == c) ? 1.5 : 0.0, d1 = (diag && r == c + 1) ? 1.5 : 0.0;
+                    y0 = d0 - 0.5 * y0;
+                    y1 = d1 - 0.5 * y1;
+                }
+                ssp[mf] = fma(y0, y0, ssp[mf]);
+                ssp[mf] = fma(y1, y1, ssp[mf]);
+                acc[mf][nf][0] = y0;
+                acc[mf][nf][1] = y1;
             }
-        pseg = seg;
-        pcode = code;
-        pslot = slot;
-        if (++slot == RS) slot = 0;
-    }
-    if (pseg >= 0) {   // the CTA's last segment
+        if (!STORE && diag) {   // warp-uniform, ~1 segment in 100 at C5
 #pragma unroll
-        for (int kc = 0; kc < NKC; kc++) epi_slice(kc);
-        epi_deposit();
+            for (int o = 16; o > 0; o >>= 1) trp += __shfl_xor_sync(0xffffffffu, trp, o);
+        }
+        CLK(unsigned long long c5 = clock64();)
+        mbar_wait(eempty, ephase ^ 1);
+        CLK(unsigned long long c6 = clock64(); c_map += c5 - c4; c_ew += c6 - c5;)
+        ephase ^= 1;
+#pragma unroll
+        for (int mf = 0; mf < MF; mf++)
+#pragma unroll
+            for (int nf = 0; nf < NF; nf++) {
+                const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
+                *reinterpret_cast<double2 *>(ebuf + r * B + (((c >> 1) ^ swz(r)) << 1)) =
+                    make_double2(acc[mf][nf][0], acc[mf][nf][1]);
+            }
+#pragma unroll
+        for (int w = MF / 2; w > 0; w >>= 1)   // fixed pairwise tree
+#pragma unroll
+            for (int mf = 0; mf < w; mf++) ssp[mf] += ssp[mf + w];
+        ess[32 * warp + lane] = ssp[0];
+        if (!STORE && diag && lane == 0) etr[warp] = trp;
+        __syncwarp();
+        if (lane == 0) {
+            if (warp == 0) *erec = make_int4(seg, e.z, 0, 0);
+            mbar_arrive(efull);
+        }
+        CLK(c_bnd += clock64() - c4;)
     }
+    // end of the launch: tell the epilogue warp (after its last tile is read)
+    mbar_wait(eempty, ephase ^ 1);
+    __syncwarp();
+    if (lane == 0) {
+        if (warp == 0) *erec = make_int4(-1, 0, 0, 0);
+        mbar_arrive(efull);
+    }
+    CLK(if (lane == 0) {
+        atomicAdd(&g_gemm_clk[0], clock64() - c_start);
+        atomicAdd(&g_gemm_clk[1], c_full);
+        atomicAdd(&g_gemm_clk[2], c_q);
+        atomicAdd(&g_gemm_clk[3], c_bnd);
+        atomicAdd(&g_gemm_clk[4], n_task);
+        atomicAdd(&g_gemm_clk[5], n_seg);
+        atomicAdd(&g_gemm_clk[6], c_map);
+        atomicAdd(&g_gemm_clk[7], c_ew);
+    })
 }
 
 template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
 static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
 {
-    constexpr int NT = 32 * (CW + 1);
-    constexpr int QN = 4, RS = 2 * QN;   // as in the kernel
-    const size_t smem = sizeof(double) * 2 * STAGES * B * B + 2 * STAGES * sizeof(uint64_t) +
-                        2 * QN * sizeof(uint64_t) + QN * sizeof(int4) + RS * 2 * CW * sizeof(double) +
-                        RS * sizeof(int);
+    constexpr int NT = 32 * (CW + 1 + EW);
+    const size_t smem = GemmSmem<B, CW, STAGES>::bytes;
     auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI, TA>;
     static std::atomic<uint64_t> configured{0};
     static std::atomic<int> occ_cache{0};
