@@ -88,7 +88,7 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
 //   warps 0..CW-1 (consumers): per task wait for the stage, load fragments,
 //     issue DMMAs into register accumulators, release the stage; at the end of a
 //     segment apply the value map (H = 1.5 delta - 0.5 X, alpha), form their share
-//     of ||C_ij||^2 (and tr X_ii) in short FMA chains, deposit values (pool layout)
+//     of ||C_ij||^2 (and tr X_ii) in short FMA chains, deposit values (eswz layout)
 //     and partial in the smem epilogue tile and go on to the next segment.
 //   warps CW+1 .. CW+EW (epilogue): copy the deposited tile to the pool with
 //     contiguous 16-byte stores; the first also sums the consumers' partials in a
@@ -104,6 +104,12 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
 // the tile needs a proxy fence in every consumer thread (5.6 % at the boundary).
 // TA = 1: the left operand is A^T (single channel, §8(f) f2): the A tile is read
 // with the column pattern of the B fragments (A^T[m][k] = A[k][m]).
+// The epilogue tile's own chunk swizzle: chunk c/2 of row r at (c/2) ^ eswz(r).  A deposit
+// instruction (rows 8mf + g8, chunks 4nf + t4 + const) then fills 8 distinct 16-byte bank
+// slots in each 8-lane phase (the pool swizzle would put rows 2p and 2p+1 on the same 4:
+// two-way conflicts); the epilogue warps read whole rows and store them in the pool layout.
+__device__ __forceinline__ int eswz(int r) { return (r & 1) << 2; }
+
 template <int B, int CW, int STAGES>
 struct GemmSmem {
     static constexpr int TILE = B * B;
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
     constexpr uint32_t TILE_BYTES = TILE * 8;
     extern __shared__ __align__(1024) double smem[];
     constexpr int QN = GemmSmem<B, CW, STAGES>::QN;
-    double *ebuf = smem + 2 * STAGES * TILE;                  // the epilogue tile (pool layout)
+    double *ebuf = smem + 2 * STAGES * TILE;                  // the epilogue tile (eswz layout)
     double *ess = ebuf + TILE;                                // [CW][32] lanes' ||C_ij||^2 partials
     double *etr = ess + 32 * CW;                              // [CW] warps' tr partials (diagonal blocks)
     uint64_t *full = reinterpret_cast<uint64_t *>(etr + GemmSmem<B, CW, STAGES>::ETR);
@@ -247,7 +253,10 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
 #pragma unroll
                 for (int j = 0; j < NU; j++) v[j] = eb2[lane + 32 * (ew + EW * (i0 + j))];
 #pragma unroll
-                for (int j = 0; j < NU; j++) dst[lane + 32 * (ew + EW * (i0 + j))] = v[j];
+                for (int j = 0; j < NU; j++) {
+                    const int ch = lane + 32 * (ew + EW * (i0 + j)), r = ch / (B / 2), q = ch % (B / 2);
+                    dst[r * (B / 2) + (q ^ eswz(r) ^ swz(r))] = v[j];   // to the pool layout
+                }
             }
             double ss = 0.0, tr = 0.0;
             const int I = morton_i(code), J = morton_j(code);
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
             }
         }
         // the value map and this thread's share of ||C_ij||^2 (and tr X_ii), then deposit
-        // the values (pool layout) and the partials once the epilogue warp has stored the
+        // the values (eswz layout) and the partials once the epilogue warp has stored the
         // previous tile, and go on to the next segment
         CLK(unsigned long long c4 = clock64(); n_seg++;)
         const uint32_t code = (uint32_t)e.z;
@@ -419,7 +428,7 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
 #pragma unroll
             for (int nf = 0; nf < NF; nf++) {
                 const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
-                *reinterpret_cast<double2 *>(ebuf + r * B + (((c >> 1) ^ swz(r)) << 1)) =
+                reinterpret_cast<double2 *>(ebuf)[r * (B / 2) + ((c >> 1) ^ eswz(r))] =
                     make_double2(acc[mf][nf][0], acc[mf][nf][1]);
             }
 #pragma unroll
