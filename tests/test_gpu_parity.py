@@ -172,6 +172,30 @@ def test_multiply_random(ctx, n, b, tau):
         assert rel(sp().spamm_to_dense(ctx, C).cpu().numpy(), ref) <= 1e-13
 
 
+@pytest.mark.parametrize("b", [64, 32, 16])
+@pytest.mark.parametrize("band", [0, 1])
+def test_multiply_short_segments(ctx, b, band):
+    """Block-(tri)diagonal operands with nb = 1024 block rows: every output block has 1
+    (band 0) or 1-3 (band 1) leaf tasks, so each CTA of the persistent GEMM hands the
+    epilogue tile from its consumer warps to its epilogue warps after every task or two,
+    ~7-20 times per launch.  Values, norms and task order go through check_product."""
+    nb = 1024
+    n = nb * b
+    r = np.random.default_rng(b + band)
+    bi, bj = [], []
+    for I in range(nb):
+        for J in range(max(0, I - band), min(nb, I + band + 1)):
+            bi.append(I)
+            bj.append(J)
+    bi = np.array(bi, dtype=np.int32)
+    bj = np.array(bj, dtype=np.int32)
+    A, Ao = build_pair(ctx, "blocks", (bi, bj, r.standard_normal((len(bi), b, b))), b, n)
+    B, Bo = build_pair(ctx, "blocks", (bi, bj, r.standard_normal((len(bi), b, b))), b, n)
+    C, st = sp().spamm_multiply(ctx, A, B, 0.0, want_stats=True)
+    assert st["segments"] == (nb if band == 0 else 5 * nb - 6)   # |I - J| <= 2 * band
+    check_product(ctx, A, Ao, B, Bo, 0.0)
+
+
 def test_multiply_degenerate(ctx):
     z = np.zeros((128, 128))
     Z, Zo = build_pair(ctx, "dense", z, 16, 128)
