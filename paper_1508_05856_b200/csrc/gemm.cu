@@ -119,6 +119,7 @@ struct GemmSmem {
     static constexpr int ETR = (CW + 1) & ~1;   // tr partials, padded to keep 16-byte alignment
     static constexpr size_t bytes = sizeof(double) * ((2 * STAGES + 1) * TILE + 32 * CW + ETR) +
                                     sizeof(uint64_t) * (2 * STAGES + 2 * QN + 2) + sizeof(int4) * (QN + 1);
+    static_assert(bytes <= 227 * 1024, "the leaf GEMM's shared memory exceeds the 227 KiB an sm_100a CTA may use");
 };
 
 #ifndef SPAMM_EPI_WARPS
