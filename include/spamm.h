@@ -75,6 +75,9 @@ typedef struct {
     int64_t halo_blocks;        /* row partition: remote right-operand blocks fetched */
     int64_t local_segments;     /* row partition: segments needing no remote block (run
                                    while the halo is exchanged)                        */
+    int32_t transport;          /* row partition, world > 1: 1 = halo exchange over the
+                                   communicator (v2), 2 = peer memory: remote tiles read in
+                                   place from the owners' pools (v3); 0 otherwise        */
 } spamm_stats;
 
 /* Options of spamm_ns_sqrt (NULL => defaults).  History buffers are HOST memory. */
@@ -139,10 +142,15 @@ spamm_status spamm_comm_nccl_unique_id(void *id128);
 spamm_status spamm_comm_nccl_create(const void *id128, int32_t rank, int32_t world, int32_t device,
                                     spamm_comm *out);
 /* An in-process group of `world` ranks (comms[0..world-1]) for host threads that
- * each drive their own context, possibly on the same device: collectives are
+ * each drive their own context, on one device or several: collectives are
  * stream-ordered device copies joined by host barriers and CUDA events (no
- * kernel ever waits on another rank's kernel).  Used to check the partitioned
- * path on one GPU; the arithmetic is the same as with NCCL. */
+ * kernel ever waits on another rank's kernel).  The group also offers peer
+ * memory: ranks publish their right operand's pool and slot
+ * map once per product and the leaf GEMM bulk-copies remote tiles straight from
+ * the owner's pool (peer access over NVLink between devices, enabled on first
+ * use); no halo is exchanged.  Where two ranks' devices cannot reach each other,
+ * or with SPAMM_PEER=0, products use the halo exchange.  The arithmetic is the
+ * same on every transport (bitwise equal results). */
 spamm_status spamm_comm_local_group(int32_t world, spamm_comm *comms);
 void spamm_comm_destroy(spamm_comm comm);
 /* Attach a communicator (borrowed; NULL detaches) and the row partition:

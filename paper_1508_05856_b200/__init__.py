@@ -49,12 +49,13 @@ class SpammError(RuntimeError):
 class spamm_stats(C.Structure):
     _fields_ = [("tasks", C.c_int64), ("segments", C.c_int64), ("candidates", C.c_int64),
                 ("level_survivors", C.c_int64 * 24), ("flops", C.c_double), ("halo_blocks", C.c_int64),
-                ("local_segments", C.c_int64)]
+                ("local_segments", C.c_int64), ("transport", C.c_int32)]
 
     def as_dict(self):
         return dict(tasks=self.tasks, segments=self.segments, candidates=self.candidates,
                     level_survivors=list(self.level_survivors), flops=self.flops,
-                    halo_blocks=self.halo_blocks, local_segments=self.local_segments)
+                    halo_blocks=self.halo_blocks, local_segments=self.local_segments,
+                    transport=self.transport)
 
 
 class spamm_ns_opts(C.Structure):

@@ -6,7 +6,9 @@
 //               resolved with dlopen so the library has no link-time NCCL
 //               dependency (PyTorch's libnccl.so.2 is normally already loaded).
 //   LocalComm : `world` ranks inside one process, one host thread and one
-//               context (stream) per rank, possibly all on the same device.
+//               context (stream) per rank, on one device or several (peer access
+//               enabled on first use).  Also offers peer memory (v3 of §8(e)):
+//               ranks share device pointers and the GEMM reads remote tiles in place.
 //               A collective is: publish buffers + a "ready" event, host
 //               barrier, each rank pushes its data with stream-ordered copies
 //               after waiting on the receivers' ready events, records "done",
@@ -131,6 +133,8 @@ struct LocalShared {
         size_t bytes = 0;
         const size_t *soff = nullptr, *scnt = nullptr, *roff = nullptr, *rcnt = nullptr;
         cudaEvent_t ready = nullptr, done = nullptr;
+        const void *const *ptrs = nullptr;   // peer_share: the published pointers
+        int device = -1;
     };
     std::vector<Slot> slot;
     void barrier()
@@ -190,6 +194,49 @@ struct LocalComm : spamm_comm_s {
         if (e1 != cudaSuccess) return check_cuda(ctx, e1, "local comm ready");
         if (e2 != cudaSuccess) return check_cuda(ctx, e2, "local comm push");
         if (e3 != cudaSuccess) return check_cuda(ctx, e3, "local comm wait");
+        return SPAMM_OK;
+    }
+    bool peer_capable() const override { return true; }
+    // publish + ready, barrier, read the peers' slots and wait for their ready events,
+    // barrier (the slots may be reused by the next call only now)
+    spamm_status peer_share(spamm_ctx ctx, const void *const *mine, int n, const void **all, int *ok) override
+    {
+        ST(ensure_events(ctx));
+        LocalShared::Slot &me = sh->slot[rank];
+        me.ptrs = mine;
+        me.device = ctx->device;
+        cudaError_t e1 = cudaEventRecord(me.ready, ctx->stream);
+        sh->barrier();
+        int can = 1;
+        cudaError_t e2 = cudaSuccess;
+        for (int p = 0; p < world && e2 == cudaSuccess; p++) {
+            const LocalShared::Slot &q = sh->slot[p];
+            for (int i = 0; i < n; i++) all[(size_t)p * n + i] = q.ptrs[i];
+            if (q.device != ctx->device) {
+                int a = 0;
+                if (cudaDeviceCanAccessPeer(&a, ctx->device, q.device) != cudaSuccess || !a) can = 0;
+                else if (cudaDeviceEnablePeerAccess(q.device, 0) == cudaErrorPeerAccessAlreadyEnabled)
+                    cudaGetLastError();
+            }
+            e2 = cudaStreamWaitEvent(ctx->stream, q.ready, 0);
+        }
+        sh->barrier();
+        *ok = can;
+        if (e1 != cudaSuccess) return check_cuda(ctx, e1, "peer share ready");
+        if (e2 != cudaSuccess) return check_cuda(ctx, e2, "peer share wait");
+        return SPAMM_OK;
+    }
+    spamm_status peer_barrier(spamm_ctx ctx) override
+    {
+        ST(ensure_events(ctx));
+        LocalShared::Slot &me = sh->slot[rank];
+        cudaError_t e1 = cudaEventRecord(me.ready, ctx->stream);
+        sh->barrier();
+        cudaError_t e2 = cudaSuccess;
+        for (int p = 0; p < world && e2 == cudaSuccess; p++) e2 = cudaStreamWaitEvent(ctx->stream, sh->slot[p].ready, 0);
+        sh->barrier();
+        if (e1 != cudaSuccess) return check_cuda(ctx, e1, "peer barrier ready");
+        if (e2 != cudaSuccess) return check_cuda(ctx, e2, "peer barrier wait");
         return SPAMM_OK;
     }
     spamm_status allgather(spamm_ctx ctx, const void *send, void *recv, size_t bytes) override

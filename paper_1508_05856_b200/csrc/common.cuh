@@ -46,6 +46,21 @@ struct spamm_comm_s {
                                    const size_t *scnt, void *recv, const size_t *roff,
                                    const size_t *rcnt) = 0;
     virtual const char *kind() const = 0;
+    // Peer memory: a rank's kernels may read another rank's device
+    // memory directly (same process; the same device or peer access over NVLink).
+    // peer_share publishes n device pointers, returns every rank's (rank-major in all),
+    // and makes the calling stream wait for the work every rank queued before the call
+    // (so the memory behind the pointers is complete); *ok = 0 when some pair of ranks
+    // cannot access each other's memory.  peer_barrier: the calling stream waits for the
+    // work every rank queued before the call (readers are done before an owner reuses
+    // or frees what it shared).
+    virtual bool peer_capable() const { return false; }
+    virtual spamm_status peer_share(spamm_ctx, const void *const *, int, const void **, int *ok)
+    {
+        *ok = 0;
+        return SPAMM_OK;
+    }
+    virtual spamm_status peer_barrier(spamm_ctx) { return SPAMM_OK; }
 };
 
 struct spamm_ctx_s {
@@ -328,6 +343,11 @@ spamm_status gather_rows(spamm_ctx ctx, const Parts &p, double *vec, int width);
 // fetch the remote right-operand blocks the local tasks of cw use; patches
 // cw->tB (remote => -(h+1), h = halo slot) and returns the halo pool
 spamm_status halo_exchange(spamm_ctx ctx, struct Cull *cw, spamm_mat B, double **halo, int64_t *nhalo);
+// peer memory (§8(e) v3): when every rank can read every other's memory, resolve the
+// remote tasks' B slots in the owners' slot maps and point the GEMM at the owners'
+// pools (cw->peer_*); *used = false => use halo_exchange.  The caller runs
+// comm->peer_barrier after the GEMM (owners keep their B until every reader is done).
+spamm_status peer_patch(spamm_ctx ctx, struct Cull *cw, spamm_mat B, bool *used);
 // stable split of the segments into all-local (every task's B block is row-local)
 // then remote-using ones: order[nsegs] (device, caller frees), *nlocal (host)
 spamm_status seg_split(spamm_ctx ctx, struct Cull *cw, int32_t **order, int64_t *nlocal);
@@ -360,6 +380,10 @@ struct Cull {
     double alpha = 1.0;           // EPI_STORE output scale of the next GEMM (fused unscale)
     int64_t gen = 0;              // bumped by every (re)allocation (captured graphs check it)
     bool counts_only = false;     // a counting query (its tasks never reach a GEMM)
+    // peer memory (dist.cu peer_patch): remote right-operand tiles are read in place from
+    // the owners' pools; tB = -(slot * peer_world + owner) - 1 for those tasks
+    int peer_world = 0;
+    const double *peer_pool[SPAMM_MAX_WORLD] = {};
     spamm_stats stats{};
 };
 // Enqueue the query, synchronise once to read the counts, and grow + re-run

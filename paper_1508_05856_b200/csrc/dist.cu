@@ -310,6 +310,69 @@ spamm_status halo_exchange(spamm_ctx ctx, Cull *cw, spamm_mat B, double **halo, 
     return SPAMM_OK;
 }
 
+// ------------------------------------------------------------ peer memory
+// §8(e) v3: where the ranks can read each other's memory (LocalComm: one process, one
+// device or peer access over NVLink), the request / pack / send-recv sequence and the
+// halo pool disappear.  The owners publish their pool and slot map; each remote task's
+// B slot is resolved in the owner's slot map (a peer read) and encoded as
+// tB = -(slot * W + owner) - 1; the GEMM producer bulk-copies those tiles straight from
+// the owner's pool, so the transfer is overlapped with the DMMAs tile by tile by the
+// GEMM's own pipeline.  Same tasks, same k order: bitwise the v2 and single-device
+// results.
+struct PeerSlots {
+    const int32_t *p[SPAMM_MAX_WORLD];
+};
+
+__global__ void k_patch_tb_peer(const int4 *rec, int64_t n, int nb, Parts p, PeerSlots slots, int32_t *tB)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        if (tB[t] >= 0) continue;
+        const int4 r = rec[t];
+        const int k = r.y, j = morton_j((uint32_t)r.x);
+        int q = 0;
+        while (q + 1 < p.world && p.rs[q + 1] <= k) q++;
+        const int s = slots.p[q][morton(k, j)];
+        SPAMM_ASSERT(s >= 0);   // a surviving triple's B block is stored by its owner
+        tB[t] = -(s * p.world + q) - 1;
+    }
+}
+
+// SPAMM_PEER=0: the v2 halo exchange even where peer memory is available (read per
+// product, so a test can switch it between runs)
+static int peer_mode()
+{
+    const char *e = getenv("SPAMM_PEER");
+    return e && *e ? atoi(e) : 1;
+}
+
+spamm_status peer_patch(spamm_ctx ctx, Cull *cw, spamm_mat B, bool *used)
+{
+    *used = false;
+    cw->peer_world = 0;
+    if (!B->dist || B->parts.world <= 1 || !ctx->comm || !ctx->comm->peer_capable() || !peer_mode())
+        return SPAMM_OK;
+    const int W = B->parts.world;
+    const void *mine[2] = {B->pool, B->slot};
+    std::vector<const void *> all((size_t)2 * W);
+    int ok = 0;
+    ST(ctx->comm->peer_share(ctx, mine, 2, all.data(), &ok));
+    if (!ok) return SPAMM_OK;   // some pair cannot reach each other's memory: the v2 exchange
+    PeerSlots ps{};
+    for (int q = 0; q < W; q++) {
+        cw->peer_pool[q] = static_cast<const double *>(all[(size_t)2 * q]);
+        ps.p[q] = static_cast<const int32_t *>(all[(size_t)2 * q + 1]);
+    }
+    if (cw->ntasks > 0) {
+        const int grid = (int)std::min<int64_t>(cdiv(cw->ntasks, 256), 8 * ctx->sm_count);
+        k_patch_tb_peer<<<grid, 256, 0, ctx->stream>>>(cw->rec[cw->final_buf], cw->ntasks, B->nb, B->parts, ps, cw->tB);
+        ctx->launches++;
+        CKL(ctx);
+    }
+    cw->peer_world = W;
+    *used = true;
+    return SPAMM_OK;
+}
+
 // ------------------------------------------------- local-first segment order
 // flag[s] = 1 iff every task of segment s reads a row-local B block (tB >= 0); those
 // segments can run while the halo is in flight (overlap at

@@ -46,6 +46,8 @@ struct GemmArgs {
     double alpha;      // EPI_STORE: C = alpha (A (x) B) (the final unscale of the NS run, fused)
     const int32_t *nseg_dev;   // non-null: the segment count is read here (device-driven
                                // steps: the cull's count, no host round trip)
+    int peer_world;            // > 0: tB < 0 is -(slot * peer_world + owner) - 1, a tile read in
+    const double *peer_pool[SPAMM_MAX_WORLD];   // place from the owner's pool (peer memory)
     // capacities, checked by the SPAMM_DEBUG build only
     int64_t a_cap, b_cap, halo_cap, c_cap, task_cap, seg_cap;
     int nb;
@@ -209,13 +211,20 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
                     const int a = __shfl_sync(0xffffffffu, sa, j);
                     const int b = __shfl_sync(0xffffffffu, sb, j);
                     SPAMM_ASSERT(a >= 0 && a < g.a_cap);
-                    SPAMM_ASSERT(b >= 0 ? b < g.b_cap : (-b - 1) < g.halo_cap);
+                    SPAMM_ASSERT(b >= 0 ? b < g.b_cap : (g.peer_world > 0 || (-b - 1) < g.halo_cap));
                     if (lane == 0) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         mbar_expect_tx(&full[stage], 2 * TILE_BYTES);
                         bulk_g2s(smem + (2 * stage) * TILE, g.a_pool + (int64_t)a * TILE, TILE_BYTES, &full[stage]);
-                        const double *bsrc = b >= 0 ? g.b_pool + (int64_t)b * TILE
-                                                    : g.b_halo + (int64_t)(-b - 1) * TILE;
+                        const double *bsrc;
+                        if (b >= 0) {
+                            bsrc = g.b_pool + (int64_t)b * TILE;
+                        } else if (g.peer_world > 0) {   // the owner's pool (peer memory)
+                            const int e = -b - 1;
+                            bsrc = g.peer_pool[e % g.peer_world] + (int64_t)(e / g.peer_world) * TILE;
+                        } else {
+                            bsrc = g.b_halo + (int64_t)(-b - 1) * TILE;
+                        }
                         bulk_g2s(smem + (2 * stage + 1) * TILE, bsrc, TILE_BYTES, &full[stage]);
                     }
                     if (++stage == STAGES) {
@@ -508,8 +517,9 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
     GemmArgs g{A->pool, B->pool, b_halo, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
                (int)nseg, seg_order, C->pool, C->coord, C->slot, C->norm2 + pyr_off(C->L), trace_part,
                cw->counters + CNT_GEMM_TICKET + ticket, cw->alpha,
-               device_count ? cw->counters + CNT_NSEG : nullptr,
+               device_count ? cw->counters + CNT_NSEG : nullptr, cw->peer_world, {},
                A->cap, B->cap, b_halo ? (int64_t)1 << 40 : 0, C->cap, cw->cap, cw->cap_segs, A->nb};
+    for (int q = 0; q < cw->peer_world; q++) g.peer_pool[q] = cw->peer_pool[q];
     if (transA) {
         if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 1>(ctx, A->b, g);
         if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 1>(ctx, A->b, g);

@@ -281,6 +281,7 @@ static spamm_status overlapped_gemm(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_
         ctx->stream = main_s;
         cw->stats.halo_blocks = nhalo;
         cw->stats.local_segments = nloc;
+        cw->stats.transport = 1;
     }
     if (!st) {
         CK(cudaEventRecord(ctx->ev[1], comm_s));
@@ -325,10 +326,19 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
     g_product_id++;
     if (selfcheck_mode()) selfcheck_cull(ctx, cw, A, B, tau, transA);
     if (ctx->vsink) ST(volume_record(ctx, cw));
-    const bool overlap = A->dist && A->parts.world > 1;
+    bool peer = false;
+    if (A->dist && A->parts.world > 1) {
+        int px = prof_begin(ctx, SPAMM_PH_OTHER);
+        sc = peer_patch(ctx, cw, B, &peer);
+        prof_end(ctx, px);
+        if (sc) return sc;
+    }
+    // peer memory: one GEMM over all segments reading remote tiles in place; otherwise
+    // the v2 halo exchange overlapped with the all-local segments
+    const bool overlap = A->dist && A->parts.world > 1 && !peer;
     double *halo = nullptr;
     int64_t nhalo = 0;
-    if (A->dist && !overlap) {
+    if (A->dist && !overlap && !peer) {
         // world size 1: nothing is remote, the exchange is a no-op
         int px = prof_begin(ctx, SPAMM_PH_OTHER);
         sc = halo_exchange(ctx, cw, B, &halo, &nhalo);
@@ -344,6 +354,10 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
     }
     if (st) {
         dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
+        if (peer) {   // the peers are waiting for this rank in the post-GEMM barrier
+            cw->peer_world = 0;
+            ctx->comm->peer_barrier(ctx);
+        }
         return st;
     }
     st = mat_reset_pattern(ctx, m);
@@ -362,6 +376,14 @@ static spamm_status product(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, d
         if (!st && selfcheck_mode()) selfcheck_gemm(ctx, cw, A, B, halo, m, epi, transA);
     }
     dev_free(ctx, halo, sizeof(double) * nhalo * A->b * A->b);
+    if (peer) {
+        // every rank's reads of this rank's B are done before any rank goes on (and may
+        // free or overwrite what it shared); the barrier runs whatever happened above
+        cw->peer_world = 0;
+        cw->stats.transport = 2;
+        const spamm_status sb = ctx->comm->peer_barrier(ctx);
+        if (!st) st = sb;
+    }
     if (!st) {
         m->nblk = cw->nsegs;
         // absent diagonal blocks of X: H_ii = 1.5 I (plain map) or X_ii = 0 (scaled map,

@@ -39,6 +39,15 @@ def gpu():
     return 0
 
 
+@pytest.fixture(params=["peer", "halo"])
+def transport(request, monkeypatch):
+    """The in-process group's two transports: peer memory (v3, the default: the GEMM
+    reads remote tiles in place from the owners' pools) and the halo exchange (v2,
+    SPAMM_PEER=0, also what NCCL ranks use).  The library reads SPAMM_PEER per product."""
+    monkeypatch.setenv("SPAMM_PEER", "1" if request.param == "peer" else "0")
+    return {"peer": 2, "halo": 1}[request.param]
+
+
 def gaussian(n, b, seed=150805856, sigma=0.8, tau_min=1e-7):
     cfg = si.Config("t", "gauss", n, b, 1e-7, 30, sigma=sigma, shift=1e-3, seed=seed, tau_min=tau_min)
     return si.make_input(cfg)[1]
@@ -89,6 +98,7 @@ def dist_ns(world, n, b, payload, tau, iters, row_start=None, mu=0.0, scale=0.0)
         r = sp().spamm_ns_sqrt(ctx, S, tau, iters, mu=mu, scale=scale)
         out = dict(Y=blocks_of(ctx, r["Y"]), Z=blocks_of(ctx, r["Z"]), t=r["t"].copy(), c=r["c"],
                    tasks=np.array([[p["tasks"] for p in k] for k in r["stats"]]),
+                   transport={p["transport"] for k in r["stats"] for p in k},
                    rows=sp().spamm_mat_rows(r["Y"]),
                    n2=sp().spamm_level_norms2(ctx, r["Y"], (n // b).bit_length() - 1))
         for m in (S, r["Y"], r["Z"]):
@@ -98,7 +108,9 @@ def dist_ns(world, n, b, payload, tau, iters, row_start=None, mu=0.0, scale=0.0)
     return dist().run_rank_threads(world, fn)
 
 
-def check_same(ref, res, world):
+def check_same(ref, res, world, transport=None):
+    if transport is not None and world > 1:
+        assert all(r["transport"] == {transport} for r in res), [r["transport"] for r in res]
     assert_bitwise(merged(res, "Y"), ref["Y"])
     assert_bitwise(merged(res, "Z"), ref["Z"])
     for r in res:
@@ -113,25 +125,25 @@ def check_same(ref, res, world):
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_ns_kms_bitwise_equal_to_single_device(gpu, world):
+def test_ns_kms_bitwise_equal_to_single_device(gpu, world, transport):
     c = si.CONFIGS["C2"]
     s = si.kms(c.n, c.rho)
     iters = 12
     ref = single_ns(c.n, c.b, s, c.tau, iters)
     res = dist_ns(world, c.n, c.b, s, c.tau, iters)
-    check_same(ref, res, world)
+    check_same(ref, res, world, transport)
 
 
 @pytest.mark.parametrize("world,row_start", [(2, None), (4, None), (4, [0, 5, 6, 40, 64]),
                                              (8, None), (3, [0, 0, 64, 64])])
-def test_ns_gaussian_bitwise(gpu, world, row_start):
+def test_ns_gaussian_bitwise(gpu, world, row_start, transport):
     """n = 4096, b = 64 (nb = 64) Gaussian overlap, uneven and empty ranges."""
     n, b = 4096, 64
     payload = gaussian(n, b)
     iters = 10
     ref = single_ns(n, b, payload, 1e-7, iters)
     res = dist_ns(world, n, b, payload, 1e-7, iters, row_start)
-    check_same(ref, res, world)
+    check_same(ref, res, world, transport)
     if row_start is not None:
         assert [r["rows"] for r in res] == [(row_start[p], row_start[p + 1]) for p in range(world)]
 
@@ -152,7 +164,7 @@ def test_ns_dist_matches_oracle(gpu):
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("tau", [0.0, 1e-6])
-def test_multiply_bitwise_and_tasks(gpu, world, tau):
+def test_multiply_bitwise_and_tasks(gpu, world, tau, transport):
     n, b = 2048, 32
     r = np.random.default_rng(7)
     i = np.arange(n)
@@ -170,7 +182,8 @@ def test_multiply_bitwise_and_tasks(gpu, world, tau):
         c2 = sp().spamm_ctx_create(0, library_stream=True)
         sp().spamm_ctx_set_comm(c2, comm, dist().balanced_partition(counts, world))
         A2 = build(c2, n, b, a)
-        C2 = sp().spamm_multiply(c2, A2, A2, tau)
+        C2, st = sp().spamm_multiply(c2, A2, A2, tau, want_stats=True)
+        assert st["transport"] == transport
         out = (blocks_of(c2, C2), {tuple(x) for x in sp().spamm_export_tasks(c2)},
                sp().spamm_row_task_counts(c2, A2, A2, tau), sp().spamm_mat_rows(C2))
         A2.free()
