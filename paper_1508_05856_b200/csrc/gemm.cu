@@ -90,20 +90,27 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
 //   warps 0..CW-1 (consumers): per task wait for the stage, load fragments,
 //     issue DMMAs into register accumulators, release the stage; at the end of a
 //     segment apply the value map (H = 1.5 delta - 0.5 X, alpha), form their share
-//     of ||C_ij||^2 (and tr X_ii) in short FMA chains, deposit values (eswz layout)
-//     and partial in the smem epilogue tile and go on to the next segment.
-//   warps CW+1 .. CW+EW (epilogue): copy the deposited tile to the pool with
-//     contiguous 16-byte stores; the first also sums the consumers' partials in a
-//     fixed order (deterministic) and writes the block's metadata.
+//     of ||C_ij||^2 (and tr X_ii) in short FMA chains, hand the values and the partial
+//     to the epilogue warps and go on to the next segment.
+//   warps CW+1 .. CW+EW (epilogue): store the handed-off tile to the pool; the first
+//     also sums the consumers' partials in a fixed order (deterministic) and writes
+//     the block's metadata.
 // The consumers issue no global stores, shuffle trees or cross-warp hand-offs, so
-// the DMMA pipe keeps running across segment boundaries.  Measured on the C5 k = 8
-// products (4.6 tasks per segment; tools/gemm_clocks.py): the whole epilogue in the
-// consumer warps, interleaved with the next segment's first task, took 4.2 % of their
-// cycles + 0.9 % at the boundary; here the boundary is ~3.8 %.  EW = 2 measured best
-// (NS step GEMM 59.61 ms against 59.98 before, EW = 1: 59.65, EW = 4: 60.02); a single
-// epilogue warp that also did the map and norms fell behind (the FP64 pipe is busy with
-// DMMAs: 10.7 % of the consumers' cycles waiting for the tile), and a TMA bulk store of
-// the tile needs a proxy fence in every consumer thread (5.6 % at the boundary).
+// the DMMA pipe keeps running across segment boundaries.  The hand-off (EpiCfg):
+//   b = 64: through tensor memory, NBUF = 4 tiles deep — one tcgen05.st (STTM.x32) per
+//     consumer thread, one epilogue warp per SM sub-partition reading its lanes back
+//     (LDTM.x32) and storing whole 128-byte lines.  Measured on the C5 / C3 k = 8 NS
+//     steps (tools/gemm_probe.py): GEMM 59.37 / 5.496 ms against 59.56 / 5.511 ms with
+//     the single shared-memory tile (its wait for the previous tile's store, 0.7 % of
+//     the consumers' cycles, is gone); the epilogue warps poll with a 512 ns sleep
+//     (spinning: 60.26 ms, they share the producer's sub-partition) and must store
+//     whole lines (8 rows x 64 bytes per instruction: 59.86 ms).
+//   b = 32 / 16: one shared-memory tile (eswz layout), EW = 2 epilogue warps copying
+//     it with contiguous 16-byte stores.  For b = 64 this was the round-2 design before
+//     TMEM: EW = 2 measured best (EW = 1: +0.1 %, EW = 4: +0.7 %); a single epilogue
+//     warp that also did the map and norms fell behind (the FP64 pipe is busy with
+//     DMMAs), and a TMA bulk store of the tile needs a proxy fence in every consumer
+//     thread (5.6 % of their cycles at the boundary).
 // TA = 1: the left operand is A^T (single channel, §8(f) f2): the A tile is read
 // with the column pattern of the B fragments (A^T[m][k] = A[k][m]).
 // The epilogue tile's own chunk swizzle: chunk c/2 of row r at (c/2) ^ eswz(r).  A deposit
@@ -112,25 +119,82 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
 // two-way conflicts); the epilogue warps read whole rows and store them in the pool layout.
 __device__ __forceinline__ int eswz(int r) { return (r & 1) << 2; }
 
+#ifndef SPAMM_EPI_WARPS
+#define SPAMM_EPI_WARPS 2
+#endif
+#ifndef SPAMM_EPI_TMEM
+#define SPAMM_EPI_TMEM 1
+#endif
+#ifndef SPAMM_EPI_SLEEP
+#define SPAMM_EPI_SLEEP 512   // ns between the epilogue warps' probes of the next tile; 0 = spin
+#endif
+// Epilogue hand-off.  b = 64 (8 consumer warps, 32x16 warp tiles): the finished tile goes
+// through tensor memory — each consumer warp writes its 16 values per thread with one
+// tcgen05.st into the TMEM lanes of its SM sub-partition, and one epilogue warp per
+// sub-partition (warp id mod 4 selects the lanes a warp may access) reads them back with
+// tcgen05.ld and stores them to the pool.  TMEM (256 KB per SM, otherwise unused here: FP64
+// has no tcgen05.mma kind) holds NBUF tiles, so a consumer never waits for the previous tile
+// to be stored.  Other b: one shared-memory tile, EW epilogue warps.
+template <int B, int CW>
+struct EpiCfg {
+    static constexpr bool TE = SPAMM_EPI_TMEM && B == 64 && CW == 8;
+    static constexpr int EW = TE ? 4 : SPAMM_EPI_WARPS;   // epilogue warps
+    static constexpr int NBUF = TE ? 4 : 1;               // tiles in flight to the epilogue warps
+    static constexpr uint32_t TCOLS = TE ? 64 * NBUF : 0;  // TMEM columns (b32) allocated
+};
+
 template <int B, int CW, int STAGES>
 struct GemmSmem {
     static constexpr int TILE = B * B;
     static constexpr int QN = 4;   // segment-queue depth (producer -> consumers)
-    // doubles: STAGES x {A, B} tiles, the epilogue tile, the consumers' per-lane ||.||^2
-    // partials and per-warp trace partials; then the barriers, the queue and the record
+    static constexpr int NBUF = EpiCfg<B, CW>::NBUF;
+    // doubles: STAGES x {A, B} tiles, the epilogue tile (not with TMEM), per buffer the
+    // consumers' per-lane ||.||^2 partials and per-warp trace partials; then the barriers,
+    // the queue, the records and the TMEM base address
     static constexpr int ETR = (CW + 1) & ~1;   // tr partials, padded to keep 16-byte alignment
-    static constexpr size_t bytes = sizeof(double) * ((2 * STAGES + 1) * TILE + 32 * CW + ETR) +
-                                    sizeof(uint64_t) * (2 * STAGES + 2 * QN + 2) + sizeof(int4) * (QN + 1);
+    static constexpr size_t bytes =
+        sizeof(double) * ((2 * STAGES + (EpiCfg<B, CW>::TE ? 0 : 1)) * TILE + NBUF * (32 * CW + ETR)) +
+        sizeof(uint64_t) * (2 * STAGES + 2 * QN + 2 * NBUF) + sizeof(int4) * (QN + NBUF + 1);
     static_assert(bytes <= 227 * 1024, "the leaf GEMM's shared memory exceeds the 227 KiB an sm_100a CTA may use");
 };
 
-#ifndef SPAMM_EPI_WARPS
-#define SPAMM_EPI_WARPS 2
-#endif
-constexpr int EW = SPAMM_EPI_WARPS;   // epilogue warps
+// ---- tensor memory (tcgen05) helpers for the TMEM epilogue hand-off
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+#define TM_R32(p)                                                                                          \
+    "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]), "r"(p[6]), "r"(p[7]), "r"(p[8]),     \
+        "r"(p[9]), "r"(p[10]), "r"(p[11]), "r"(p[12]), "r"(p[13]), "r"(p[14]), "r"(p[15]), "r"(p[16]),      \
+        "r"(p[17]), "r"(p[18]), "r"(p[19]), "r"(p[20]), "r"(p[21]), "r"(p[22]), "r"(p[23]), "r"(p[24]),     \
+        "r"(p[25]), "r"(p[26]), "r"(p[27]), "r"(p[28]), "r"(p[29]), "r"(p[30]), "r"(p[31])
+#define TM_W32(p)                                                                                          \
+    "=r"(p[0]), "=r"(p[1]), "=r"(p[2]), "=r"(p[3]), "=r"(p[4]), "=r"(p[5]), "=r"(p[6]), "=r"(p[7]),        \
+        "=r"(p[8]), "=r"(p[9]), "=r"(p[10]), "=r"(p[11]), "=r"(p[12]), "=r"(p[13]), "=r"(p[14]),           \
+        "=r"(p[15]), "=r"(p[16]), "=r"(p[17]), "=r"(p[18]), "=r"(p[19]), "=r"(p[20]), "=r"(p[21]),         \
+        "=r"(p[22]), "=r"(p[23]), "=r"(p[24]), "=r"(p[25]), "=r"(p[26]), "=r"(p[27]), "=r"(p[28]),         \
+        "=r"(p[29]), "=r"(p[30]), "=r"(p[31])
+#define TM_ARGS32                                                                                          \
+    "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28," \
+    "%29,%30,%31,%32}"
+// thread l of the warp: 32 consecutive b32 columns of TMEM lane (taddr.lane + l)
+__device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t (&v)[32])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], " TM_ARGS32 ";\n" ::"r"(taddr), TM_R32(v)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&v)[32])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,"
+                 "%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                 : TM_W32(v)
+                 : "r"(taddr)
+                 : "memory");
+}
 
 template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
-__global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
+__global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_gemm(GemmArgs g)
 {
     static_assert(WM * WN == CW, "warp grid");
     constexpr bool STORE = EPI == EPI_STORE || EPI == EPI_STORE_SCALED;
@@ -138,19 +202,27 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
     constexpr int MF = TM / 8, NF = TN / 8;
     constexpr int TILE = B * B;
     constexpr uint32_t TILE_BYTES = TILE * 8;
+    constexpr bool TE = EpiCfg<B, CW>::TE;
+    constexpr int EW = EpiCfg<B, CW>::EW, NBUF = EpiCfg<B, CW>::NBUF;
+    // TMEM hand-off: consumer warp w writes lanes 32 (w mod 4).. of columns 64 buf + 32 (w / 4)..;
+    // that needs the two consumer warps of a sub-partition to be warps w, w + 4 (WN = 4) and
+    // 16 values = 32 b32 columns per thread
+    static_assert(!TE || (WN == 4 && CW == 8 && MF * NF * 4 == 32 && EW == 4), "TMEM epilogue layout");
     extern __shared__ __align__(1024) double smem[];
     constexpr int QN = GemmSmem<B, CW, STAGES>::QN;
-    double *ebuf = smem + 2 * STAGES * TILE;                  // the epilogue tile (eswz layout)
-    double *ess = ebuf + TILE;                                // [CW][32] lanes' ||C_ij||^2 partials
-    double *etr = ess + 32 * CW;                              // [CW] warps' tr partials (diagonal blocks)
-    uint64_t *full = reinterpret_cast<uint64_t *>(etr + GemmSmem<B, CW, STAGES>::ETR);
+    constexpr int ETR = GemmSmem<B, CW, STAGES>::ETR;
+    double *ebuf = smem + 2 * STAGES * TILE;                  // the epilogue tile (eswz layout; not with TMEM)
+    double *ess = ebuf + (TE ? 0 : TILE);                     // [NBUF][CW][32] lanes' ||C_ij||^2 partials
+    double *etr = ess + NBUF * 32 * CW;                       // [NBUF][ETR] warps' tr partials (diagonal blocks)
+    uint64_t *full = reinterpret_cast<uint64_t *>(etr + NBUF * ETR);
     uint64_t *empty = full + STAGES;
     uint64_t *qfull = empty + STAGES;
     uint64_t *qempty = qfull + QN;
-    uint64_t *efull = qempty + QN;                            // tile deposited (CW arrivals)
-    uint64_t *eempty = efull + 1;                             // tile stored by the epilogue warp
-    int4 *segq = reinterpret_cast<int4 *>(eempty + 1);        // {seg, len, code, -} per queue entry
-    int4 *erec = segq + QN;                                   // {seg, code} of the deposited tile
+    uint64_t *efull = qempty + QN;                            // [NBUF] tile deposited (CW arrivals)
+    uint64_t *eempty = efull + NBUF;                          // [NBUF] tile stored by the epilogue warps
+    int4 *segq = reinterpret_cast<int4 *>(eempty + NBUF);     // {seg, len, code, -} per queue entry
+    int4 *erec = segq + QN;                                   // [NBUF] {seg, code} of the deposited tile
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(erec + NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pdl_trigger();   // the epilogue-side kernels that follow may stage their launch now
@@ -163,11 +235,30 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
             mbar_init(&qfull[q], 1);
             mbar_init(&qempty[q], CW);
         }
-        mbar_init(efull, CW);
-        mbar_init(eempty, EW);
+        for (int e = 0; e < NBUF; e++) {
+            mbar_init(&efull[e], CW);
+            mbar_init(&eempty[e], EW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    if constexpr (TE) {
+        // the first epilogue warp owns the allocation (and frees it at the end); one CTA per SM
+        // (the stage ring alone takes 192 KiB), so the columns are always free
+        if (warp == CW + 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "n"(EpiCfg<B, CW>::TCOLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+        }
+        tm_fence_before();
+    }
     __syncthreads();
+    uint32_t tbase = 0;
+    if constexpr (TE) {
+        tm_fence_after();
+        tbase = *tmem_slot;
+    }
 
     if (warp == CW) {
         // ------------------------------------------------------- producer
@@ -239,45 +330,90 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
 
     if (warp > CW) {
         // ------------------------------------------------------- epilogue
-        // EW warps copy the deposited tile to the pool (16-byte chunks lane + 32 (ew + EW i):
-        // contiguous 512-byte stores per warp instruction); warp 0 of them also sums the
-        // consumers' ||C_ij||^2 partials (lane l: lane l of every consumer warp in warp order,
-        // then a fixed xor tree; tr over the warps) and writes the block's metadata.
+        // Shared-memory tile: EW warps copy it to the pool (16-byte chunks lane + 32 (ew + EW i):
+        // contiguous 512-byte stores per warp instruction).  TMEM: the warp of sub-partition
+        // qd = warp mod 4 loads the values consumer warps qd and qd + 4 wrote into its lanes
+        // (thread l: lane l's 16 values of each) and stores them in the pool layout (8 rows x
+        // 64 contiguous bytes per warp instruction).  Epilogue warp 0 also sums the consumers'
+        // ||C_ij||^2 partials (lane l: lane l of every consumer warp in warp order, then a fixed
+        // xor tree; tr over the warps) and writes the block's metadata.
         const int ew = warp - CW - 1;
+        const int g8 = lane >> 2, t4 = lane & 3;
         uint32_t eph = 0;
+        int eb = 0;
         const double2 *eb2 = reinterpret_cast<const double2 *>(ebuf);
         for (;;) {
-            mbar_wait(efull, eph);
-            eph ^= 1;
-            const int4 rec = *erec;
+            if (SPAMM_EPI_SLEEP > 0) mbar_wait_sleep(&efull[eb], eph, SPAMM_EPI_SLEEP);
+            else mbar_wait(&efull[eb], eph);
+            if constexpr (TE) tm_fence_after();
+            const int4 rec = erec[eb];
             if (rec.x < 0) break;
             const int seg = rec.x;
             const uint32_t code = (uint32_t)rec.y;
             SPAMM_ASSERT(seg >= 0 && seg < g.c_cap);
             double2 *dst = reinterpret_cast<double2 *>(g.c_pool + (int64_t)seg * TILE);
-            constexpr int NCH = TILE / 2 / 32 / EW;   // chunks per lane
-            constexpr int NU = NCH < 8 ? NCH : 8;     // loads in flight
+            uint32_t tv[TE ? 2 : 1][32];
+            if constexpr (TE) {
+                const int qd = warp & 3;
+                tm_ld32(tbase + ((uint32_t)(32 * qd) << 16) + 64 * eb, tv[0]);
+                tm_ld32(tbase + ((uint32_t)(32 * qd) << 16) + 64 * eb + 32, tv[TE ? 1 : 0]);
+                tm_wait_ld();
+            } else {
+                constexpr int NCH = TILE / 2 / 32 / EW;   // chunks per lane
+                constexpr int NU = NCH < 8 ? NCH : 8;     // loads in flight
 #pragma unroll 1
-            for (int i0 = 0; i0 < NCH; i0 += NU) {
-                double2 v[NU];
+                for (int i0 = 0; i0 < NCH; i0 += NU) {
+                    double2 v[NU];
 #pragma unroll
-                for (int j = 0; j < NU; j++) v[j] = eb2[lane + 32 * (ew + EW * (i0 + j))];
+                    for (int j = 0; j < NU; j++) v[j] = eb2[lane + 32 * (ew + EW * (i0 + j))];
 #pragma unroll
-                for (int j = 0; j < NU; j++) {
-                    const int ch = lane + 32 * (ew + EW * (i0 + j)), r = ch / (B / 2), q = ch % (B / 2);
-                    dst[r * (B / 2) + (q ^ eswz(r) ^ swz(r))] = v[j];   // to the pool layout
+                    for (int j = 0; j < NU; j++) {
+                        const int ch = lane + 32 * (ew + EW * (i0 + j)), r = ch / (B / 2), q = ch % (B / 2);
+                        dst[r * (B / 2) + (q ^ eswz(r) ^ swz(r))] = v[j];   // to the pool layout
+                    }
                 }
             }
             double ss = 0.0, tr = 0.0;
             const int I = morton_i(code), J = morton_j(code);
             if (ew == 0) {
+                const double *es = ess + eb * 32 * CW;
 #pragma unroll
-                for (int w = 0; w < CW; w++) ss += ess[32 * w + lane];
+                for (int w = 0; w < CW; w++) ss += es[32 * w + lane];
                 if (!STORE && I == J)
-                    for (int w = 0; w < CW; w++) tr += etr[w];
+                    for (int w = 0; w < CW; w++) tr += etr[eb * ETR + w];
             }
+            if constexpr (TE) tm_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(eempty);   // this warp's reads of the tile are done
+            if (lane == 0) mbar_arrive(&eempty[eb]);   // this warp's reads of the tile are done
+            if constexpr (TE) {
+                // This warp's columns [16 qd, 16 qd + 16) are one 128-byte line of each row (the
+                // pool swizzle permutes 16-byte chunks inside aligned 128-byte groups).  Lane
+                // (g8, t4) holds chunks t4 (nf = 0) and 4 + t4 (nf = 1) of row 8 mf + g8; after one
+                // exchange with lane ^ 16 (g8 ^ 4) each store instruction writes 4 whole lines:
+                // rows 0..3 of the 8-row group first, then rows 4..7.
+                const bool lo = g8 < 4;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int cw = (warp & 3) + 4 * h;   // the consumer warp whose values tv[h] holds
+                    const int m0 = (cw / WN) * TM, n0 = (cw % WN) * TN;
+#pragma unroll
+                    for (int mf = 0; mf < MF; mf++) {
+                        const int j0 = 4 * (mf * NF), j1 = 4 * (mf * NF + 1);
+                        const double2 v0 = make_double2(__hiloint2double((int)tv[h][j0 + 1], (int)tv[h][j0]),
+                                                        __hiloint2double((int)tv[h][j0 + 3], (int)tv[h][j0 + 2]));
+                        double2 v1 = make_double2(__hiloint2double((int)tv[h][j1 + 1], (int)tv[h][j1]),
+                                                  __hiloint2double((int)tv[h][j1 + 3], (int)tv[h][j1 + 2]));
+                        v1.x = __shfl_xor_sync(0xffffffffu, v1.x, 16);   // now the partner's nf = 1 values
+                        v1.y = __shfl_xor_sync(0xffffffffu, v1.y, 16);
+                        const int rbase = m0 + 8 * mf;
+                        // first: rows rbase + 0..3 (own nf = 0 if g8 < 4, else the partner's nf = 1)
+                        const int ra = rbase + (g8 & 3), rb = ra + 4;
+                        const int ca = n0 + (lo ? 2 * t4 : 8 + 2 * t4), cb = n0 + (lo ? 8 + 2 * t4 : 2 * t4);
+                        dst[ra * (B / 2) + ((ca >> 1) ^ swz(ra))] = lo ? v0 : v1;
+                        dst[rb * (B / 2) + ((cb >> 1) ^ swz(rb))] = lo ? v1 : v0;
+                    }
+                }
+            }
             if (ew == 0) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -287,6 +423,21 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
                     g.c_slot[code] = seg;
                     if (!STORE && I == J) g.trace_part[I] = tr;
                 }
+            }
+            if (++eb == NBUF) {
+                eb = 0;
+                eph ^= 1;
+            }
+        }
+        if constexpr (TE) {
+            // every epilogue warp's last TMEM read is done before the owner frees the columns
+            tm_fence_before();
+            asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EW) : "memory");
+            if (ew == 0) {
+                tm_fence_after();
+                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase),
+                             "n"(EpiCfg<B, CW>::TCOLS)
+                             : "memory");
             }
         }
         return;
@@ -320,6 +471,7 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
 
     int stage = 0, q = 0;
     uint32_t phase = 0, qphase = 0, ephase = 0;
+    int eb = 0;   // epilogue buffer
     CLK(unsigned long long c_full = 0, c_q = 0, c_bnd = 0, n_task = 0, n_seg = 0, c_map = 0, c_ew = 0;
         const unsigned long long c_start = clock64();)
     for (;;) {
@@ -430,36 +582,60 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
             for (int o = 16; o > 0; o >>= 1) trp += __shfl_xor_sync(0xffffffffu, trp, o);
         }
         CLK(unsigned long long c5 = clock64();)
-        mbar_wait(eempty, ephase ^ 1);
+        mbar_wait(&eempty[eb], ephase ^ 1);
         CLK(unsigned long long c6 = clock64(); c_map += c5 - c4; c_ew += c6 - c5;)
-        ephase ^= 1;
+        if constexpr (TE) {
+            // one tcgen05.st of this thread's 16 values into TMEM lane 32 (warp mod 4) + lane
+            tm_fence_after();
+            uint32_t tv[32];
 #pragma unroll
-        for (int mf = 0; mf < MF; mf++)
+            for (int mf = 0; mf < MF; mf++)
 #pragma unroll
-            for (int nf = 0; nf < NF; nf++) {
-                const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
-                reinterpret_cast<double2 *>(ebuf)[r * (B / 2) + ((c >> 1) ^ eswz(r))] =
-                    make_double2(acc[mf][nf][0], acc[mf][nf][1]);
-            }
+                for (int nf = 0; nf < NF; nf++) {
+                    const int j = 4 * (mf * NF + nf);
+                    tv[j] = (uint32_t)__double2loint(acc[mf][nf][0]);
+                    tv[j + 1] = (uint32_t)__double2hiint(acc[mf][nf][0]);
+                    tv[j + 2] = (uint32_t)__double2loint(acc[mf][nf][1]);
+                    tv[j + 3] = (uint32_t)__double2hiint(acc[mf][nf][1]);
+                }
+            tm_st32(tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 64 * eb + 32 * (warp >> 2), tv);
+        } else {
+#pragma unroll
+            for (int mf = 0; mf < MF; mf++)
+#pragma unroll
+                for (int nf = 0; nf < NF; nf++) {
+                    const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
+                    reinterpret_cast<double2 *>(ebuf)[r * (B / 2) + ((c >> 1) ^ eswz(r))] =
+                        make_double2(acc[mf][nf][0], acc[mf][nf][1]);
+                }
+        }
 #pragma unroll
         for (int w = MF / 2; w > 0; w >>= 1)   // fixed pairwise tree
 #pragma unroll
             for (int mf = 0; mf < w; mf++) ssp[mf] += ssp[mf + w];
-        ess[32 * warp + lane] = ssp[0];
-        if (!STORE && diag && lane == 0) etr[warp] = trp;
+        ess[eb * 32 * CW + 32 * warp + lane] = ssp[0];
+        if (!STORE && diag && lane == 0) etr[eb * ETR + warp] = trp;
+        if constexpr (TE) {
+            tm_wait_st();
+            tm_fence_before();
+        }
         __syncwarp();
         if (lane == 0) {
-            if (warp == 0) *erec = make_int4(seg, e.z, 0, 0);
-            mbar_arrive(efull);
+            if (warp == 0) erec[eb] = make_int4(seg, e.z, 0, 0);
+            mbar_arrive(&efull[eb]);
+        }
+        if (++eb == NBUF) {
+            eb = 0;
+            ephase ^= 1;
         }
         CLK(c_bnd += clock64() - c4;)
     }
-    // end of the launch: tell the epilogue warp (after its last tile is read)
-    mbar_wait(eempty, ephase ^ 1);
+    // end of the launch: tell the epilogue warps (once they have read the buffer's last tile)
+    mbar_wait(&eempty[eb], ephase ^ 1);
     __syncwarp();
     if (lane == 0) {
-        if (warp == 0) *erec = make_int4(-1, 0, 0, 0);
-        mbar_arrive(efull);
+        if (warp == 0) erec[eb] = make_int4(-1, 0, 0, 0);
+        mbar_arrive(&efull[eb]);
     }
     CLK(if (lane == 0) {
         atomicAdd(&g_gemm_clk[0], clock64() - c_start);
@@ -476,7 +652,7 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EW), 1) k_leaf_gemm(GemmArgs g)
 template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
 static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
 {
-    constexpr int NT = 32 * (CW + 1 + EW);
+    constexpr int NT = 32 * (CW + 1 + EpiCfg<B, CW>::EW);
     const size_t smem = GemmSmem<B, CW, STAGES>::bytes;
     auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI, TA>;
     static std::atomic<uint64_t> configured{0};

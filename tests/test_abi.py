@@ -39,12 +39,16 @@ def test_no_cpu_fallback_without_gpu():
 
 
 def test_sass_contains_dmma():
-    """The leaf GEMM runs on the FP64 tensor pipe (SASS DMMA), built for sm_100a."""
+    """The leaf GEMM runs on the FP64 tensor pipe (SASS DMMA) with TMA bulk copies (UBLKCP)
+    and, at b = 64, hands finished tiles to its epilogue warps through tensor memory
+    (STTM / LDTM); built for sm_100a."""
     import shutil
     import subprocess
     if not shutil.which("cuobjdump"):
         return
     out = subprocess.run(["cuobjdump", "-sass", sp._build.LIB], capture_output=True, text=True).stdout
     assert "DMMA" in out
+    for op in ("UBLKCP", "STTM", "LDTM"):
+        assert op in out, op
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", sp._build.LIB], capture_output=True,
                                        text=True).stdout
