@@ -78,7 +78,8 @@ __global__ void k_row_fill(const int32_t *slot, int nb, const int32_t *rowptr, i
 template <int B, int NT>
 __global__ void __launch_bounds__(NT) k_spmv(const double *pool, const int32_t *rowptr,
                                              const int32_t *cols, const int32_t *slots,
-                                             const double *v, double *w, int32_t *ticket, int nunits)
+                                             const double *v, double *w, int32_t *ticket, int nunits,
+                                             int rev)
 {
     pdl_wait();
     pdl_trigger();
@@ -87,9 +88,10 @@ __global__ void __launch_bounds__(NT) k_spmv(const double *pool, const int32_t *
     for (;;) {
     if (threadIdx.x == 0) s_unit = atomicAdd(ticket, 1);
     __syncthreads();
-    const int unit = s_unit;
+    const int tk = s_unit;
     __syncthreads();
-    if (unit >= nunits) return;
+    if (tk >= nunits) return;
+    const int unit = rev ? nunits - 1 - tk : tk;   // zig-zag over the power steps (see power_scale)
     const int I = unit / CPR, rg = unit % CPR;
     const int p0 = rowptr[I], p1 = rowptr[I + 1];
     const int r = rg * RG + threadIdx.x / TPR;
@@ -170,6 +172,7 @@ struct SpmvTmaArgs {
     int32_t *ticket;
     int nupper;         // nb * SPT_Q units over the upper parts of the block rows
     int nunits;         // nupper (SYM) or nupper + nb (the lower parts, one unit per row)
+    int rev;            // units in descending order (zig-zag over the power steps)
 };
 
 // ------------------------------------------------- TMA-staged SpMV kernel
@@ -224,8 +227,9 @@ __global__ void __launch_bounds__(288, 1) k_spmv_tma(SpmvTmaArgs g, const int32_
         constexpr int UCH = 32;
         int issued = 0;
         for (;;) {
-            const int unit = atomicAdd(g.ticket, 1);
-            if (unit >= g.nunits) break;
+            const int tk = atomicAdd(g.ticket, 1);
+            if (tk >= g.nunits) break;
+            const int unit = g.rev ? g.nunits - 1 - tk : tk;
             int pb, pend;
             if (unit < g.nupper) {   // a quarter of the row's upper part [up[I], rowptr[I+1])
                 const int I = unit / SPT_Q, q = unit % SPT_Q;
@@ -576,7 +580,7 @@ struct SymSpmv {
 template <int B, bool SYM>
 static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
                              const int32_t *slots, const double *v, double *w, int32_t *ticket, double *part,
-                             double *nrm_part, const SymSpmv &y)
+                             double *nrm_part, const SymSpmv &y, int rev)
 {
     constexpr int STAGES = SptCfg<B>::STAGES;
     const size_t smem = sizeof(double) * STAGES * B * B + STAGES * (2 * sizeof(uint64_t) + sizeof(int4));
@@ -585,7 +589,7 @@ static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, 
         return cudaFuncSetAttribute(k_spmv_tma<B, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }));
     const int nupper = s->nb * SPT_Q;
-    SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, nupper, SYM ? nupper : nupper + s->nb};
+    SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, part, ticket, nupper, SYM ? nupper : nupper + s->nb, rev};
     if (s->dist) {   // the predecessor is a collective: plain launches
         k_spmv_tma<B, SYM><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, y.up, y.mir, y.colpart);
         CKL(ctx);
@@ -613,7 +617,7 @@ __global__ void __launch_bounds__(256) k_row_sumsq(const double *w, double *nrm_
 
 template <int B>
 static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
-                         const int32_t *slots, const double *v, double *w, int32_t *ticket)
+                         const int32_t *slots, const double *v, double *w, int32_t *ticket, int rev)
 {
     // NT = 64: more, smaller units than 256 threads (C2 setup 3.37 -> 3.23 ms, C1 0.74 ->
     // 0.66 ms); the register-light 64-thread CTAs also fill the SMs better
@@ -629,8 +633,8 @@ static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, cons
     const int nunits = s->nb * CPR;
     int grid = ctx->sm_count * occ;
     if (grid > nunits) grid = nunits;
-    if (s->dist) k_spmv<B, NT><<<grid, NT, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits);
-    else CK(launch_pdl(k_spmv<B, NT>, grid, NT, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits));
+    if (s->dist) k_spmv<B, NT><<<grid, NT, 0, ctx->stream>>>(s->pool, rowptr, cols, slots, v, w, ticket, nunits, rev);
+    else CK(launch_pdl(k_spmv<B, NT>, grid, NT, 0, ctx->stream, s->pool, rowptr, cols, slots, v, w, ticket, nunits, rev));
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -651,6 +655,16 @@ static int spmv_sym_mode()
 {
     static const int m = [] {
         const char *e = getenv("SPAMM_SPMV_SYM");
+        return e && *e ? atoi(e) : 1;
+    }();
+    return m;
+}
+
+// SPAMM_SPMV_ZIGZAG=0: every SpMV takes its units in ascending order (A/B runs)
+static int zigzag_mode()
+{
+    static const int m = [] {
+        const char *e = getenv("SPAMM_SPMV_ZIGZAG");
         return e && *e ? atoi(e) : 1;
     }();
     return m;
@@ -717,24 +731,29 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     // row partition: local block rows of w = s v, then all ranks gather the full w and
     // form the norm partials from it (each row is computed by one rank with the
     // single-device arithmetic: bitwise G-invariant)
+    // Zig-zag: consecutive SpMVs take their work units in opposite orders, so each pass
+    // starts on the blocks the previous one touched last, which are still in L2 (s of
+    // C2 is 132 MB, the symmetric half of C3's 165 MB: around the 126 MB of L2).  Only
+    // the schedule changes; every row is summed in the same order: w is bitwise the same.
     auto mv = [&](const double *x, double *y, int32_t *tk) -> spamm_status {
+        const int rev = zigzag_mode() ? (int)((tk - tickets) & 1) : 0;
         if (tma) {
             switch (s->b) {
             case 16: {
-                spamm_status r = sym ? spmv_tma<16, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy)
-                                     : spmv_tma<16, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+                spamm_status r = sym ? spmv_tma<16, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy, rev)
+                                     : spmv_tma<16, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy, rev);
                 ST(r);
                 break;
             }
             case 32: {
-                spamm_status r = sym ? spmv_tma<32, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy)
-                                     : spmv_tma<32, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+                spamm_status r = sym ? spmv_tma<32, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy, rev)
+                                     : spmv_tma<32, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy, rev);
                 ST(r);
                 break;
             }
             default: {
-                spamm_status r = sym ? spmv_tma<64, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy)
-                                     : spmv_tma<64, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy);
+                spamm_status r = sym ? spmv_tma<64, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy, rev)
+                                     : spmv_tma<64, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy, rev);
                 ST(r);
                 break;
             }
@@ -751,9 +770,9 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
             return SPAMM_OK;
         }
         switch (s->b) {
-        case 16: ST(spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk)); break;
-        case 32: ST(spmv<32>(ctx, s, rowptr, cols, slots, x, y, tk)); break;
-        default: ST(spmv<64>(ctx, s, rowptr, cols, slots, x, y, tk)); break;
+        case 16: ST(spmv<16>(ctx, s, rowptr, cols, slots, x, y, tk, rev)); break;
+        case 32: ST(spmv<32>(ctx, s, rowptr, cols, slots, x, y, tk, rev)); break;
+        default: ST(spmv<64>(ctx, s, rowptr, cols, slots, x, y, tk, rev)); break;
         }
         return s->dist ? gather_rows(ctx, s->parts, y, s->b) : SPAMM_OK;
     };
