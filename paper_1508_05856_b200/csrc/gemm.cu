@@ -125,6 +125,12 @@ __device__ __forceinline__ int eswz(int r) { return (r & 1) << 2; }
 #ifndef SPAMM_EPI_TMEM
 #define SPAMM_EPI_TMEM 1
 #endif
+#ifndef SPAMM_SMEM_NBUF
+#define SPAMM_SMEM_NBUF 1   // shared-memory epilogue tiles (b = 32 / 16)
+#endif
+#ifndef SPAMM_B32_STAGES
+#define SPAMM_B32_STAGES 4
+#endif
 #ifndef SPAMM_EPI_SLEEP
 #define SPAMM_EPI_SLEEP 512   // ns between the epilogue warps' probes of the next tile; 0 = spin
 #endif
@@ -139,7 +145,7 @@ template <int B, int CW>
 struct EpiCfg {
     static constexpr bool TE = SPAMM_EPI_TMEM && B == 64 && CW == 8;
     static constexpr int EW = TE ? 4 : SPAMM_EPI_WARPS;   // epilogue warps
-    static constexpr int NBUF = TE ? 4 : 1;               // tiles in flight to the epilogue warps
+    static constexpr int NBUF = TE ? 4 : SPAMM_SMEM_NBUF;  // tiles in flight to the epilogue warps
     static constexpr uint32_t TCOLS = TE ? 64 * NBUF : 0;  // TMEM columns (b32) allocated
 };
 
@@ -153,7 +159,7 @@ struct GemmSmem {
     // the queue, the records and the TMEM base address
     static constexpr int ETR = (CW + 1) & ~1;   // tr partials, padded to keep 16-byte alignment
     static constexpr size_t bytes =
-        sizeof(double) * ((2 * STAGES + (EpiCfg<B, CW>::TE ? 0 : 1)) * TILE + NBUF * (32 * CW + ETR)) +
+        sizeof(double) * ((2 * STAGES + (EpiCfg<B, CW>::TE ? 0 : NBUF)) * TILE + NBUF * (32 * CW + ETR)) +
         sizeof(uint64_t) * (2 * STAGES + 2 * QN + 2 * NBUF) + sizeof(int4) * (QN + NBUF + 1);
     static_assert(bytes <= 227 * 1024, "the leaf GEMM's shared memory exceeds the 227 KiB an sm_100a CTA may use");
 };
@@ -211,8 +217,8 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
     extern __shared__ __align__(1024) double smem[];
     constexpr int QN = GemmSmem<B, CW, STAGES>::QN;
     constexpr int ETR = GemmSmem<B, CW, STAGES>::ETR;
-    double *ebuf = smem + 2 * STAGES * TILE;                  // the epilogue tile (eswz layout; not with TMEM)
-    double *ess = ebuf + (TE ? 0 : TILE);                     // [NBUF][CW][32] lanes' ||C_ij||^2 partials
+    double *ebuf = smem + 2 * STAGES * TILE;                  // [NBUF] epilogue tiles (eswz layout; not with TMEM)
+    double *ess = ebuf + (TE ? 0 : NBUF * TILE);              // [NBUF][CW][32] lanes' ||C_ij||^2 partials
     double *etr = ess + NBUF * 32 * CW;                       // [NBUF][ETR] warps' tr partials (diagonal blocks)
     uint64_t *full = reinterpret_cast<uint64_t *>(etr + NBUF * ETR);
     uint64_t *empty = full + STAGES;
@@ -341,9 +347,10 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
         const int g8 = lane >> 2, t4 = lane & 3;
         uint32_t eph = 0;
         int eb = 0;
-        const double2 *eb2 = reinterpret_cast<const double2 *>(ebuf);
         for (;;) {
-            if (SPAMM_EPI_SLEEP > 0) mbar_wait_sleep(&efull[eb], eph, SPAMM_EPI_SLEEP);
+            // (TMEM ring: 4 tiles deep, the store is off the critical path; the single shared-
+            // memory tile of b = 32 / 16 is waited for by the consumers: spin)
+            if (TE && SPAMM_EPI_SLEEP > 0) mbar_wait_sleep(&efull[eb], eph, SPAMM_EPI_SLEEP);
             else mbar_wait(&efull[eb], eph);
             if constexpr (TE) tm_fence_after();
             const int4 rec = erec[eb];
@@ -359,6 +366,7 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
                 tm_ld32(tbase + ((uint32_t)(32 * qd) << 16) + 64 * eb + 32, tv[TE ? 1 : 0]);
                 tm_wait_ld();
             } else {
+                const double2 *eb2 = reinterpret_cast<const double2 *>(ebuf + eb * TILE);
                 constexpr int NCH = TILE / 2 / 32 / EW;   // chunks per lane
                 constexpr int NU = NCH < 8 ? NCH : 8;     // loads in flight
 #pragma unroll 1
@@ -605,7 +613,7 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
 #pragma unroll
                 for (int nf = 0; nf < NF; nf++) {
                     const int r = m0 + 8 * mf + g8, c = n0 + 8 * nf + 2 * t4;
-                    reinterpret_cast<double2 *>(ebuf)[r * (B / 2) + ((c >> 1) ^ eswz(r))] =
+                    reinterpret_cast<double2 *>(ebuf + eb * TILE)[r * (B / 2) + ((c >> 1) ^ eswz(r))] =
                         make_double2(acc[mf][nf][0], acc[mf][nf][1]);
                 }
         }
@@ -679,7 +687,7 @@ static spamm_status gemm_dispatch(spamm_ctx ctx, int b, const GemmArgs &g)
 {
     switch (b) {
     case 64: return launch_gemm<64, 8, 2, 4, 3, EPI, TA>(ctx, g);
-    case 32: return launch_gemm<32, 4, 2, 2, 4, EPI, TA>(ctx, g);
+    case 32: return launch_gemm<32, 4, 2, 2, SPAMM_B32_STAGES, EPI, TA>(ctx, g);
     case 16: return launch_gemm<16, 1, 1, 1, 4, EPI, TA>(ctx, g);
     default: return set_err(ctx, SPAMM_EINVAL, "b=%d", b);
     }

@@ -6,7 +6,9 @@
 O=gpurun_out/${1:-final}
 mkdir -p $O
 nvidia-smi -q > $O/nvidia_smi.txt 2>&1
+if [ -z "$SKIP_TESTS" ]; then
 python -m pytest tests -m gpu -q -p no:cacheprovider -s --durations=40 > $O/gputest.log 2>&1; echo "rc=$?" >> $O/gputest.log
+fi
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
 python bench.py --steps 20 --warmup 5 > $O/bench_C5.json 2> $O/bench_C5.err
 python bench.py --config C3 --steps 10 --warmup 3 > $O/bench_C3.json 2> $O/bench_C3.err
