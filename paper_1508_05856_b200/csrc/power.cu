@@ -6,8 +6,12 @@
 //   b = 64 : k_spmv_tma<64, SYM> — persistent, warp-specialised TMA ring; with s
 //            checked bitwise symmetric (k_sym_check) only the blocks on and above
 //            the block diagonal are read (SYM), the rest via column sums;
-//   b < 64 : k_spmv — register streaming (the ring's per-block synchronisation
-//            costs more than it saves on 8 / 2 KiB blocks).
+//   b = 32 : k_spmv_blk<32, SYM> — persistent, one warp per staged block, every block's
+//            row (and, SYM, column) part stored on its own and summed per row by
+//            k_spmv_bfix in CSR order; the normalisation folded into the next SpMV
+//            (C2: 3.12 -> 2.01 ms per power iteration);
+//   b = 16 : k_spmv — register streaming (C1, n = 256, is launch-bound).
+// Consecutive SpMVs take their work units in opposite orders (zig-zag, L2 reuse).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -369,6 +373,211 @@ __device__ __forceinline__ void cta_sumsq_part(double x, double *nrm_part)
     }
 }
 
+// ------------------------------------------------- per-block SpMV (b = 32 / 16)
+// The TMA ring above keeps row accumulators across a unit's blocks, and its column pass needs
+// a CTA barrier per block; on 8 / 2 KiB blocks those per-block synchronisations cost more than
+// the data (C2: 34 us per pass with s in L2).  Here every block is handled by ONE warp from its
+// own shard of the ring, and every block's results are stored on their own, so no warp waits
+// for another:
+//   row pass     t[r] = sum_c S_IJ[r, c] v_J[c]   (c ascending)  -> bpart[p],    p = (I, J)
+//   column pass  u[c] = sum_r S_IJ[r, c] v_I[r]   (r ascending)  -> bpart[p'],   p' = (J, I)
+// (the column pass only with SYM, for the blocks above the diagonal; then only those blocks
+// are read: s of C2 is 132 MB, its upper half fits in L2).  k_spmv_bfix then forms
+// w_J = sum over the CSR positions p of row J, ascending, of bpart[p].  Without SYM (an
+// asymmetric s, or the row partition, whose ranks hold only their own rows) every block gets
+// the row pass; for a lower block (J, I) that is sum_c S_JI[c', c] v_I[c] = the column pass
+// of its mirror term by term, so all paths give w bit for bit.
+// Warp w of a CTA takes the CTA's blocks w, w + 8, ... from its shard of BRS stages; a block's
+// position in the CTA's stream does not enter its arithmetic (results are deterministic).
+#ifndef SPAMM_SPB_VTMA
+#define SPAMM_SPB_VTMA 0   // 1: the vector segments staged with the block by bulk copies (C2: 2.38 vs 2.01 ms per power iteration with __ldg)
+#endif
+template <int B> struct SpbCfg {
+    static constexpr int BRS = B == 32 ? 3 : 8;        // stages per consumer warp
+    static constexpr int NST = 8 * BRS;
+    static constexpr int SD = B * B + 2 * B;            // a stage: the block, then x_J, x_I
+    static constexpr size_t smem = sizeof(double) * (NST * SD + 8 * 2 * B) +
+                                   NST * (2 * sizeof(uint64_t) + sizeof(int4));
+};
+
+// x: the input vector; nrm_part (nullable, single device): x is the previous w and the
+// vector is v = x / sqrt(sum of the np partials), the norm formed by every CTA exactly as
+// k_norm_apply forms it (so v is bitwise the vector k_norm_apply would have written).
+template <int B, bool SYM>
+__global__ void __launch_bounds__(288, 1) k_spmv_blk(SpmvTmaArgs g, const int32_t *up, const int32_t *mir,
+                                                     double *bpart, const double *nrm_part, int np)
+{
+    pdl_wait();
+    pdl_trigger();
+    using Cf = SpbCfg<B>;
+    constexpr int TILE = B * B, BRS = Cf::BRS, NST = Cf::NST, SD = Cf::SD;
+    extern __shared__ __align__(1024) double sm[];
+    double *vbuf = sm + NST * SD;                                     // [8][2][B]: v_J, v_I per warp
+    uint64_t *full = reinterpret_cast<uint64_t *>(vbuf + 8 * 2 * B);
+    uint64_t *empty = full + NST;
+    int4 *meta = reinterpret_cast<int4 *>(empty + NST);               // {p (-1: end), I, J, mirror p'}
+    __shared__ double red[256];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int st = 0; st < NST; st++) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {   // ---------------------------------------------- producer
+        int issued = 0;
+        // stage of the CTA's block number i: shard i % 8, slot (i / 8) % BRS
+        auto slot = [&](int i, int &st, uint32_t &ph) {
+            const int k = i >> 3;
+            st = (i & 7) * BRS + k % BRS;
+            ph = (uint32_t)((k / BRS) & 1);
+        };
+        for (;;) {
+            int tk = 0;
+            if (lane == 0) tk = atomicAdd(g.ticket, 1);
+            tk = __shfl_sync(0xffffffffu, tk, 0);
+            if (tk >= g.nunits) break;
+            const int unit = g.rev ? g.nunits - 1 - tk : tk;
+            const int I = unit / SPT_Q, q = unit % SPT_Q;
+            const int r0 = SYM ? up[I] : g.rowptr[I], len = g.rowptr[I + 1] - r0;
+            const int pb = r0 + (q * len) / SPT_Q, pend = r0 + ((q + 1) * len) / SPT_Q;
+            for (int p0 = pb; p0 < pend; p0 += 32) {
+                // the indices of up to 32 blocks, one per lane, then lane 0 issues them
+                const int p = p0 + lane;
+                const int sl = p < pend ? __ldg(g.slots + p) : 0, J = p < pend ? __ldg(g.cols + p) : 0;
+                const int pm = p < pend ? (SYM ? __ldg(mir + p) : p) : 0;
+                const int cnt = pend - p0 < 32 ? pend - p0 : 32;
+                for (int j = 0; j < cnt; j++) {
+                    const int slj = __shfl_sync(0xffffffffu, sl, j), Jj = __shfl_sync(0xffffffffu, J, j);
+                    const int pmj = __shfl_sync(0xffffffffu, pm, j);
+                    if (lane == 0) {
+                        int st;
+                        uint32_t ph;
+                        slot(issued, st, ph);
+                        if (issued >= NST) mbar_wait(&empty[st], ph ^ 1);
+                        meta[st] = make_int4(p0 + j, I, Jj, pmj);
+                        const bool cp = SYM && Jj != I;
+                        double *d = sm + st * SD;
+                        if (SPAMM_SPB_VTMA) {
+                            mbar_expect_tx(&full[st], (TILE + (cp ? 2 : 1) * B) * 8);
+                            bulk_g2s(d, g.pool + (int64_t)slj * TILE, TILE * 8, &full[st]);
+                            bulk_g2s(d + TILE, g.v + (int64_t)Jj * B, B * 8, &full[st]);
+                            if (cp) bulk_g2s(d + TILE + B, g.v + (int64_t)I * B, B * 8, &full[st]);
+                        } else {
+                            mbar_expect_tx(&full[st], TILE * 8);
+                            bulk_g2s(d, g.pool + (int64_t)slj * TILE, TILE * 8, &full[st]);
+                        }
+                    }
+                    issued++;
+                }
+            }
+        }
+        if (lane == 0)
+            for (int w = 0; w < 8; w++) {   // end marker for every shard
+                const int i = issued + ((w - issued) & 7);   // the next block number of shard w
+                int st;
+                uint32_t ph;
+                slot(i, st, ph);
+                if (i >= NST) mbar_wait(&empty[st], ph ^ 1);
+                meta[st] = make_int4(-1, 0, 0, 0);
+                mbar_arrive(&full[st]);
+            }
+        return;
+    }
+    // ----------------------------------------------------------------- consumers
+    // the 256 consumer threads form ||x|| in k_norm_apply's order (256 strided partial sums,
+    // then the halving tree; consumer-only named barrier) while the producer's first copies fly
+    double nrm = 1.0;
+    if (nrm_part) {
+        double t = 0.0;
+        for (int i = tid; i < np; i += 256) t += nrm_part[i];
+        red[tid] = t;
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        for (int k = 128; k > 0; k >>= 1) {
+            if (tid < k) red[tid] += red[tid + k];
+            asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        }
+        nrm = sqrt(red[0]);
+    }
+    double *vJ = vbuf + warp * 2 * B, *vI = vJ + B;
+    for (int k = 0;; k++) {
+        const int st = warp * BRS + k % BRS;
+        mbar_wait(&full[st], (uint32_t)((k / BRS) & 1));
+        const int4 mt = meta[st];
+        if (mt.x < 0) break;
+        const double *tile = sm + st * SD;
+        const bool colpass = SYM && mt.z != mt.y;   // warp-uniform
+        if (lane < B) {
+            const double xj = SPAMM_SPB_VTMA ? tile[TILE + lane] : __ldg(g.v + (int64_t)mt.z * B + lane);
+            vJ[lane] = nrm_part ? xj / nrm : xj;
+            if (colpass) {
+                const double xi = SPAMM_SPB_VTMA ? tile[TILE + B + lane] : __ldg(g.v + (int64_t)mt.y * B + lane);
+                vI[lane] = nrm_part ? xi / nrm : xi;
+            }
+        }
+        __syncwarp();
+        if (lane < B) {
+            double t = 0.0;
+#pragma unroll
+            for (int c = 0; c < B; c++) t = fma(tile[pool_at(lane, c, B)], vJ[c], t);
+            bpart[(int64_t)mt.x * B + lane] = t;
+            if (colpass) {
+                double u = 0.0;
+#pragma unroll
+                for (int r = 0; r < B; r++) u = fma(tile[pool_at(r, lane, B)], vI[r], u);
+                bpart[(int64_t)mt.w * B + lane] = u;
+            }
+        }
+        // generic-proxy reads of the stage (and of vJ / vI) before its refill
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+}
+
+// w[J*b + c] = sum over the CSR positions p of row J, ascending, of bpart[p*b + c]: SL = 256/b
+// lanes per element each sum every SL-th position in order, then a fixed pairwise tree
+// (deterministic); also the CTA's ||w||^2 partial (threads 0..b-1 hold the row: the reduction
+// of k_row_sumsq).
+template <int B>
+__global__ void __launch_bounds__(256) k_spmv_bfix(const int32_t *rowptr, const double *bpart, double *w,
+                                                   double *nrm_part)
+{
+    pdl_wait();
+    pdl_trigger();
+    constexpr int SL = 256 / B;
+    __shared__ double sp[SL][B];
+    const int J = blockIdx.x, c = threadIdx.x % B, q = threadIdx.x / B;
+    const int p1 = rowptr[J + 1];
+    double sl = 0.0;
+    // loads in batches of 8 (independent of the running sum), then added in order
+    for (int p0 = rowptr[J] + q; p0 < p1; p0 += 8 * SL) {
+        double x[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) x[i] = p0 + i * SL < p1 ? bpart[(int64_t)(p0 + i * SL) * B + c] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (p0 + i * SL < p1) sl += x[i];
+    }
+    sp[q][c] = sl;
+    __syncthreads();
+    double t = 0.0;
+    if (q == 0) {
+        double u[SL];
+#pragma unroll
+        for (int i = 0; i < SL; i++) u[i] = sp[i][c];
+#pragma unroll
+        for (int h = SL / 2; h > 0; h >>= 1)
+#pragma unroll
+            for (int i = 0; i < h; i++) u[i] += u[i + h];
+        t = u[0];
+        w[(int64_t)J * B + c] = t;
+    }
+    cta_sumsq_part(t, nrm_part);
+}
+
 // w[J*b + c] = (P0 + P1) + (P2 + P3) over J's upper quarters, then + the column
 // parts of the blocks (I, J), I < J: colpart rows [rowptr[J], up[J]), ascending I.
 // One CTA per block row J: SL = 256/b lanes per output element each sum every SL-th
@@ -604,6 +813,36 @@ static spamm_status spmv_tma(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, 
     return SPAMM_OK;
 }
 
+// w = s v with the per-block kernel (b = 32 / 16), then the fix-up: w rows and their ||w||^2
+// partials (one per block row).  bpart: one b-vector per CSR position.
+// xnrm (nullable): v is x / ||x|| with ||x||^2 = the sum of xnrm's nb partials (fused
+// normalisation, single device)
+template <int B, bool SYM>
+static spamm_status spmv_blk(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
+                             const int32_t *slots, const double *v, double *w, int32_t *ticket,
+                             double *nrm_part, const SymSpmv &y, int rev, const double *xnrm)
+{
+    const size_t smem = SpbCfg<B>::smem;
+    static std::atomic<uint64_t> configured{0};
+    CK(once_per_device(configured, ctx->device, [&]() {
+        return cudaFuncSetAttribute(k_spmv_blk<B, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }));
+    const int nunits = s->nb * SPT_Q;
+    SpmvTmaArgs g{s->pool, rowptr, cols, slots, v, nullptr, ticket, nunits, nunits, rev};
+    if (s->dist) {   // the predecessor is a collective: plain launches
+        k_spmv_blk<B, SYM><<<ctx->sm_count, 288, smem, ctx->stream>>>(g, y.up, y.mir, y.colpart, nullptr, 0);
+        CKL(ctx);
+        k_spmv_bfix<B><<<s->nb, 256, 0, ctx->stream>>>(rowptr, y.colpart, w, nrm_part);
+    } else {
+        CK(launch_pdl(k_spmv_blk<B, SYM>, ctx->sm_count, 288, smem, ctx->stream, g, y.up, y.mir, y.colpart, xnrm,
+                      s->nb));
+        CKL(ctx);
+        CK(launch_pdl(k_spmv_bfix<B>, s->nb, 256, 0, ctx->stream, rowptr, (const double *)y.colpart, w, nrm_part));
+    }
+    CKL(ctx);
+    return SPAMM_OK;
+}
+
 // ||w||^2 partials per block row of the gathered w (row partition), with exactly the
 // reduction of k_spmv_sym_fix (threads 0..b-1 hold the row's entries)
 template <int B>
@@ -650,6 +889,16 @@ static int spmv_tma_mode()
     }();
     return m;
 }
+// SPAMM_SPMV_BLK: 0 = the register-streaming SpMV for b = 32 too, 1 = per-block kernel for
+// b = 32 (default), 2 = also for b = 16 (A/B runs)
+static int spmv_blk_mode()
+{
+    static const int m = [] {
+        const char *e = getenv("SPAMM_SPMV_BLK");
+        return e && *e ? atoi(e) : 1;
+    }();
+    return m;
+}
 // 0 = off, 1 = b = 64 (default), 2 = every leaf size (measurement)
 static int spmv_sym_mode()
 {
@@ -684,17 +933,23 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     // ring dominates (C2 setup 4.3 -> 8.4 ms measured), so those keep the register kernel
     const int tmam = spmv_tma_mode();
     const bool tma = tmam == 2 || (tmam == 1 && s->b == 64);
+    // b = 32 / 16: the per-block kernel (one warp per block, results per block, no CTA barrier)
+    // (b = 16 keeps the register kernel: C1, n = 256, is launch-bound and the fix-up launch
+    // costs more than it saves: 0.67 vs 0.98 ms per power iteration)
+    const bool blk = !tma && (s->b == 32 || (s->b == 16 && spmv_blk_mode() == 2)) && spmv_blk_mode() != 0;
+    const bool ring = tma || blk;   // fix-up + fused normalisation; symmetric read possible
     // symmetric s (checked below, single device): read only the upper half of the blocks
     const int symm = spmv_sym_mode();
-    bool sym = tma && !s->dist && (symm == 2 || (symm == 1 && s->b == 64));
+    bool sym = ring && !s->dist && (symm == 2 || (symm == 1 && (s->b == 64 || blk)));
     double *part = tma ? dalloc<double>(ctx, (int64_t)nb * SPT_Q * s->b) : nullptr;
-    double *nrm_part = tma ? dalloc<double>(ctx, nb) : nullptr;   // ||w||^2 partials, one per block row
-    int32_t *up = tma ? dalloc<int32_t>(ctx, nb) : nullptr, *mir = tma ? dalloc<int32_t>(ctx, nblk) : nullptr;
-    double *colpart = tma ? dalloc<double>(ctx, nblk * s->b) : nullptr;
+    double *nrm_part = ring ? dalloc<double>(ctx, nb) : nullptr;   // ||w||^2 partials, one per block row
+    int32_t *up = ring ? dalloc<int32_t>(ctx, nb) : nullptr, *mir = ring ? dalloc<int32_t>(ctx, nblk) : nullptr;
+    // column parts (TMA ring) / per-block parts (per-block kernel), one b-vector per CSR position
+    double *colpart = ring ? dalloc<double>(ctx, nblk * s->b) : nullptr;
     // every exit (errors included) goes through the one cleanup below
     auto body = [&]() -> spamm_status {
-    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets ||
-        (tma && (!part || !nrm_part || !up || !mir || !colpart)))
+    if (!cnt || !rowptr || !cols || !slots || !v || !w || !c || !tickets || (tma && !part) ||
+        (ring && (!nrm_part || !up || !mir || !colpart)))
         return set_err(ctx, SPAMM_ENOMEM, "power");
     CK(cudaMemsetAsync(tickets, 0, sizeof(int32_t) * (K + 1), ctx->stream));
     int nmv = 0;
@@ -705,7 +960,7 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     k_fill<<<cdiv(n, 256), 256, 0, st>>>(v, n, 1.0 / sqrt((double)n));
     ctx->launches += 4;
     SymSpmv sy{up, mir, colpart};
-    if (tma) {
+    if (ring) {
         // up[] for every TMA SpMV; the mirror positions and the bitwise symmetry check
         // only where the symmetric kernel may run (with a row partition some mirrors
         // live on other ranks)
@@ -735,10 +990,17 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     // starts on the blocks the previous one touched last, which are still in L2 (s of
     // C2 is 132 MB, the symmetric half of C3's 165 MB: around the 126 MB of L2).  Only
     // the schedule changes; every row is summed in the same order: w is bitwise the same.
-    auto mv = [&](const double *x, double *y, int32_t *tk) -> spamm_status {
+    auto mv = [&](const double *x, double *y, int32_t *tk, const double *xnrm = nullptr) -> spamm_status {
         const int rev = zigzag_mode() ? (int)((tk - tickets) & 1) : 0;
-        if (tma) {
-            switch (s->b) {
+        if (ring) {
+            if (blk) {
+                spamm_status r = s->b == 32
+                    ? (sym ? spmv_blk<32, true>(ctx, s, rowptr, cols, slots, x, y, tk, nrm_part, sy, rev, xnrm)
+                           : spmv_blk<32, false>(ctx, s, rowptr, cols, slots, x, y, tk, nrm_part, sy, rev, xnrm))
+                    : (sym ? spmv_blk<16, true>(ctx, s, rowptr, cols, slots, x, y, tk, nrm_part, sy, rev, xnrm)
+                           : spmv_blk<16, false>(ctx, s, rowptr, cols, slots, x, y, tk, nrm_part, sy, rev, xnrm));
+                ST(r);
+            } else switch (s->b) {
             case 16: {
                 spamm_status r = sym ? spmv_tma<16, true>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy, rev)
                                      : spmv_tma<16, false>(ctx, s, rowptr, cols, slots, x, y, tk, part, nrm_part, sy, rev);
@@ -779,7 +1041,7 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
     // one power step: w = s v, then v = w / ||w|| (its ticket zeroed first)
     auto power_step = [&](int32_t *tk) -> spamm_status {
         ST(mv(v, w, tk));
-        if (tma) {   // the fix-up's (or, row partition, k_row_sumsq's) per-block-row partials
+        if (ring) {   // the fix-up's (or, row partition, k_row_sumsq's) per-block-row partials
             const int g = (int)std::min<int64_t>(NRM_CTAS, nb);
             if (s->dist) k_norm_apply<<<g, 256, 0, st>>>(w, n, nrm_part, nb, v);
             else CK(launch_pdl(k_norm_apply, g, 256, 0, st, (const double *)w, n, (const double *)nrm_part, nb, v));
@@ -794,9 +1056,28 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
         ctx->launches++;
         return SPAMM_OK;
     };
-    for (int it = 0; it < K; it++) ST(power_step(tickets + nmv++));
-    ST(mv(v, w, tickets + K));
-    k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
+    if (blk && !s->dist && K > 0) {
+        // per-block kernel on one device: v <- w / ||w|| is folded into the next SpMV (every CTA
+        // forms ||w|| from the fix-up's partials in k_norm_apply's order), so a power step is
+        // two launches; w and v alternate as the SpMV's input and output
+        double *x = v, *y = w;
+        const double *xn = nullptr;
+        for (int it = 0; it < K; it++) {
+            ST(mv(x, y, tickets + nmv++, xn));
+            xn = nrm_part;
+            std::swap(x, y);   // x = w_it
+        }
+        // materialise v_K = w_K / ||w_K||, then w = s v_K and c = v_K . w
+        const int g = (int)std::min<int64_t>(NRM_CTAS, nb);
+        CK(launch_pdl(k_norm_apply, g, 256, 0, st, (const double *)x, n, (const double *)nrm_part, nb, y));
+        ctx->launches++;
+        ST(mv(y, x, tickets + K));
+        k_dot<<<1, 1024, 0, st>>>(y, x, n, c);
+    } else {
+        for (int it = 0; it < K; it++) ST(power_step(tickets + nmv++));
+        ST(mv(v, w, tickets + K));
+        k_dot<<<1, 1024, 0, st>>>(v, w, n, c);
+    }
     CKL(ctx);
     double h = 0;
     ST(fetch1(ctx, c, &h, sizeof(double)));

@@ -461,26 +461,29 @@ def test_ns_nonfinite_reported(ctx):
     assert np.all(np.isfinite(r["t"]))
 
 
-def test_power_scale_sym_and_full_paths_bitwise(ctx):
+@pytest.mark.parametrize("cfg", ["C3", "C2", "C1"])
+def test_power_scale_sym_and_full_paths_bitwise(ctx, cfg):
     """For a symmetric s the upper-triangle SpMV and the full SpMV (used when s is not
     symmetric, and by every rank of a row partition) compute the lower blocks' share in
     the same order, so c is bitwise the same (what keeps the row-partitioned run bitwise
-    equal to the single-device run)."""
+    equal to the single-device run).  C3: the TMA ring (b = 64); C2 / C1: the per-block
+    kernel (b = 32 / 16); the zig-zag schedule must not change c either."""
     code = ("import sys; sys.path.insert(0, %r); import paper_1508_05856_b200 as sp, spamm_inputs as si, torch\n"
-            "c = si.CONFIGS['C3']; kind, p = si.make_input(c); ctx = sp.spamm_ctx_create(0)\n"
-            "S = sp.spamm_build_tree_blocks(ctx, c.n, c.b, *(torch.from_numpy(x).cuda() for x in p))\n"
+            "c = si.CONFIGS[%r]; kind, p = si.make_input(c); ctx = sp.spamm_ctx_create(0)\n"
+            "S = (sp.spamm_build_tree_blocks(ctx, c.n, c.b, *(torch.from_numpy(x).cuda() for x in p))\n"
+            "     if kind == 'blocks' else sp.spamm_build_tree(ctx, torch.from_numpy(p).cuda(), c.b))\n"
             "print(repr(sp.spamm_power_scale(ctx, S, 100)))\n")
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = []
-    for sym in ("1", "0"):
-        p = subprocess.run([sys.executable, "-c", code % root], capture_output=True, text=True, timeout=600,
-                           env={**os.environ, "SPAMM_SPMV_SYM": sym})
+    for env in ({"SPAMM_SPMV_SYM": "1"}, {"SPAMM_SPMV_SYM": "0"}, {"SPAMM_SPMV_ZIGZAG": "0"}):
+        p = subprocess.run([sys.executable, "-c", code % (root, cfg)], capture_output=True, text=True, timeout=600,
+                           env={**os.environ, **env})
         assert p.returncode == 0, p.stderr[-2000:]
         out.append(p.stdout.strip().splitlines()[-1])
-    assert out[0] == out[1], out
+    assert out[0] == out[1] == out[2], out
 
 
 def test_volume_sink_whole_run_matches_oracle(ctx):
