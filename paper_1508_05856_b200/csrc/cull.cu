@@ -539,6 +539,224 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
     }
 }
 
+// ------------------------------------------------------- flat small query
+// For nb <= 128 the whole query is cheaper as a flat test than as a walk: the walk's levels
+// are a chain of dependent global round trips (k_cull_small: ~40 us per product at C2,
+// 1 CTA), while all nb^3 <= 2.1M leaf triples, and the 8^l triples of each level above, can
+// be tested at once on every SM.  Because a parent's n2 is >= each child's (sums of
+// non-negative numbers, rounded monotonically) and rounded products are monotone, a triple
+// passes the test at level l exactly when the walk reaches and keeps it: the walk's
+// survivors at level l are the level-l triples that pass, and its leaf tasks are the
+// passing leaf triples.  Three launches write exactly what the walk writes (level counts,
+// the final records {Morton(i,j), k, group start, group end}, tA/tB/tK in (Morton(i,j), k)
+// order, segments, NSEG, overflow):
+//   k_cullf_count (grid)  tiles of 8 x 8 output pairs (i,j) (Morton code m), their leaf norms
+//                         staged in shared memory; one warp per pair: ballots of the k that
+//                         pass -> pmask[m][w], count -> pcnt[m]; per-CTA counts of the passing
+//                         triples of each level l0..L-1 -> lvl[l][cta]
+//   k_cullf_scan (1 CTA)  level counts, exclusive scan of (tasks, non-empty) over m ->
+//                         ppre[m] = (first task, segment), totals, overflow
+//   k_cullf_emit (grid)   one warp per non-empty pair: its segment, records and tasks
+// (tests/test_gpu_determinism.py: SPAMM_CULL_FLAT=0/1 give the same NS runs bitwise, every
+// product's task, segment and per-level survivor counts included)
+constexpr int FLAT_T = 256;
+
+__global__ void __launch_bounds__(FLAT_T) k_cullf_count(CullArgs g, int l0, uint32_t *pmask, int32_t *pcnt,
+                                                        int32_t *lvl, CullClear clr)
+{
+    pdl_wait();
+    pdl_trigger();
+    __shared__ int sred[FLAT_T / 32];
+    const int nbL = 1 << g.L, W = (nbL + 31) >> 5;
+    const int64_t gtid = blockIdx.x * (int64_t)FLAT_T + threadIdx.x, gstride = (int64_t)gridDim.x * FLAT_T;
+    cull_clear(clr, gtid, gstride);
+    const double T = cull_T(g);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {
+        // leaf pairs in tiles of TI x TI: the TI rows of A's leaf norms and TI columns of B's
+        // (each a run of TI x TI Morton quadtree nodes: contiguous) staged in shared memory
+        __shared__ double sA[8 * 128], sB[8 * 128];
+        const double *an = g.a_n2 + pyr_off(g.L), *bn = g.b_n2 + pyr_off(g.L);
+        const int TI = nbL < 8 ? nbL : 8, tpr = nbL / TI;
+        for (int tile = blockIdx.x; tile < tpr * tpr; tile += gridDim.x) {
+            const int i0 = (tile / tpr) * TI, j0 = (tile % tpr) * TI;
+            __syncthreads();
+            for (int e = threadIdx.x; e < TI * nbL; e += FLAT_T) {
+                const int r = e / nbL, k = e % nbL;
+                sA[e] = an[a_code(g, i0 + r, k)];
+                sB[e] = bn[morton(k, j0 + r)];
+            }
+            __syncthreads();
+            for (int q = warp; q < TI * TI; q += FLAT_T / 32) {
+                const int ri = q / TI, rj = q % TI, i = i0 + ri, j = j0 + rj;
+                const uint32_t m = morton(i, j);
+                const bool rm = rows_meet(g, i, g.L);
+                int c = 0;
+                for (int w = 0; w < W; w++) {
+                    const int k = 32 * w + lane;
+                    const bool kp = rm && k < nbL && keep(sA[ri * nbL + k], sB[rj * nbL + k], T);
+                    const uint32_t bal = __ballot_sync(0xffffffffu, kp);
+                    if (lane == 0) pmask[(int64_t)m * W + w] = bal;
+                    c += __popc(bal);
+                }
+                if (lane == 0) pcnt[m] = c;
+            }
+        }
+    }
+    for (int l = l0; l < g.L; l++) {
+        const int S = 1 << l;
+        const int64_t C = (int64_t)S * S * S;
+        const double *an = g.a_n2 + pyr_off(l), *bn = g.b_n2 + pyr_off(l);
+        int c = 0;
+        for (int64_t idx = gtid; idx < C; idx += gstride) {
+            const uint32_t code = (uint32_t)(idx / S);
+            const int K = (int)(idx % S), I = morton_i(code), J = morton_j(code);
+            if (rows_meet(g, I, l) && keep(an[a_code(g, I, K)], bn[morton(K, J)], T)) c++;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) sred[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < FLAT_T / 32; w++) t += sred[w];
+            lvl[(l - l0) * gridDim.x + blockIdx.x] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// (every count is an integer: the reductions' order does not matter).  The nb^2 <= 16384
+// counts go through shared memory (coalesced global loads and stores, conflict-free warp
+// scans: a per-thread run of consecutive pairs had 16-way bank conflicts, 23 us per launch).
+constexpr int FLAT_PT = 16;
+constexpr size_t FLAT_SMEM = sizeof(int32_t) * 3 * SMALL_T * FLAT_PT;   // counts, prefixes, segment ids
+__global__ void __launch_bounds__(SMALL_T) k_cullf_scan(CullArgs g, int l0, const int32_t *pcnt, int2 *ppre,
+                                                        const int32_t *lvl, int nlvl_cta, int64_t cap_segs,
+                                                        int32_t *cnt)
+{
+    __shared__ int4 sw4[SMALL_T / 32];
+    __shared__ int sred[SMALL_T / 32];
+    extern __shared__ int32_t fsm[];
+    int32_t *sn = fsm, *sp = fsm + SMALL_T * FLAT_PT, *ss = sp + SMALL_T * FLAT_PT;
+    pdl_wait();
+    pdl_trigger();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 64; i += SMALL_T) cnt[i] = 0;
+    const int np = 1 << (2 * g.L), pt = (np + SMALL_T - 1) / SMALL_T;
+    for (int m = tid; m < np; m += SMALL_T) sn[m] = pcnt[m];
+    // level counts: the per-CTA partials summed by the whole CTA
+    for (int li = 0; li < g.L - l0; li++) {
+        int t = 0;
+        for (int c = tid; c < nlvl_cta; c += SMALL_T) t += lvl[li * nlvl_cta + c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) sred[warp] = t;
+        __syncthreads();
+        if (tid == 0) {
+            int u = 0;
+            for (int w = 0; w < SMALL_T / 32; w++) u += sred[w];
+            cnt[l0 + li] = u;
+            if (u > g.cap) cnt[CNT_OVERFLOW] = 1;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    // warp w scans the pairs [w*32*pt, (w+1)*32*pt) in pt rounds of 32 (lane = pair within the
+    // round: conflict-free shared-memory access), after a block scan of the warp totals
+    const int base = warp * 32 * pt;
+    int2 ws = make_int2(0, 0);
+    for (int i = 0; i < pt; i++) {
+        const int e = base + 32 * i + lane, v = e < np ? sn[e] : 0;
+        ws.x += v;
+        ws.y += v > 0 ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ws.x += __shfl_xor_sync(0xffffffffu, ws.x, o);
+        ws.y += __shfl_xor_sync(0xffffffffu, ws.y, o);
+    }
+    if (lane == 0) sw4[warp] = make_int4(ws.x, ws.y, 0, 0);
+    __syncthreads();
+    int2 run = make_int2(0, 0), tot = make_int2(0, 0);
+    for (int w = 0; w < SMALL_T / 32; w++) {
+        if (w < warp) run = make_int2(run.x + sw4[w].x, run.y + sw4[w].y);
+        tot = make_int2(tot.x + sw4[w].x, tot.y + sw4[w].y);
+    }
+    for (int i = 0; i < pt; i++) {
+        const int e = base + 32 * i + lane, v = e < np ? sn[e] : 0;
+        int2 inc = make_int2(v, v > 0 ? 1 : 0);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int ox = __shfl_up_sync(0xffffffffu, inc.x, d), oy = __shfl_up_sync(0xffffffffu, inc.y, d);
+            if (lane >= d) {
+                inc.x += ox;
+                inc.y += oy;
+            }
+        }
+        if (e < np) {
+            sp[e] = run.x + inc.x - v;
+            ss[e] = run.y + inc.y - (v > 0 ? 1 : 0);
+        }
+        run.x += __shfl_sync(0xffffffffu, inc.x, 31);
+        run.y += __shfl_sync(0xffffffffu, inc.y, 31);
+    }
+    __syncthreads();
+    for (int m = tid; m < np; m += SMALL_T) ppre[m] = make_int2(sp[m], ss[m]);
+    if (tid == 0) {
+        cnt[g.L] = tot.x;
+        cnt[CNT_NSEG] = tot.y;
+        if (tot.x > g.cap || tot.y > cap_segs) cnt[CNT_OVERFLOW] = 1;
+    }
+}
+
+__global__ void __launch_bounds__(FLAT_T) k_cullf_emit(CullArgs g, const uint32_t *pmask, const int32_t *pcnt,
+                                                       const int2 *ppre,
+                                                       int4 *rec, int32_t *tA, int32_t *tB, int32_t *tK,
+                                                       int32_t *seg_code, int32_t *seg_start, int32_t *seg_len,
+                                                       const int32_t *cnt)
+{
+    pdl_wait();
+    pdl_trigger();
+    if (cnt[CNT_OVERFLOW]) return;
+    const int nbL = 1 << g.L, W = (nbL + 31) >> 5, lane = threadIdx.x & 31;
+    const int64_t gtid = blockIdx.x * (int64_t)FLAT_T + threadIdx.x, gstride = (int64_t)gridDim.x * FLAT_T;
+    const int nw = (int)(gstride >> 5), np = nbL * nbL;
+    // chunks of 32 pairs per warp: lane l looks at pair m0 + l, then the warp emits the
+    // non-empty ones in order
+    for (int m0 = (int)(gtid >> 5) * 32; m0 < np; m0 += nw * 32) {
+        const int ml = m0 + lane, cl = ml < np ? pcnt[ml] : 0;
+        const int2 pl = ml < np ? ppre[ml] : make_int2(0, 0);
+        uint32_t todo = __ballot_sync(0xffffffffu, cl > 0);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int m = m0 + src, c = __shfl_sync(0xffffffffu, cl, src);
+            const int px = __shfl_sync(0xffffffffu, pl.x, src), py = __shfl_sync(0xffffffffu, pl.y, src);
+            const int i = morton_i((uint32_t)m), j = morton_j((uint32_t)m);
+            const int gs = px, ge = px + c;
+            if (lane == 0) {
+                seg_code[py] = m;
+                seg_start[py] = gs;
+                seg_len[py] = c;
+            }
+            int run = gs;
+            for (int w = 0; w < W; w++) {
+                const uint32_t bal = pmask[(int64_t)m * W + w];
+                if ((bal >> lane) & 1u) {
+                    const int k = 32 * w + lane, pos = run + __popc(bal & ((1u << lane) - 1u));
+                    rec[pos] = make_int4(m, k, gs, ge);
+                    tA[pos] = g.a_slot[a_code(g, i, k)];
+                    tB[pos] = g.b_slot[morton(k, j)];
+                    tK[pos] = k;
+                    SPAMM_ASSERT(g.counts_only || (tA[pos] >= 0 && (tB[pos] >= 0 || g.r1 - g.r0 < (1 << g.L))));
+                }
+                run += __popc(bal);
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------- host side
 void cull_free(spamm_ctx ctx, Cull *cw)
 {
@@ -609,6 +827,26 @@ static bool cull_small_ok(spamm_ctx ctx, const Cull *cw, spamm_mat A)
     return false;
 }
 
+// The flat query (nb <= 128; SPAMM_CULL_FLAT=1 selects it, default off: measured slower than
+// the single-CTA walk — C2 6.89 vs 6.63 ms, C1 2.26 vs 1.99 ms per run; under ncu its three
+// launches take 14 + 14 + 18 us per product against the walk's 41 us in one, and in the
+// step the extra launch gaps cost more than the shorter chain saves) needs the workspace to hold the
+// nb^2 pair records (rec[1]), their pass masks (pre) and the per-CTA level counts (mask);
+// decided from the shape and the capacity alone (the host-driven and the captured step
+// always size the workspace for at least nb^2 records at these sizes).
+static bool cull_flat_ok(spamm_ctx ctx, const Cull *cw, spamm_mat A)
+{
+    static const int mode = [] {
+        const char *e = getenv("SPAMM_CULL_FLAT");
+        return e && *e ? atoi(e) : 0;
+    }();
+    if (!mode || A->nb > 128) return false;
+    const int64_t np = (int64_t)A->nb * A->nb, W = (A->nb + 31) / 32;
+    const int l0 = A->L < INIT_L0 ? A->L : INIT_L0;
+    const int64_t lvl_bytes = (int64_t)sizeof(int32_t) * (A->L - l0) * 4 * ctx->sm_count;
+    return cw->cap >= np && 4 * (cw->cap + 1) >= np * W && cw->cap >= lvl_bytes;
+}
+
 // Enqueue the whole query (no host sync).
 static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau, int r0,
                                  int r1, int transA, const CullClear *clear = nullptr)
@@ -621,6 +859,31 @@ static spamm_status cull_enqueue(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat
     cw->b = A->b;
     CullArgs g{A->norm2, B->norm2, A->slot, B->slot, tau, cw->cap, L, r0, r1, transA, cw->counts_only ? 1 : 0};
     cudaStream_t s = ctx->stream;
+    if (cull_flat_ok(ctx, cw, A)) {
+        // pair records in rec[1], the pass masks in pre, per-CTA level counts in mask
+        const int64_t np = (int64_t)A->nb * A->nb;
+        const int ti = A->nb < 8 ? A->nb : 8;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(np / (ti * ti), 4 * ctx->sm_count));
+        cw->final_buf = 0;
+        int32_t *pcnt = reinterpret_cast<int32_t *>(cw->rec[1]);      // [np] counts, then
+        int2 *ppre = reinterpret_cast<int2 *>(pcnt + (np + 1) / 2 * 2);   // [np] (first task, segment)
+        uint32_t *pmask = reinterpret_cast<uint32_t *>(cw->pre);
+        int32_t *lvl = reinterpret_cast<int32_t *>(cw->mask);
+        static std::atomic<uint64_t> configured{0};
+        CK(once_per_device(configured, ctx->device, [&]() {
+            return cudaFuncSetAttribute(k_cullf_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLAT_SMEM);
+        }));
+        CK(launch_k(ctx, k_cullf_count, grid, FLAT_T, 0, g, l0, pmask, pcnt, lvl, clr));
+        CKL(ctx);
+        CK(launch_k(ctx, k_cullf_scan, 1, SMALL_T, FLAT_SMEM, g, l0, (const int32_t *)pcnt, ppre, (const int32_t *)lvl,
+                    grid, cw->cap_segs, cw->counters));
+        CKL(ctx);
+        CK(launch_k(ctx, k_cullf_emit, grid, FLAT_T, 0, g, (const uint32_t *)pmask, (const int32_t *)pcnt,
+                    (const int2 *)ppre, cw->rec[0], cw->tA, cw->tB, cw->tK, cw->seg_code, cw->seg_start, cw->seg_len,
+                    (const int32_t *)cw->counters));
+        CKL(ctx);
+        return SPAMM_OK;
+    }
     if (cull_small_ok(ctx, cw, A)) {
         cw->final_buf = (L - l0) & 1;
         static std::atomic<uint64_t> configured{0};

@@ -127,27 +127,31 @@ def test_allocators_agree_bitwise(gpu):
 def test_ab_switches_bitwise():
     """The A/B switches change stream and launch ordering only: SPAMM_CONCURRENT_CULL=0/1
     (the Z' cull on the side stream or after the Y' cull), SPAMM_PDL=0/1 (programmatic
-    dependent launch or plain stream order) and SPAMM_CULL_SMALL=0/1 (the single-CTA
-    query or the multi-kernel chain) give the same NS run bitwise (t_k, Y, Z)."""
+    dependent launch or plain stream order), SPAMM_CULL_SMALL=0/1 (the single-CTA
+    query or the multi-kernel chain) and SPAMM_CULL_FLAT=0/1 (the flat small-problem query
+    or the level walk) give the same NS run bitwise (t_k, Y, Z, every product's task,
+    segment and per-level survivor counts)."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
             "import paper_1508_05856_b200 as sp, spamm_inputs as si\n"
             "c = si.CONFIGS['C2']; s = si.kms(c.n, c.rho); ctx = sp.spamm_ctx_create(0)\n"
             "S = sp.spamm_build_tree(ctx, s, c.b); r = sp.spamm_ns_sqrt(ctx, S, c.tau, 12)\n"
-            "h = hashlib.sha1(r['t'].tobytes())\n"
+            "h = hashlib.sha1(r['t'].tobytes() + repr([[p['tasks'], p['segments'], p['level_survivors']]"
+            " for k in r['stats'] for p in k]).encode())\n"
             "for M in (r['Y'], r['Z']):\n"
             "    bi, bj, blk = sp.spamm_export_blocks(ctx, M); o = np.lexsort((bj, bi))\n"
             "    h.update(bi[o].tobytes() + bj[o].tobytes() + blk[o].tobytes())\n"
             "print('hash', h.hexdigest())\n") % ROOT
     seen = {}
-    for conc, pdl, small in (("0", "0", "1"), ("0", "1", "1"), ("1", "0", "1"), ("1", "1", "1"), ("1", "1", "0"),
-                             ("0", "0", "0")):
+    for conc, pdl, small, flat in (("0", "0", "1", "0"), ("0", "1", "1", "0"), ("1", "0", "1", "0"),
+                                   ("1", "1", "1", "0"), ("1", "1", "1", "1"), ("1", "1", "0", "0"),
+                                   ("0", "0", "0", "0"), ("0", "0", "1", "1")):
         p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
                            env={**os.environ, "SPAMM_CONCURRENT_CULL": conc, "SPAMM_PDL": pdl,
-                                "SPAMM_CULL_SMALL": small})
+                                "SPAMM_CULL_SMALL": small, "SPAMM_CULL_FLAT": flat})
         assert p.returncode == 0, p.stderr[-2000:]
-        seen[(conc, pdl, small)] = [l for l in p.stdout.splitlines() if l.startswith("hash")][-1]
+        seen[(conc, pdl, small, flat)] = [l for l in p.stdout.splitlines() if l.startswith("hash")][-1]
     assert len(set(seen.values())) == 1, seen
 
 
