@@ -10,6 +10,10 @@ if [ -z "$SKIP_TESTS" ]; then
 python -m pytest tests -m gpu -q -p no:cacheprovider -s --durations=40 > $O/gputest.log 2>&1; echo "rc=$?" >> $O/gputest.log
 fi
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
+if [ -z "$SKIP_TESTS" ]; then
+(echo "# SPAMM_LIB=libspamm_b200_debug.so (-DSPAMM_DEBUG device bounds asserts) SPAMM_POISON=1 pytest parity/dist/fullsize"
+ SPAMM_LIB=paper_1508_05856_b200/libspamm_b200_debug.so SPAMM_POISON=1 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dist.py tests/test_gpu_fullsize.py -m gpu -q -p no:cacheprovider) > $O/gputest_debug_poison.log 2>&1; echo "rc=$?" >> $O/gputest_debug_poison.log
+fi
 python bench.py --steps 20 --warmup 5 > $O/bench_C5.json 2> $O/bench_C5.err
 python bench.py --config C3 --steps 10 --warmup 3 > $O/bench_C3.json 2> $O/bench_C3.err
 for c in C1 C2; do python bench.py --config $c --steps 20 --warmup 5 > $O/bench_$c.json 2> $O/bench_$c.err; done
