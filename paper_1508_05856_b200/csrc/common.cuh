@@ -331,6 +331,7 @@ static inline cudaError_t once_per_device(std::atomic<uint64_t> &done, int devic
 spamm_status mat_new(spamm_ctx ctx, int64_t n, int b, int64_t cap, spamm_mat *out);
 spamm_status mat_reset_pattern(spamm_ctx ctx, spamm_mat m);     // slot=-1, leaf norms=0
 spamm_status pyramid_build(spamm_ctx ctx, spamm_mat m);           // levels L-1..0 from leaves
+spamm_status pyramid_build_pair(spamm_ctx ctx, spamm_mat m, spamm_mat m2);   // two, one launch per pass
 spamm_status mat_map(spamm_ctx ctx, spamm_mat src, int op, double c, double mu, spamm_mat *out);
 int is_device_ptr(const void *p);
 
@@ -422,6 +423,8 @@ enum { EPI_STORE = 0, EPI_NS_H = 1, EPI_NS_X = 2 };
 spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
                       spamm_mat C, int epi, double *trace_part, const int32_t *seg_order = nullptr,
                       int64_t nseg = -1, int ticket = 0, int transA = 0, bool device_count = false);
+spamm_status gemm_run_pair(spamm_ctx ctx, struct Cull *c1, spamm_mat A1, spamm_mat B1, spamm_mat C1,
+                           struct Cull *c2, spamm_mat A2, spamm_mat B2, spamm_mat C2);
 // diag_fixup with the base slot read from the device (the X cull's segment count) and
 // caller-provided scratch (newslot [nb]); no allocation, no host round trip
 spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, double value, int32_t *newslot,

@@ -199,9 +199,13 @@ __device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&v)[32])
                  : "memory");
 }
 
-template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
-__global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_gemm(GemmArgs g)
+// GRP = 1: two products in one launch (the Y' and Z' products of a captured NS step, both plain
+// stores): tickets [0, n1) are g's segments, [n1, n1 + n2) g2's; the segment's product rides in
+// the queue entry and the epilogue record.  Single device only (no halo / peer tiles).
+template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA, int GRP = 0>
+__global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_gemm(GemmArgs g, GemmArgs g2)
 {
+    static_assert(!GRP || (EPI == EPI_STORE && TA == 0), "grouped launches: plain-store products");
     static_assert(WM * WN == CW, "warp grid");
     constexpr bool STORE = EPI == EPI_STORE || EPI == EPI_STORE_SCALED;
     constexpr int TM = B / WM, TN = B / WN;
@@ -273,27 +277,37 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
         int stage = 0, q = 0;
         uint32_t phase = 0, qphase = 0;
         for (;;) {
-            int seg = 0, start = 0, len = 0;
+            int seg = 0, start = 0, len = 0, pp = 0;
             if (lane == 0) {
                 seg = atomicAdd(g.ticket, 1);
-                if (seg >= (g.nseg_dev ? *g.nseg_dev : g.nseg)) seg = -1;
-                else if (g.seg_order) seg = g.seg_order[seg];
+                const int lim = g.nseg_dev ? *g.nseg_dev : g.nseg;
+                if (seg >= lim) {
+                    seg -= lim;
+                    pp = 1;
+                    if (!GRP || seg >= (g2.nseg_dev ? *g2.nseg_dev : g2.nseg)) seg = -1;
+                } else if (g.seg_order) {
+                    seg = g.seg_order[seg];
+                }
                 int code = 0;
                 if (seg >= 0) {
-                    SPAMM_ASSERT(seg < g.seg_cap);
-                    start = g.seg_start[seg];
-                    len = g.seg_len[seg];
-                    code = g.seg_code[seg];
-                    SPAMM_ASSERT(len > 0 && start >= 0 && start + len <= g.task_cap);
-                    SPAMM_ASSERT((int64_t)code < (int64_t)g.nb * g.nb);
+                    const GemmArgs &gp = (GRP && pp) ? g2 : g;
+                    SPAMM_ASSERT(seg < gp.seg_cap);
+                    start = gp.seg_start[seg];
+                    len = gp.seg_len[seg];
+                    code = gp.seg_code[seg];
+                    SPAMM_ASSERT(len > 0 && start >= 0 && start + len <= gp.task_cap);
+                    SPAMM_ASSERT((int64_t)code < (int64_t)gp.nb * gp.nb);
                 }
                 mbar_wait(&qempty[q], qphase ^ 1);
-                segq[q] = make_int4(seg, len, code, 0);
+                segq[q] = make_int4(seg, len, code, pp);
                 mbar_arrive(&qfull[q]);
             }
             seg = __shfl_sync(0xffffffffu, seg, 0);
             start = __shfl_sync(0xffffffffu, start, 0);
             len = __shfl_sync(0xffffffffu, len, 0);
+            if (GRP) pp = __shfl_sync(0xffffffffu, pp, 0);
+            const int32_t *tAp = (GRP && pp) ? g2.tA : g.tA, *tBp = (GRP && pp) ? g2.tB : g.tB;
+            const double *apool = (GRP && pp) ? g2.a_pool : g.a_pool, *bpool = (GRP && pp) ? g2.b_pool : g.b_pool;
             if (++q == QN) {
                 q = 0;
                 qphase ^= 1;
@@ -301,21 +315,22 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
             if (seg < 0) break;
             for (int t0 = 0; t0 < len; t0 += 32) {
                 const int t = t0 + lane;
-                const int sa = t < len ? g.tA[start + t] : 0;
-                const int sb = t < len ? g.tB[start + t] : 0;
+                const int sa = t < len ? tAp[start + t] : 0;
+                const int sb = t < len ? tBp[start + t] : 0;
                 const int cnt = len - t0 < 32 ? len - t0 : 32;
                 for (int j = 0; j < cnt; j++) {
                     const int a = __shfl_sync(0xffffffffu, sa, j);
                     const int b = __shfl_sync(0xffffffffu, sb, j);
-                    SPAMM_ASSERT(a >= 0 && a < g.a_cap);
-                    SPAMM_ASSERT(b >= 0 ? b < g.b_cap : (g.peer_world > 0 || (-b - 1) < g.halo_cap));
+                    SPAMM_ASSERT(a >= 0 && a < ((GRP && pp) ? g2.a_cap : g.a_cap));
+                    SPAMM_ASSERT(b >= 0 ? b < ((GRP && pp) ? g2.b_cap : g.b_cap)
+                                        : (!GRP && (g.peer_world > 0 || (-b - 1) < g.halo_cap)));
                     if (lane == 0) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         mbar_expect_tx(&full[stage], 2 * TILE_BYTES);
-                        bulk_g2s(smem + (2 * stage) * TILE, g.a_pool + (int64_t)a * TILE, TILE_BYTES, &full[stage]);
+                        bulk_g2s(smem + (2 * stage) * TILE, apool + (int64_t)a * TILE, TILE_BYTES, &full[stage]);
                         const double *bsrc;
                         if (b >= 0) {
-                            bsrc = g.b_pool + (int64_t)b * TILE;
+                            bsrc = bpool + (int64_t)b * TILE;
                         } else if (g.peer_world > 0) {   // the owner's pool (peer memory)
                             const int e = -b - 1;
                             bsrc = g.peer_pool[e % g.peer_world] + (int64_t)(e / g.peer_world) * TILE;
@@ -357,8 +372,9 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
             if (rec.x < 0) break;
             const int seg = rec.x;
             const uint32_t code = (uint32_t)rec.y;
-            SPAMM_ASSERT(seg >= 0 && seg < g.c_cap);
-            double2 *dst = reinterpret_cast<double2 *>(g.c_pool + (int64_t)seg * TILE);
+            const bool p2 = GRP && rec.z;   // grouped launch: the segment's product
+            SPAMM_ASSERT(seg >= 0 && seg < (p2 ? g2.c_cap : g.c_cap));
+            double2 *dst = reinterpret_cast<double2 *>((p2 ? g2.c_pool : g.c_pool) + (int64_t)seg * TILE);
             uint32_t tv[TE ? 2 : 1][32];
             if constexpr (TE) {
                 const int qd = warp & 3;
@@ -426,9 +442,9 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
                 if (lane == 0) {
-                    g.c_leaf_n2[code] = ss;
-                    g.c_coord[seg] = (int32_t)code;
-                    g.c_slot[code] = seg;
+                    (p2 ? g2.c_leaf_n2 : g.c_leaf_n2)[code] = ss;
+                    (p2 ? g2.c_coord : g.c_coord)[seg] = (int32_t)code;
+                    (p2 ? g2.c_slot : g.c_slot)[code] = seg;
                     if (!STORE && I == J) g.trace_part[I] = tr;
                 }
             }
@@ -629,7 +645,7 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
         }
         __syncwarp();
         if (lane == 0) {
-            if (warp == 0) erec[eb] = make_int4(seg, e.z, 0, 0);
+            if (warp == 0) erec[eb] = make_int4(seg, e.z, e.w, 0);
             mbar_arrive(&efull[eb]);
         }
         if (++eb == NBUF) {
@@ -657,12 +673,12 @@ __global__ void __launch_bounds__(32 * (CW + 1 + EpiCfg<B, CW>::EW), 1) k_leaf_g
     })
 }
 
-template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA>
-static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
+template <int B, int CW, int WM, int WN, int STAGES, int EPI, int TA, int GRP = 0>
+static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g, const GemmArgs &g2 = GemmArgs{})
 {
     constexpr int NT = 32 * (CW + 1 + EpiCfg<B, CW>::EW);
     const size_t smem = GemmSmem<B, CW, STAGES>::bytes;
-    auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI, TA>;
+    auto kern = k_leaf_gemm<B, CW, WM, WN, STAGES, EPI, TA, GRP>;
     static std::atomic<uint64_t> configured{0};
     static std::atomic<int> occ_cache{0};
     CK(once_per_device(configured, ctx->device, [&]() {
@@ -677,7 +693,7 @@ static spamm_status launch_gemm(spamm_ctx ctx, const GemmArgs &g)
     int grid = ctx->sm_count * occ;
     if (!g.nseg_dev && grid > g.nseg) grid = g.nseg;
     if (ctx->gemm_grid_cap > 0 && grid > ctx->gemm_grid_cap) grid = ctx->gemm_grid_cap;
-    kern<<<grid, NT, smem, ctx->stream>>>(g);
+    kern<<<grid, NT, smem, ctx->stream>>>(g, g2);
     CKL(ctx);
     return SPAMM_OK;
 }
@@ -693,9 +709,8 @@ static spamm_status gemm_dispatch(spamm_ctx ctx, int b, const GemmArgs &g)
     }
 }
 
-spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
-                      spamm_mat C, int epi, double *trace_part, const int32_t *seg_order, int64_t nseg,
-                      int ticket, int transA, bool device_count)
+static GemmArgs gemm_args(Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo, spamm_mat C,
+                          double *trace_part, const int32_t *seg_order, int64_t nseg, int ticket, bool device_count)
 {
     if (nseg < 0) nseg = cw->nsegs;
     GemmArgs g{A->pool, B->pool, b_halo, cw->tA, cw->tB, cw->seg_code, cw->seg_start, cw->seg_len,
@@ -704,6 +719,14 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
                device_count ? cw->counters + CNT_NSEG : nullptr, cw->peer_world, {},
                A->cap, B->cap, b_halo ? (int64_t)1 << 40 : 0, C->cap, cw->cap, cw->cap_segs, A->nb};
     for (int q = 0; q < cw->peer_world; q++) g.peer_pool[q] = cw->peer_pool[q];
+    return g;
+}
+
+spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const double *b_halo,
+                      spamm_mat C, int epi, double *trace_part, const int32_t *seg_order, int64_t nseg,
+                      int ticket, int transA, bool device_count)
+{
+    const GemmArgs g = gemm_args(cw, A, B, b_halo, C, trace_part, seg_order, nseg, ticket, device_count);
     if (transA) {
         if (epi == EPI_NS_H) return gemm_dispatch<EPI_NS_H, 1>(ctx, A->b, g);
         if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 1>(ctx, A->b, g);
@@ -714,6 +737,24 @@ spamm_status gemm_run(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, const d
     if (epi == EPI_NS_X) return gemm_dispatch<EPI_NS_X, 0>(ctx, A->b, g);
     if (g.alpha != 1.0) return gemm_dispatch<EPI_STORE_SCALED, 0>(ctx, A->b, g);
     return gemm_dispatch<EPI_STORE, 0>(ctx, A->b, g);
+}
+
+// Two plain-store products in one launch (the Y' and Z' GEMMs of a captured NS step): both
+// segment counts read on the device, the launch's ticket in c1's counters.  Each segment is
+// still owned by one CTA and accumulated in ascending k: results equal two launches bitwise.
+spamm_status gemm_run_pair(spamm_ctx ctx, Cull *c1, spamm_mat A1, spamm_mat B1, spamm_mat C1, Cull *c2,
+                           spamm_mat A2, spamm_mat B2, spamm_mat C2)
+{
+    if (c1->alpha != 1.0 || c2->alpha != 1.0 || c1->peer_world || c2->peer_world || A1->b != A2->b)
+        return set_err(ctx, SPAMM_EINVAL, "grouped GEMM: plain single-device products of one leaf size");
+    const GemmArgs g1 = gemm_args(c1, A1, B1, nullptr, C1, nullptr, nullptr, 0, 0, true);
+    const GemmArgs g2 = gemm_args(c2, A2, B2, nullptr, C2, nullptr, nullptr, 0, 0, true);
+    switch (A1->b) {
+    case 64: return launch_gemm<64, 8, 2, 4, 3, EPI_STORE, 0, 1>(ctx, g1, g2);
+    case 32: return launch_gemm<32, 4, 2, 2, SPAMM_B32_STAGES, EPI_STORE, 0, 1>(ctx, g1, g2);
+    case 16: return launch_gemm<16, 1, 1, 1, 4, EPI_STORE, 0, 1>(ctx, g1, g2);
+    default: return set_err(ctx, SPAMM_EINVAL, "b=%d", A1->b);
+    }
 }
 
 // ------------------------------------------------------- LPT segment order

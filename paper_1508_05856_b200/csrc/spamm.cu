@@ -767,6 +767,16 @@ static bool graph_split(int nb)
     return m == 2 || (m == 1 && nb <= 32);
 }
 
+// SPAMM_GRAPH_PAIR=0: the Y' and Z' GEMMs (and pyramids) as separate launches (A/B runs)
+static bool graph_pair()
+{
+    static const int m = [] {
+        const char *e = getenv("SPAMM_GRAPH_PAIR");
+        return e && *e ? atoi(e) : 1;
+    }();
+    return m != 0;
+}
+
 // One device-driven dual step: (Y, Z) -> (Yn, Zn) through the fixed buffers (captured).
 //   main:  X cull (also clears H, Y', Z' patterns and the trace partials) -> X GEMM ->
 //          diagonal fix-up -> pyramid(H) -> t_k -> fork
@@ -806,7 +816,12 @@ static spamm_status graph_step(spamm_ctx ctx, NsGraph *g, spamm_mat Y, spamm_mat
     ST(st);
     CK(cudaEventRecord(ctx->ev[1], ctx->comm_stream));
     CK(cudaStreamWaitEvent(main_s, ctx->ev[1], 0));
-    if (!split) {
+    if (!split && graph_pair()) {
+        // Y' and Z' in one GEMM launch (tickets over both segment lists) and their pyramids in
+        // one launch per pass: two launch boundaries fewer on the step's critical path
+        ST(gemm_run_pair(ctx, c1, Y, H, Yn, c2, H, Z, Zn));
+        ST(pyramid_build_pair(ctx, Yn, Zn));
+    } else if (!split) {
         ST(gemm_run(ctx, c1, Y, H, nullptr, Yn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true));
         ST(pyramid_build(ctx, Yn));
         ST(gemm_run(ctx, c2, H, Z, nullptr, Zn, EPI_STORE, nullptr, nullptr, 0, 0, 0, true));

@@ -306,13 +306,19 @@ __global__ void k_build_scatter(BlockSrc src, int64_t count, const int32_t *slot
 // values the other CTAs stored -- one launch instead of two, the same (c0 + c1) + (c2 + c3)
 // per node, so the same bits.
 template <int LV>
-__global__ void k_pyramid(double *norm2, int lf, int levels, int tail)
+__global__ void k_pyramid(double *norm2, int lf, int levels, int tail, double *norm2b, int grida)
 {
     pdl_wait();
     pdl_trigger();
+    // norm2b (nullable): a second pyramid of the same shape built by CTAs grida.. of the same
+    // launch (the Y' and Z' pyramids of a captured NS step)
+    const bool second = norm2b && (int)blockIdx.x >= grida;
+    if (second) norm2 = norm2b;
+    const int bid = second ? blockIdx.x - grida : blockIdx.x;
+    const int ncta = norm2b ? (second ? gridDim.x - grida : grida) : gridDim.x;
     constexpr int N = 1 << (2 * LV);
     __shared__ double buf[N];
-    const int64_t base = (int64_t)blockIdx.x * N;
+    const int64_t base = (int64_t)bid * N;
     const double *src = norm2 + pyr_off(lf);
     const int64_t cnt = int64_t(1) << (2 * lf);
     for (int i = threadIdx.x; i < N; i += blockDim.x) buf[i] = (base + i < cnt) ? src[base + i] : 0.0;
@@ -341,7 +347,7 @@ __global__ void k_pyramid(double *norm2, int lf, int levels, int tail)
         unsigned long long *done = reinterpret_cast<unsigned long long *>(norm2 + 1);
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) s_last = atomicAdd(done, 1ull) == gridDim.x - 1;
+        if (threadIdx.x == 0) s_last = atomicAdd(done, 1ull) == (unsigned long long)(ncta - 1);
         __syncthreads();
         if (!s_last) return;
         __threadfence();
@@ -361,20 +367,21 @@ __global__ void k_pyramid(double *norm2, int lf, int levels, int tail)
     }
 }
 
-static spamm_status pyramid_kernels(spamm_ctx ctx, spamm_mat m)
+static spamm_status pyramid_kernels(spamm_ctx ctx, spamm_mat m, spamm_mat m2 = nullptr)
 {
     int lf = m->L;
+    double *n2b = m2 ? m2->norm2 : nullptr;
     while (lf > 0) {
         int lv = lf >= 5 ? 5 : lf;
         const int rest = lf - lv, tail = rest <= 5 ? rest : 0;   // the last CTA finishes <= 5 levels
         int64_t cnt = int64_t(1) << (2 * lf);
-        int grid = cdiv(cnt, int64_t(1) << (2 * lv));
+        const int grid = cdiv(cnt, int64_t(1) << (2 * lv)), g2 = m2 ? 2 * grid : grid;
         switch (lv) {
-        case 5: CK(launch_k(ctx, k_pyramid<5>, grid, 256, 0, m->norm2, lf, 5, tail)); break;
-        case 4: CK(launch_k(ctx, k_pyramid<4>, grid, 256, 0, m->norm2, lf, 4, tail)); break;
-        case 3: CK(launch_k(ctx, k_pyramid<3>, grid, 64, 0, m->norm2, lf, 3, tail)); break;
-        case 2: CK(launch_k(ctx, k_pyramid<2>, grid, 16, 0, m->norm2, lf, 2, tail)); break;
-        default: CK(launch_k(ctx, k_pyramid<1>, grid, 4, 0, m->norm2, lf, 1, tail)); break;
+        case 5: CK(launch_k(ctx, k_pyramid<5>, g2, 256, 0, m->norm2, lf, 5, tail, n2b, grid)); break;
+        case 4: CK(launch_k(ctx, k_pyramid<4>, g2, 256, 0, m->norm2, lf, 4, tail, n2b, grid)); break;
+        case 3: CK(launch_k(ctx, k_pyramid<3>, g2, 64, 0, m->norm2, lf, 3, tail, n2b, grid)); break;
+        case 2: CK(launch_k(ctx, k_pyramid<2>, g2, 16, 0, m->norm2, lf, 2, tail, n2b, grid)); break;
+        default: CK(launch_k(ctx, k_pyramid<1>, g2, 4, 0, m->norm2, lf, 1, tail, n2b, grid)); break;
         }
         CKL(ctx);
         lf -= lv + tail;
@@ -383,6 +390,12 @@ static spamm_status pyramid_kernels(spamm_ctx ctx, spamm_mat m)
 }
 
 spamm_status pyramid_build(spamm_ctx ctx, spamm_mat m) { return pyramid_kernels(ctx, m); }
+// two pyramids of the same shape in one launch per pass (bitwise the two separate builds)
+spamm_status pyramid_build_pair(spamm_ctx ctx, spamm_mat m, spamm_mat m2)
+{
+    if (m2->L != m->L) return set_err(ctx, SPAMM_EINVAL, "pyramid pair: shapes differ");
+    return pyramid_kernels(ctx, m, m2);
+}
 
 // ------------------------------------------------------------- build API
 static spamm_status build_common(spamm_ctx ctx, BlockSrc src, int64_t count, int64_t n, int b,
