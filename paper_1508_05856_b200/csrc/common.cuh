@@ -402,6 +402,7 @@ struct CullClear {
     double *z;
     int64_t nz;
 };
+spamm_status cull_clear_enqueue(spamm_ctx ctx, const CullClear &clr);
 // enqueue only (fixed workspace, capacity-sized grids): for CUDA graph capture
 spamm_status cull_enqueue_fixed(spamm_ctx ctx, Cull *cw, spamm_mat A, spamm_mat B, double tau,
                                 const CullClear *clear = nullptr);

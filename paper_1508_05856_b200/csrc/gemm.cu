@@ -913,9 +913,78 @@ spamm_status diag_fixup_async(spamm_ctx ctx, spamm_mat H, int64_t nseg, double v
     return SPAMM_OK;
 }
 
+// The captured step's fix-up in ONE launch (1 CTA): k_diag_assign's scan, then the new blocks
+// filled as k_diag_fill fills them (same values, same leaf norms), then t exactly as trace_256
+// forms it (threads 0..255).  At C1/C2 a launch boundary costs more than this whole kernel.
+__global__ void __launch_bounds__(1024) k_diag_fix1(int32_t *slot_map, int32_t *coord, int nb, int r0, int r1,
+                                                    const int32_t *base_dev, int32_t *newslot, int64_t *count_out,
+                                                    int64_t cap, double *pool, int b, double value, double *leaf_n2,
+                                                    const double *trace_part, double n, double *t_out)
+{
+    pdl_wait();
+    pdl_trigger();
+    __shared__ V1 sw[1024 / 32];
+    __shared__ double sh[256];
+    const int64_t base = *base_dev;
+    int64_t run = 0;
+    for (int i0 = 0; i0 < nb; i0 += 1024) {
+        const int i = i0 + threadIdx.x;
+        const uint32_t code = i < nb ? morton(i, i) : 0;
+        V1 v{(i >= r0 && i < r1 && slot_map[code] < 0) ? 1 : 0};
+        V1 tot;
+        V1 ex = block_excl_scan<V1, 1024>(v, &tot, sw);
+        if (i < nb) {
+            const int32_t sl = v.x ? (int32_t)(base + run + ex.x) : -1;
+            SPAMM_ASSERT(sl < 0 || sl < cap);
+            newslot[i] = sl;
+            if (v.x) {
+                slot_map[code] = sl;
+                coord[sl] = (int32_t)code;
+            }
+        }
+        run += tot.x;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count_out = run;
+    if (run > 0) {   // (CTA-uniform) the new diagonal blocks: value * I
+        for (int i = 0; i < nb; i++) {
+            const int sl = newslot[i];
+            if (sl < 0) continue;
+            double *d = pool + (int64_t)sl * b * b;
+            for (int e = threadIdx.x; e < b * b; e += 1024) d[e] = (e / b == pool_col(e, b)) ? value : 0.0;
+            if (threadIdx.x == 0) {
+                double ss = 0.0;
+                for (int r = 0; r < b; r++) ss += value * value;
+                leaf_n2[morton(i, i)] = ss;
+            }
+        }
+    }
+    // t = (n - sum_i trace_part[i]) / n in trace_256's order
+    double t = 0.0;
+    if (threadIdx.x < 256)
+        for (int i = threadIdx.x; i < nb; i += 256) t += trace_part[i];
+    if (threadIdx.x < 256) sh[threadIdx.x] = t;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *t_out = (n - sh[0]) / n;
+}
+
 spamm_status diag_fixup_dev(spamm_ctx ctx, spamm_mat H, const int32_t *nseg_dev, double value, int32_t *newslot,
                             int64_t *dcount, const double *trace_part, double *t_out)
 {
+    static const int one = [] {
+        const char *e = getenv("SPAMM_DIAG_ONE");
+        return e && *e ? atoi(e) : 1;
+    }();
+    if (one && trace_part) {
+        CK(launch_k(ctx, k_diag_fix1, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, nseg_dev, newslot, dcount,
+                    H->cap, H->pool, H->b, value, H->norm2 + pyr_off(H->L), trace_part, (double)H->n, t_out));
+        CKL(ctx);
+        return SPAMM_OK;
+    }
     CK(launch_k(ctx, k_diag_assign<1024>, 1, 1024, 0, H->slot, H->coord, H->nb, H->r0, H->r1, (int64_t)0, newslot,
                 dcount, nseg_dev, H->cap));
     CKL(ctx);

@@ -767,6 +767,16 @@ static bool graph_split(int nb)
     return m == 2 || (m == 1 && nb <= 32);
 }
 
+// SPAMM_GRAPH_SIDE_CLEAR=0: the pattern clearing inside the X cull's (single-CTA) kernel
+static bool graph_side_clear()
+{
+    static const int m = [] {
+        const char *e = getenv("SPAMM_GRAPH_SIDE_CLEAR");
+        return e && *e ? atoi(e) : 1;
+    }();
+    return m != 0;
+}
+
 // SPAMM_GRAPH_PAIR=0: the Y' and Z' GEMMs (and pyramids) as separate launches (A/B runs)
 static bool graph_pair()
 {
@@ -790,8 +800,23 @@ static spamm_status graph_step(spamm_ctx ctx, NsGraph *g, spamm_mat Y, spamm_mat
     const int nb = Y->nb;
     CullClear clr{{H->slot, Yn->slot, Zn->slot}, {H->norm2, Yn->norm2, Zn->norm2}, (int64_t)nb * nb,
                   pyr_size(Y->L), g->trace_part, nb};
-    // X = Z (x)_tau Y -> H = 1/2 (3I - X), tr X partials, absent diagonal blocks 1.5 I
-    ST(cull_enqueue_fixed(ctx, c0, Z, Y, g->tau, &clr));
+    // X = Z (x)_tau Y -> H = 1/2 (3I - X), tr X partials, absent diagonal blocks 1.5 I.  The
+    // H, Y', Z' patterns are cleared by a kernel on the side stream beside the X cull (they are
+    // none of its inputs); the X GEMM, which writes H, waits for it.
+    if (graph_side_clear() && nb >= 64) {   // (C1, nb = 16: the fork costs more than the clear)
+        CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev[2], 0));
+        const cudaStream_t ms = ctx->stream;
+        ctx->stream = ctx->comm_stream;
+        const spamm_status cs = cull_clear_enqueue(ctx, clr);
+        ctx->stream = ms;
+        ST(cs);
+        CK(cudaEventRecord(ctx->ev[2], ctx->comm_stream));
+        ST(cull_enqueue_fixed(ctx, c0, Z, Y, g->tau, nullptr));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev[2], 0));
+    } else {
+        ST(cull_enqueue_fixed(ctx, c0, Z, Y, g->tau, &clr));
+    }
     c0->alpha = 1.0;
     ST(gemm_run(ctx, c0, Z, Y, nullptr, H, EPI_NS_H, g->trace_part, nullptr, 0, 0, 0, true));
     ST(diag_fixup_dev(ctx, H, c0->counters + CNT_NSEG, 1.5, g->newslot, g->hadd, g->trace_part, ctx->dscratch));

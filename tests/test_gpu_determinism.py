@@ -129,8 +129,9 @@ def test_ab_switches_bitwise():
     (the Z' cull on the side stream or after the Y' cull), SPAMM_PDL=0/1 (programmatic
     dependent launch or plain stream order), SPAMM_CULL_SMALL=0/1 (the single-CTA
     query or the multi-kernel chain) and SPAMM_CULL_FLAT=0/1 (the flat small-problem query
-    or the level walk) give the same NS run bitwise (t_k, Y, Z, every product's task,
-    segment and per-level survivor counts)."""
+    or the level walk), SPAMM_GRAPH_PAIR=0/1 (the captured step's Y' and Z' GEMMs and
+    pyramids grouped or not) and SPAMM_GRAPH_SIDE_CLEAR=0/1 give the same NS run bitwise
+    (t_k, Y, Z, every product's task, segment and per-level survivor counts)."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
@@ -152,6 +153,12 @@ def test_ab_switches_bitwise():
                                 "SPAMM_CULL_SMALL": small, "SPAMM_CULL_FLAT": flat})
         assert p.returncode == 0, p.stderr[-2000:]
         seen[(conc, pdl, small, flat)] = [l for l in p.stdout.splitlines() if l.startswith("hash")][-1]
+    # the captured step's grouped Y'/Z' GEMM + pyramids and its side-stream pattern clearing
+    for pair, side in (("0", "1"), ("1", "0"), ("0", "0")):
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                           env={**os.environ, "SPAMM_GRAPH_PAIR": pair, "SPAMM_GRAPH_SIDE_CLEAR": side})
+        assert p.returncode == 0, p.stderr[-2000:]
+        seen[("pair", pair, side)] = [l for l in p.stdout.splitlines() if l.startswith("hash")][-1]
     assert len(set(seen.values())) == 1, seen
 
 
