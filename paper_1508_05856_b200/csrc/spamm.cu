@@ -792,7 +792,8 @@ static bool graph_pair()
 //          diagonal fix-up -> pyramid(H) -> t_k -> fork
 //   main:  Y' cull [-> Y' GEMM (half the SMs) -> pyramid(Y')]   } concurrent branches
 //   side:  Z' cull [-> Z' GEMM (half the SMs) -> pyramid(Z')]   } ([..]: split mode)
-//   join [-> Y' GEMM -> pyramid(Y') -> Z' GEMM -> pyramid(Z')] -> step record.
+//   join [-> Y' and Z' GEMMs in one launch -> both pyramids in one launch] -> step record.
+// For nb >= 64 the H, Y', Z' pattern clearing runs on the side stream beside the X cull.
 static spamm_status graph_step(spamm_ctx ctx, NsGraph *g, spamm_mat Y, spamm_mat Z, spamm_mat Yn, spamm_mat Zn)
 {
     Cull *c0 = ctx->cw[0], *c1 = ctx->cw[1], *c2 = ctx->cw[2];
