@@ -104,10 +104,11 @@ __global__ void k_cull_reset(int32_t *cnt, int ncnt, int32_t *flags, int64_t nfl
     cull_clear(clr, i0, stride);
 }
 
-// the init level for a CTA of 1024 threads (k_cull_init and k_cull_small)
-__device__ __forceinline__ void cull_init_body(const CullArgs &g, int l0, int4 *rec, int32_t *cnt)
+// the init level for a CTA of 1024 threads (k_cull_init and k_cull_small); returns the
+// level's survivor count to every thread
+__device__ __forceinline__ int cull_init_body(const CullArgs &g, int l0, int4 *rec, int32_t *cnt)
 {
-    __shared__ int sw[32];
+    __shared__ V1 sw[32];
     __shared__ int gpre[(1 << (2 * INIT_L0)) + 1];   // exclusive prefix at each group (I,J) start
     const int S = 1 << l0;
     const int C = S * S * S;
@@ -119,38 +120,26 @@ __device__ __forceinline__ void cull_init_body(const CullArgs &g, int l0, int4 *
     for (int e = 0; e < ipt; e++) {
         const int idx = base + e;
         if (idx < C) {
-            const uint32_t code = idx / S;
-            const int K = idx % S, I = morton_i(code), J = morton_j(code);
+            const uint32_t code = idx >> l0;        // idx = code * S + K
+            const int K = idx & (S - 1), I = morton_i(code), J = morton_j(code);
             if (rows_meet(g, I, l0) && keep(an[a_code(g, I, K)], bn[morton(K, J)], T)) f |= 1u << e;
         }
     }
     const int mycount = __popc(f);
-    // block exclusive scan of mycount
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int inc = mycount;
-    for (int d = 1; d < 32; d <<= 1) {
-        int o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-    }
-    if (lane == 31) sw[warp] = inc;
-    __syncthreads();
-    int wpre = 0, tot = 0;
-    for (int w = 0; w < 32; w++) {
-        if (w < warp) wpre += sw[w];
-        tot += sw[w];
-    }
-    const int ex = wpre + inc - mycount;
+    V1 vtot;
+    const int ex = block_excl_scan<V1, 1024>(V1{mycount}, &vtot, sw).x;
+    const int tot = vtot.x;
     for (int e = 0; e < ipt; e++) {
         const int idx = base + e;
-        if (idx < C && idx % S == 0) gpre[idx / S] = ex + __popc(f & ((1u << e) - 1u));
+        if (idx < C && (idx & (S - 1)) == 0) gpre[idx >> l0] = ex + __popc(f & ((1u << e) - 1u));
     }
     if (threadIdx.x == 0) gpre[S * S] = tot;
     __syncthreads();
     int run = ex;
     for (int e = 0; e < ipt; e++) {
         if (f & (1u << e)) {
-            const int idx = base + e, code = idx / S;
-            if (run < g.cap) rec[run] = make_int4(code, idx % S, gpre[code], gpre[code + 1]);
+            const int idx = base + e, code = idx >> l0;
+            if (run < g.cap) rec[run] = make_int4(code, idx & (S - 1), gpre[code], gpre[code + 1]);
             run++;
         }
     }
@@ -158,6 +147,7 @@ __device__ __forceinline__ void cull_init_body(const CullArgs &g, int l0, int4 *
         cnt[l0] = tot;
         if (tot > g.cap) cnt[CNT_OVERFLOW] = 1;
     }
+    return tot;
 }
 
 __global__ void __launch_bounds__(1024) k_cull_init(CullArgs g, int l0, int4 *rec, int32_t *cnt)
@@ -439,12 +429,15 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
     __syncthreads();
     int4 *rec[2] = {rec0, rec1};
     int cur = 0;
-    cull_init_body(g, l0, rec[cur], cnt);
+    // every thread holds each level's count (the scan totals are block-wide), so neither
+    // the count nor the overflow flag (set exactly when a count exceeds cap; the counters
+    // were zeroed above) is re-read from global memory between phases
+    int nl = cull_init_body(g, l0, rec[cur], cnt);
     __syncthreads();
     const double T = cull_T(g);
     for (int l = l0; l < g.L; l++) {
-        if (cnt[CNT_OVERFLOW]) return;
-        const int n = clamp_n(cnt, l, g.cap);
+        if (nl > g.cap) return;
+        const int n = nl;
         const double *an = g.a_n2 + pyr_off(l + 1), *bn = g.b_n2 + pyr_off(l + 1);
         const bool staged = n <= SMALL_STAGE;
         int4 *const pre = staged ? pre_s : pre_g;
@@ -476,14 +469,14 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
             }
             carry = vadd(carry, tot);
         }
+        const int total = carry.x + carry.y + carry.z + carry.w;
         if (threadIdx.x == 0) {
             pre[n] = carry;
-            const int total = carry.x + carry.y + carry.z + carry.w;
             cnt[l + 1] = total;
             if (total > g.cap) cnt[CNT_OVERFLOW] = 1;
         }
         __syncthreads();
-        if (cnt[CNT_OVERFLOW]) return;
+        if (total > g.cap) return;
         if (l + 1 == g.L) {
             for (int t = threadIdx.x; t < n; t += SMALL_T)
                 cull_scatter_one<true>(g, rec[cur], mask, pre, t, rec[cur ^ 1], tA, tB, tK);
@@ -492,10 +485,11 @@ __global__ void __launch_bounds__(SMALL_T) k_cull_small(CullArgs g, int l0, int4
                 cull_scatter_one<false>(g, rec[cur], mask, pre, t, rec[cur ^ 1], nullptr, nullptr, nullptr);
         }
         cur ^= 1;
+        nl = total;
         __syncthreads();
     }
-    if (cnt[CNT_OVERFLOW]) return;
-    const int n = clamp_n(cnt, g.L, g.cap);
+    if (nl > g.cap) return;
+    const int n = nl;
     if (l0 == g.L) {   // the init level is the leaf level: tasks straight from the records
         for (int t = threadIdx.x; t < n; t += SMALL_T) {
             const int4 r = rec[cur][t];

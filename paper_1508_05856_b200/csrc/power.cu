@@ -14,6 +14,8 @@
 // Consecutive SpMVs take their work units in opposite orders (zig-zag, L2 reuse).
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "scan.cuh"
 #include "tma.cuh"
@@ -878,6 +880,152 @@ static spamm_status spmv(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, cons
     return SPAMM_OK;
 }
 
+// ------------------------------------------------- tiny s: the whole iteration on one cluster
+// For the smallest problems (C1: n = 256, 512 KB of blocks) every launch of the power
+// iteration is latency: 2 launches per step, ~6.4 us.  Here a cluster of PC_CN CTAs keeps s
+// resident in shared memory for all K + 1 SpMVs (CTA q owns the block rows I = q mod PC_CN)
+// and exchanges w through distributed shared memory, one cluster barrier per step.  The
+// arithmetic is exactly that of the launch loop it replaces (k_spmv: per lane, E-term fma
+// chains added to acc over the row's blocks in CSR order, then the TPR lanes' xor tree;
+// k_normalize: 1024 fma partials and its halving tree; k_dot likewise), so c is bitwise the
+// same (tests/test_gpu_parity.py::test_power_cluster_bitwise).
+constexpr int PC_CN = 8;     // CTAs per cluster (portable size)
+constexpr int PC_NT = 256;   // threads per CTA
+
+template <int B>
+__global__ void __launch_bounds__(PC_NT) k_power_cluster(const double *pool, const int32_t *rowptr,
+                                                         const int32_t *cols, const int32_t *slots, int nb,
+                                                         int K, double v0, double *c_out)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    constexpr int E = B >= 32 ? 4 : 1, TPR = B / E;
+    const int q = (int)cl.block_rank();
+    const int n = nb * B;
+    extern __shared__ __align__(16) double pc_smem[];
+    double *red = pc_smem;                 // [1024] reduction slots
+    double *v = red + 1024;                // [n]
+    double *wb[2] = {v + n, v + 2 * n};    // [n] each: w, written by every CTA of the cluster
+    double *sb = v + 3 * n;                // this CTA's blocks, its rows in order, CSR order inside
+    // stage the blocks of the owned rows
+    int nloc = 0;
+    for (int I = q; I < nb; I += PC_CN) {
+        const int p0 = rowptr[I], p1 = rowptr[I + 1];
+        for (int p = p0; p < p1; p++) {
+            const double *src = pool + (int64_t)slots[p] * B * B;
+            double *dst = sb + (int64_t)(nloc + p - p0) * B * B;
+            for (int e = threadIdx.x; e < B * B; e += PC_NT) dst[e] = src[e];
+        }
+        nloc += p1 - p0;
+    }
+    for (int i = threadIdx.x; i < n; i += PC_NT) v[i] = v0;
+    const int nown = (nb - q + PC_CN - 1) / PC_CN;
+    const int items = nown * B * TPR;   // (row, lane) pairs: a multiple of 32
+    __syncthreads();
+    for (int it = 0; it <= K; it++) {
+        double *w = wb[it & 1];
+        // w rows of the owned block rows: k_spmv's per-lane arithmetic and xor tree
+        for (int base = 0; base < items; base += PC_NT) {
+            const int x = base + threadIdx.x;
+            double acc = 0.0;
+            int I = 0, r = 0;
+            if (x < items) {
+                const int lrow = x / TPR, t = x % TPR;
+                const int li = lrow / B;
+                r = lrow % B;
+                I = q + li * PC_CN;
+                // local block index of row I's first block: the rows before it, in order
+                int lb = 0;
+                for (int J = q; J < I; J += PC_CN) lb += rowptr[J + 1] - rowptr[J];
+                const int p0 = rowptr[I], p1 = rowptr[I + 1];
+                const int e0 = r * B + t * E;
+                int lc[E];
+#pragma unroll
+                for (int i = 0; i < E; i++) lc[i] = pool_col(e0 + i, B);
+                for (int p = p0; p < p1; p++) {
+                    const double *blk = sb + (int64_t)(lb + p - p0) * B * B + e0;
+                    const double *vv = v + (int64_t)cols[p] * B;
+                    double sdot = 0.0;
+#pragma unroll
+                    for (int i = 0; i < E; i++) sdot = fma(blk[i], vv[lc[i]], sdot);
+                    acc += sdot;
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (x < items && (x % TPR) == 0) {
+                const int gi = I * B + r;
+                for (int d = 0; d < PC_CN; d++) cl.map_shared_rank(w, d)[gi] = acc;
+            }
+        }
+        cl.sync();   // every w row has landed in every CTA (release / acquire)
+        // it < K: v = w / ||w|| (k_normalize); it == K: c = v . w (k_dot)
+        for (int t = threadIdx.x; t < 1024; t += PC_NT) {
+            double a = 0.0;
+            for (int i = t; i < n; i += 1024) a = it < K ? fma(w[i], w[i], a) : fma(v[i], w[i], a);
+            red[t] = a;
+        }
+        __syncthreads();
+        for (int k = 512; k > 0; k >>= 1) {
+            for (int t = threadIdx.x; t < k; t += PC_NT) red[t] += red[t + k];
+            __syncthreads();
+        }
+        if (it < K) {
+            const double nrm = sqrt(red[0]);
+            for (int i = threadIdx.x; i < n; i += PC_NT) v[i] = w[i] / nrm;
+            __syncthreads();
+        } else if (q == 0 && threadIdx.x == 0) {
+            *c_out = red[0];
+        }
+    }
+}
+
+// bytes of shared memory k_power_cluster<B> needs for s in the worst case (dense rows), or
+// 0 if it is not eligible
+static size_t power_cluster_smem(const spamm_mat s)
+{
+    const int64_t nb = s->nb, n = s->n, b = s->b;
+    const int64_t rows = (nb + PC_CN - 1) / PC_CN;
+    const int64_t bytes = sizeof(double) * (1024 + 3 * n + rows * nb * b * b);
+    return bytes <= 200 * 1024 ? (size_t)bytes : 0;
+}
+
+// SPAMM_POWER_CLUSTER=0: the launch loop even where the cluster kernel fits (A/B, tests)
+static bool power_cluster_mode()
+{
+    static const int m = [] {
+        const char *e = getenv("SPAMM_POWER_CLUSTER");
+        return e && *e ? atoi(e) : 1;
+    }();
+    return m != 0;
+}
+
+template <int B>
+static spamm_status power_cluster(spamm_ctx ctx, spamm_mat s, const int32_t *rowptr, const int32_t *cols,
+                                  const int32_t *slots, int K, double v0, double *c, size_t smem)
+{
+    static std::atomic<uint64_t> configured{0};
+    CK(once_per_device(configured, ctx->device, [&]() {
+        return cudaFuncSetAttribute(k_power_cluster<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    }));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(PC_CN);
+    cfg.blockDim = dim3(PC_NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = PC_CN;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_power_cluster<B>, s->pool, rowptr, cols, slots, (int)s->nb, K, v0, c));
+    ctx->launches++;
+    CKL(ctx);
+    return SPAMM_OK;
+}
+
 // SPAMM_SPMV_TMA=0 selects the register-streaming SpMV (k_spmv) instead of the TMA
 // ring; SPAMM_SPMV_SYM=0 disables the symmetric (upper-half) SpMV
 // 0 = off, 1 = b = 64 (default), 2 = every leaf size (measurement)
@@ -1056,7 +1204,14 @@ spamm_status power_scale(spamm_ctx ctx, spamm_mat s, int K, double *c_host)
         ctx->launches++;
         return SPAMM_OK;
     };
-    if (blk && !s->dist && K > 0) {
+    const size_t pcs = (!ring && !s->dist && K > 0 && (s->b == 16 || s->b == 32) && power_cluster_mode())
+                           ? power_cluster_smem(s) : 0;
+    if (pcs) {
+        // tiny s: the whole iteration (v0 as k_fill's) on one cluster, s resident in shared memory
+        const double v0 = 1.0 / sqrt((double)n);
+        ST(s->b == 16 ? power_cluster<16>(ctx, s, rowptr, cols, slots, K, v0, c, pcs)
+                      : power_cluster<32>(ctx, s, rowptr, cols, slots, K, v0, c, pcs));
+    } else if (blk && !s->dist && K > 0) {
         // per-block kernel on one device: v <- w / ||w|| is folded into the next SpMV (every CTA
         // forms ||w|| from the fix-up's partials in k_norm_apply's order), so a power step is
         // two launches; w and v alternate as the SpMV's input and output

@@ -50,9 +50,13 @@ struct ScanTiles {
 
 // Block-wide exclusive scan of one value per thread; returns the thread's
 // exclusive prefix and writes the block total to *total (all threads).
+// Warp-inclusive shuffle scan, then warp 0 scans the THREADS/32 warp totals in
+// place (inclusive over warps), so a thread reads two entries instead of looping
+// over all warps: integer sums, so the result does not depend on the grouping.
 template <typename T, int THREADS>
 __device__ __forceinline__ T block_excl_scan(T v, T *total, T *smem_warp /*[THREADS/32]*/)
 {
+    constexpr int NW = THREADS / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     T inc = v;
 #pragma unroll
@@ -62,16 +66,20 @@ __device__ __forceinline__ T block_excl_scan(T v, T *total, T *smem_warp /*[THRE
     }
     if (lane == 31) smem_warp[warp] = inc;
     __syncthreads();
-    T wpre = vzero(v), tot = vzero(v);
+    if (NW > 1 && warp == 0) {
+        T s = lane < NW ? smem_warp[lane] : vzero(v);
 #pragma unroll
-    for (int w = 0; w < THREADS / 32; w++) {
-        T s = smem_warp[w];
-        if (w < warp) wpre = vadd(wpre, s);
-        tot = vadd(tot, s);
+        for (int d = 1; d < NW; d <<= 1) {
+            T o = vshfl_up(s, d);
+            if (lane >= d) s = vadd(s, o);
+        }
+        if (lane < NW) smem_warp[lane] = s;
     }
     __syncthreads();
-    *total = tot;
-    // exclusive = inclusive - v  (computed as wpre + inclusive-of-previous-lanes)
+    const T wpre = warp > 0 ? smem_warp[warp - 1] : vzero(v);
+    *total = smem_warp[NW - 1];
+    __syncthreads();   // smem_warp may be reused by the next call
+    // exclusive = wpre + inclusive-of-previous-lanes
     T ex = vshfl_up(inc, 1);
     if (lane == 0) ex = vzero(v);
     return vadd(wpre, ex);

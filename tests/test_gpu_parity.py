@@ -546,3 +546,61 @@ def test_async_host_io_equals_sync(ctx):
     with pytest.raises(sp().SpammError) as e:
         sp().spamm_build_tree_staged(ctx, 4096, 64, h1)
     assert e.value.code == 1
+
+
+@pytest.mark.parametrize("case", ["C1", "b16_holes", "b32_reg"])
+def test_power_cluster_bitwise(ctx, case):
+    """Tiny s (C1: n = 256): the whole power iteration runs on one thread-block cluster
+    with s resident in shared memory (power.cu k_power_cluster).  Its arithmetic is the
+    launch loop's (register SpMV, k_normalize, k_dot), so c is bitwise the same with
+    SPAMM_POWER_CLUSTER=0/1, and matches the oracle's power iteration (reading L12).
+    Cases: the C1 input; n = 256 b = 16 with absent off-diagonal blocks and an empty
+    block-row tail; n = 512 b = 32 on the register SpMV (SPAMM_SPMV_BLK=0, E = 4 lanes)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "import paper_1508_05856_b200 as sp, spamm_inputs as si, torch\n"
+            "from test_gpu_parity import decaying\n"
+            "ctx = sp.spamm_ctx_create(0); case = %r\n"
+            "if case == 'C1':\n"
+            "    c = si.CONFIGS['C1']; kind, p = si.make_input(c); n, b = c.n, c.b\n"
+            "    m = p if kind == 'dense' else None\n"
+            "    S = (sp.spamm_build_tree(ctx, torch.from_numpy(p).cuda(), b) if kind == 'dense' else\n"
+            "         sp.spamm_build_tree_blocks(ctx, n, b, *(torch.from_numpy(x).cuda() for x in p)))\n"
+            "else:\n"
+            "    n, b = (256, 16) if case == 'b16_holes' else (512, 32)\n"
+            "    m = np.abs(decaying(n, 0.02, 5)); m = m + m.T\n"
+            "    if case == 'b16_holes':\n"
+            "        r = np.random.default_rng(4)\n"
+            "        for I in range(n // b):\n"
+            "            for J in range(I + 1, n // b):\n"
+            "                if r.random() < 0.4: m[I*b:(I+1)*b, J*b:(J+1)*b] = 0; m[J*b:(J+1)*b, I*b:(I+1)*b] = 0\n"
+            "        m[n - b:, :] = 0; m[:, n - b:] = 0\n"
+            "    S = sp.spamm_build_tree(ctx, torch.from_numpy(m).cuda(), b)\n"
+            "print(repr(sp.spamm_power_scale(ctx, S, 100)))\n")
+    out = []
+    for mode in ("1", "0"):
+        env = {**os.environ, "SPAMM_POWER_CLUSTER": mode}
+        if case == "b32_reg":
+            env["SPAMM_SPMV_BLK"] = "0"
+        p = subprocess.run([sys.executable, "-c", code % (root, os.path.join(root, "tests"), case)],
+                           capture_output=True, text=True, timeout=600, env=env)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out.append(p.stdout.strip().splitlines()[-1])
+    assert out[0] == out[1], out
+    if case != "C1":
+        n, b = (256, 16) if case == "b16_holes" else (512, 32)
+        m = np.abs(decaying(n, 0.02, 5))
+        m = m + m.T
+        if case == "b16_holes":
+            r = np.random.default_rng(4)
+            for I in range(n // b):
+                for J in range(I + 1, n // b):
+                    if r.random() < 0.4:
+                        m[I * b:(I + 1) * b, J * b:(J + 1) * b] = 0
+                        m[J * b:(J + 1) * b, I * b:(I + 1) * b] = 0
+            m[n - b:, :] = 0
+            m[:, n - b:] = 0
+        assert float(out[0]) == pytest.approx(O.power_scale(O.OMat.from_dense(m, b), 100), rel=1e-12)
