@@ -48,8 +48,9 @@ out = dict(kernel=f"k_leaf_gemm<64,...> ({cfg}, NS iteration k={k}: X, Y', Z' la
            bytes_per_launch=sum(x["dram_total"] for x in launches) / 3,
            flops_per_launch=sum(x["flops"] for x in launches) / 3,
            source=cmd, launches=launches,
-           note="dram read ~= the compulsory unique operand blocks; write = the output blocks; "
-                "the operand stream is served from L2")
+           note="dram write = the output blocks; dram read = the unique operand blocks plus what L2 "
+                "(126 MB) cannot hold of the operand stream (C3: ~compulsory; C5 Y': ~1.8x the "
+                "unique blocks, DESIGN.md section 5)")
 json.dump(out, open(os.path.join("profiles", f"gemm_traffic_{cfg}.json"), "w"), indent=1)
 json.dump(r, open(os.path.join("profiles", os.environ.get("SPAMM_ROUND", "r02"), f"gemm_{cfg}_k{k}_full.json"), "w"), indent=1)
 for x in launches:
